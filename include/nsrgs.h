@@ -1,0 +1,179 @@
+/*
+ * nsrgs.h — C-ABI of the B200-native NS-RGS hot path (libnsrgs.so).
+ *
+ * NS-RGS = "Newton-Schulz based Riemannian Gradient Scheme" for orthogonal group
+ * synchronization, arxiv 2604.07372.  Citations "PAPER.md:L" are lines of the
+ * paper's LaTeX source, with the section / equation / algorithm they fall in.
+ *
+ * Problem (PAPER.md:192-194 Eq. def:f problem, :232-235 Alg. 2 "Input"): given the
+ * symmetric block measurement matrix A = [A_ij] in R^{nd x nd} with A_ii = 0
+ * (PAPER.md:225-230 Eq. def:measurements), estimate X = (X_1; ...; X_n), X_i in O(d),
+ * minimising F(X) = sum_{i != j} 1/2 ||X_i X_j^T - A_ij||_F^2.
+ *
+ * Conventions (all entry points):
+ *  - Every call returns an nsrgs_status; 0 = success.  On failure the context keeps a
+ *    message readable with nsrgs_last_error().  No call aborts the process.
+ *  - Calls are SYNCHRONOUS with respect to the context's CUDA stream: they return after the
+ *    device work they enqueue has completed (so device-side error words can be reported).
+ *  - Multi-GPU (world > 1): one context per process/GPU; every call except
+ *    nsrgs_plan / nsrgs_get_nccl_unique_id / nsrgs_last_error / nsrgs_version is
+ *    COLLECTIVE — all ranks must make the same sequence of calls with the same scalar
+ *    arguments (NCCL semantics).  A is row-block sharded by node: rank g owns nodes
+ *    [g n/world, (g+1) n/world), i.e. A rows [g N/world, (g+1) N/world), N = n d, all N
+ *    columns.  X is replicated on every rank.
+ *  - Matrices are row-major.  "block stack" = n blocks of d x d, block i at offset i*d*d,
+ *    i.e. the nd x d matrix (X_1; ...; X_n) of PAPER.md:128 (§1.4) in row-major order.
+ *  - Element type of every matrix argument = the context dtype (float or double).
+ *  - Pointers marked "host" are host memory (pinned or pageable); "device" are CUDA device
+ *    pointers on the context's device.  The library never frees caller memory.
+ *  - Update rule: Jacobi — every block of X^{t+1} is computed from X^t.
+ */
+#ifndef NSRGS_H
+#define NSRGS_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NSRGS_VERSION 1
+
+typedef struct nsrgs_ctx nsrgs_ctx; /* opaque; one per (process, GPU) */
+
+typedef enum {
+  NSRGS_OK = 0,
+  NSRGS_ERR_INVALID_ARG = 1,       /* bad size / pointer / unsupported (d, dtype) combination   */
+  NSRGS_ERR_STATE = 2,             /* call out of order (e.g. step before A or X is set)        */
+  NSRGS_ERR_CUDA = 3,              /* CUDA runtime/driver error (message has cudaGetErrorString) */
+  NSRGS_ERR_NCCL = 4,              /* NCCL error or NCCL library not loadable                    */
+  NSRGS_ERR_OOM = 5,               /* device allocation failed                                  */
+  NSRGS_ERR_DIVERGENCE = 6,        /* retraction left the NS region: non-finite X or
+                                      ||S||_F > 10 sqrt(d) after Algorithm 1       */
+  NSRGS_ERR_SINGULAR = 7,          /* init polar sgn(Y_i) did not converge: sigma_min(Y_i) ~ 0
+                                      (PAPER.md:141 needs full rank), or Cholesky of Y^T Y failed */
+  NSRGS_ERR_EIG_NOT_CONVERGED = 8, /* spectral subspace iteration hit max_sweeps above tol      */
+  NSRGS_ERR_NONFINITE = 9          /* objective / metric evaluated to NaN or Inf                */
+} nsrgs_status;
+
+typedef enum { NSRGS_F32 = 0, NSRGS_F64 = 1 } nsrgs_dtype;
+
+/* Context description. */
+typedef struct {
+  int64_t n;                    /* number of nodes (group elements), n >= 2                     */
+  int32_t d;                    /* block size; supported: 2..10 (F32), 2..6 (F64)               */
+  int32_t dtype;                /* nsrgs_dtype: storage + arithmetic type of A, X (fp64 partials) */
+  int32_t rank, world;          /* world >= 1, 0 <= rank < world, n % world == 0; for world > 1
+                                   also (n/world)*d*sizeof(dtype) % 16 == 0 (TMA row-segment
+                                   alignment of the per-rank column slices)                      */
+  int32_t device;               /* CUDA device ordinal the context binds to                      */
+  const void *nccl_unique_id;   /* host, 128 bytes from nsrgs_get_nccl_unique_id() on rank 0,
+                                   broadcast by the caller; must be NULL iff world == 1          */
+  void *cuda_stream;            /* cudaStream_t to enqueue on; NULL = library-created stream    */
+} nsrgs_desc;
+
+/* Static sharding plan (pure host arithmetic; callable without a GPU). */
+typedef struct {
+  int64_t n_local;      /* nodes owned by this rank = n / world                               */
+  int64_t node0;        /* first owned node = rank * n_local                                  */
+  int64_t rows_local;   /* A rows owned = n_local * d (also the width of one rank's X slice)  */
+  int64_t row0;         /* first owned A row = node0 * d                                      */
+  int64_t col_tile;     /* X/A column tile width (elements) of the device layout = 128        */
+  int64_t tiles_per_rank; /* ceil(rows_local / col_tile)                                       */
+  int64_t x_elems;      /* elements of one device X buffer = world*tiles_per_rank*d*col_tile  */
+  int64_t x_slice_elems;/* elements of one rank's contiguous X slice (NCCL all-gather count)  */
+} nsrgs_plan_t;
+
+int nsrgs_version(void);
+
+/* Pure host: the sharding plan of (n, d, world, rank).  Returns INVALID_ARG if the
+ * combination is not supported.  Device X layout ("tile layout"): element
+ * (row c of the nd x d stack, component k) lives at
+ *   ((g * tiles_per_rank + j) * d + k) * col_tile + o,  g = c / rows_local,
+ *   j = (c % rows_local) / col_tile, o = (c % rows_local) % col_tile;
+ * padding entries are zero.  */
+int nsrgs_plan(int64_t n, int32_t d, int32_t world, int32_t rank, nsrgs_plan_t *out);
+
+/* Pure host: convert between the nd x d row-major stack and the tile layout above
+ * (host buffers, element type by dtype).  Used by tests of the sharded layout. */
+int nsrgs_pack_host(int64_t n, int32_t d, int32_t world, int32_t dtype, const void *stack, void *tiled);
+int nsrgs_unpack_host(int64_t n, int32_t d, int32_t world, int32_t dtype, const void *tiled, void *stack);
+
+/* Rank 0 only: create an NCCL unique id (128 bytes, host) to broadcast to all ranks. */
+int nsrgs_get_nccl_unique_id(void *out128);
+
+/* Create / destroy a context.  Allocates the library-owned X buffers (2 x x_elems), partial
+ * buffers and (world > 1) the NCCL communicator.  *out is NULL on failure. */
+int nsrgs_create(const nsrgs_desc *desc, nsrgs_ctx **out);
+int nsrgs_destroy(nsrgs_ctx *ctx);
+const char *nsrgs_last_error(const nsrgs_ctx *ctx); /* never NULL; "" if no error */
+
+/* Use a caller-owned A shard: device pointer to rows_local x (n d) elements, row stride lda
+ * (elements, lda >= n d, lda*sizeof(dtype) % 16 == 0, pointer 16-byte aligned).  BORROWED:
+ * read-only, must outlive the context (or the next attach/generate).  The diagonal blocks
+ * A_ii of the owned rows must be zero; the library does not check symmetry.
+ * Computes ||A||_F^2 (fp64, all-reduced) for the objective.  (Alg. 2 Input.) */
+int nsrgs_attach_A(nsrgs_ctx *ctx, const void *A_shard_dev, int64_t lda);
+
+/* Generate the synthetic instance of PAPER.md:59-66 / :225-230 on the device (library-OWNED
+ * A shard; no host traffic): Z_i = Q of QR(G_i) with diag(R) > 0, G_i Gaussian from Philox
+ * counter (i,0,q,1); W_ij (i<j) from counter (i,j,q,2); A_ij = round(Z_i Z_j^T + sigma W_ij),
+ * A_ji = A_ij^T, A_ii = 0.  Each rank generates only its
+ * own rows; the instance is independent of world.  Z_out: host, n*d*d elements of dtype,
+ * nullable — receives the ground truth.  sigma >= 0. */
+int nsrgs_generate(nsrgs_ctx *ctx, uint64_t seed, double sigma, void *Z_out_host);
+
+/* Copy rows [row0, row0+nrows) of THIS rank's A shard (local row index) to host `out`
+ * (nrows x n d, dense).  Diagnostic / sampled-parity helper. */
+int nsrgs_copy_A_rows(nsrgs_ctx *ctx, int64_t row0, int64_t nrows, void *out_host);
+
+/* Spectral initialisation (Alg. 2): Y = top-d eigenvectors of A
+ * by subspace iteration Y <- A Y (the same panel A.X kernel as nsrgs_step) with Cholesky-QR,
+ * Y_0 Gaussian from Philox counter (r,0,q,3), stopped when ||Y_new - Y_old(Y_old^T Y_new)||_F
+ * < tol or after max_sweeps; then X^0 = sgn(Y) blockwise by scaled Newton-Schulz (no SVD).
+ * Sets the current iterate.  sweeps_used: host, nullable.  Returns
+ * NSRGS_ERR_EIG_NOT_CONVERGED (X^0 still set) if tol was not reached. */
+int nsrgs_init_spectral(nsrgs_ctx *ctx, uint64_t seed, int max_sweeps, double tol, int *sweeps_used);
+
+/* One NS-RGS iteration t -> t+1 of Algorithm 2:
+ *   G_i = sum_{j!=i}(X_i - A_ij X_j),  F_i = X_i - eta P_{T_{X_i}}(G_i),  X_i <- S(F_i),
+ * P_T(G) = (G - X G^T X)/2, S = K steps of Algorithm 1.
+ * eta > 0 (paper: mu = 1/n); K >= 0.  objective_before: host, nullable —
+ * receives F(X^t) computed from fp64 partials fused into the same A pass. */
+int nsrgs_step(nsrgs_ctx *ctx, double eta, int K, double *objective_before);
+
+/* T iterations of nsrgs_step.  objective_trace: host, nullable, length T, receives
+ * F(X^0..X^{T-1}).  Returns NSRGS_ERR_DIVERGENCE if any iteration left the NS region. */
+int nsrgs_run(nsrgs_ctx *ctx, int T, double eta, int K, double *objective_trace);
+
+/* F(X) of the current iterate (PAPER.md:70-72 Eq. def:f); one A pass. */
+int nsrgs_objective(nsrgs_ctx *ctx, double *F_out);
+
+/* Recovery metrics of the current iterate against ground truth Z (n*d*d elements of dtype,
+ * host if Z_on_device == 0 else device): out[0] = Rel.Err. = ||ZZ^T - XX^T||_F/||ZZ^T||_F
+ * (PAPER.md:314-317), out[1] = d_F(X, Z) = min_Q ||X - ZQ||_F via
+ * ||X||^2 + ||Z||^2 - 2||Z^T X||_* (PAPER.md:633-637), out[2] = MSE = d_F^2/n
+ * (PAPER.md:369-372).  fp64 Grams on the device. */
+int nsrgs_alignment_error(nsrgs_ctx *ctx, const void *Z, int Z_on_device, double out[3]);
+
+/* Set / get the full current iterate X (n*d*d elements, block stack).  host if on_device==0. */
+int nsrgs_set_X(nsrgs_ctx *ctx, const void *X, int on_device);
+int nsrgs_get_X(nsrgs_ctx *ctx, void *X, int on_device);
+
+/* Launch configuration + measurement hooks (bench / tests).  */
+typedef struct {
+  int32_t grid, threads, stages, rows_per_panel, splits;   /* panel kernel launch shape      */
+  int64_t panels, smem_bytes;
+  double panel_ms_total;        /* summed CUDA-event time of panel kernel launches since reset */
+  int64_t panel_launches;       /* number of panel kernel launches since reset                 */
+  int64_t kernel_launches;      /* all library kernel launches since reset                     */
+  double ns_region_max;         /* max over nodes of ||I - F_i^T F_i||_F seen since reset        */
+  double a_fro2;                /* ||A||_F^2 (global)                                           */
+} nsrgs_stats_t;
+int nsrgs_get_stats(nsrgs_ctx *ctx, nsrgs_stats_t *out);
+int nsrgs_reset_stats(nsrgs_ctx *ctx, int enable_panel_timing);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NSRGS_H */

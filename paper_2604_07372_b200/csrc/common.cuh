@@ -1,0 +1,145 @@
+// common.cuh — device helpers shared by the libnsrgs kernels (PTX wrappers for mbarrier,
+// TMA / bulk copies, L2 policies; the Philox4x32-10 counter RNG; the X tile layout).
+// Nothing here is shared with oracle/ (the oracle re-implements the generator in NumPy).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace nsrgs {
+
+constexpr int kColTile = 128;      // X/A column tile (elements); one float4/double4 per lane
+constexpr int kWarps = 7;          // consumer warps per panel CTA (7 + producer = 8 warps: 2 per SMSP, 255 regs)
+constexpr int kThreads = 32 * (kWarps + 1);   // + 1 TMA producer warp
+
+// ------------------------------------------------------------------------------------------
+// Launch parameters of the panel kernel (panel.cu).  Plain struct, passed by value.
+struct PanelParams {
+  const void *X;        // tile layout, input iterate X^t (or Y for the subspace sweep)
+  void *Xout;           // tile layout, output X^{t+1} (RGS) or W = A Y (PRODUCT)
+  void *Bpart;          // split-K partials [unit][rows_per_panel][d] (splits > 1)
+  unsigned *panel_cnt;  // split-K arrival counters [panels]
+  double *cta_part;     // per-CTA fp64 partials [grid][npart]
+  unsigned *done_cnt;   // CTA arrival counter for the last-CTA reduction
+  double *result;       // npart doubles: reduced partials of this launch
+  int *err;             // device error word (bit flags, see kErr*)
+  unsigned *ns_region;  // float bits of max ||I - F^T F||_F (atomicMax on non-negative floats)
+  int64_t n;            // total nodes
+  int64_t n_local, node0, rows_local;
+  int64_t tiles_per_rank;
+  int world, rank;
+  int panels, splits, tiles_per_split, total_tiles, units;
+  double coef;          // n - 1   (identity term of G_i)
+  double eta;           // step size mu
+  int K;                // Newton-Schulz steps (Algorithm 1)
+};
+
+constexpr int kErrDivergence = 1;   // ||S||_F > 10 sqrt(d) or non-finite after NS
+constexpr int kErrSingular = 2;     // init polar did not converge / Cholesky failed
+constexpr int kErrNonfinite = 4;
+
+// Element of the tile layout for stack row c (0 <= c < N) and component k.
+__host__ __device__ inline int64_t tile_index(int64_t c, int k, int d, int64_t rows_local,
+                                              int64_t tiles_per_rank) {
+  int64_t g = c / rows_local, cl = c - g * rows_local;
+  int64_t j = cl / kColTile, o = cl - j * kColTile;
+  return ((g * tiles_per_rank + j) * d + k) * kColTile + o;
+}
+
+// ------------------------------------------------------------------------------------------
+// Philox4x32-10 (Salmon et al., SC'11).  Same definition as oracle/instance.py, written
+// independently.
+struct U4 { uint32_t x, y, z, w; };
+__device__ __forceinline__ U4 philox4x32_10(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
+                                            uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    if (r > 0) { k0 += 0x9E3779B9u; k1 += 0xBB67AE85u; }
+    uint32_t lo0 = 0xD2511F53u * c0, hi0 = __umulhi(0xD2511F53u, c0);
+    uint32_t lo1 = 0xCD9E8D57u * c2, hi1 = __umulhi(0xCD9E8D57u, c2);
+    uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+    c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
+  }
+  return {c0, c1, c2, c3};
+}
+__device__ __forceinline__ double uniform53(uint32_t a, uint32_t b) {
+  uint64_t m = (uint64_t)(a >> 5) * 67108864ull + (uint64_t)(b >> 6);
+  return ((double)m + 1.0) * 1.1102230246251565404236316680908203125e-16;   // 2^-53
+}
+// Normals 2q and 2q+1 of the stream (c0, c1, *, tag): Box-Muller on the two uniforms.
+__device__ __forceinline__ void normal_pair(uint64_t seed, uint32_t c0, uint32_t c1, uint32_t q,
+                                            uint32_t tag, double &z0, double &z1) {
+  U4 v = philox4x32_10(c0, c1, q, tag, (uint32_t)(seed & 0xffffffffu), (uint32_t)(seed >> 32));
+  double u1 = uniform53(v.x, v.y), u2 = uniform53(v.z, v.w);
+  double r = sqrt(-2.0 * log(u1));
+  double th = (2.0 * 3.141592653589793) * u2;
+  double s, c;
+  sincos(th, &s, &c);
+  z0 = r * c;
+  z1 = r * s;
+}
+
+// ------------------------------------------------------------------------------------------
+// PTX wrappers (sm_90+/sm_100a): mbarrier, TMA tensor + bulk copies, L2 cache policies.
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}" ::"r"(addr), "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void tma_load_3d(void *smem_dst, const void *tmap, uint64_t *bar, int c0,
+                                            int c1, int c2, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_load(void *smem_dst, const void *gsrc, uint32_t bytes, uint64_t *bar,
+                                          uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(smem_dst)),
+      "l"(gsrc), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ void prefetch_tmap(const void *tmap) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tmap)) : "memory");
+}
+__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+template <typename T> struct Vec4;
+template <> struct Vec4<float> { using type = float4; };
+template <> struct Vec4<double> { using type = double4; };
+
+}  // namespace nsrgs

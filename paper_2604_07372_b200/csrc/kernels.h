@@ -1,0 +1,44 @@
+// kernels.h — host-visible entry points of the device code (internal to libnsrgs.so).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace nsrgs {
+
+enum PanelMode { kModeRgs = 0, kModeObjective = 1, kModeProduct = 2 };
+
+struct PanelShape {
+  int rows, nodes, stages, smem, npart, threads;
+};
+
+// panel.cu: shape query (shape_only) or launch of the fused A.X + epilogue kernel.
+cudaError_t panel_dispatch(int dtype, int d, int mode, bool shape_only, PanelShape *shape,
+                           const CUtensorMap *tm, const PanelParams *p, int grid, cudaStream_t s);
+
+// aux.cu
+cudaError_t launch_gen_Z(int dtype, int d, int64_t n, uint64_t seed, double *Z64, void *Zt, cudaStream_t s);
+cudaError_t launch_gen_A(int dtype, int d, int64_t n, int64_t node0, int64_t n_local, uint64_t seed,
+                         double sigma, const double *Z64, void *A, int64_t lda, double *part,
+                         int *nblocks, cudaStream_t s);
+cudaError_t launch_gen_Y0(int dtype, int d, int64_t n, uint64_t seed, void *Y, int64_t rows_local,
+                          int64_t tiles_per_rank, cudaStream_t s);
+cudaError_t launch_sumsq(int dtype, const void *A, int64_t rows, int64_t cols, int64_t lda, double *part,
+                         int *nblocks, cudaStream_t s);
+cudaError_t launch_reduce(const double *part, int nblocks, int width, double *out, cudaStream_t s);
+cudaError_t launch_pack(int dtype, int d, int64_t n, const void *stack, void *tiled, int64_t rows_local,
+                        int64_t tiles_per_rank, int unpack, cudaStream_t s);
+cudaError_t launch_chol(int d, const double *res, double *MC, int *err, cudaStream_t s);
+cudaError_t launch_scale(int dtype, int d, int64_t node0, int64_t n_local, const double *MC, void *W,
+                         const void *Yold, int64_t rows_local, int64_t tiles_per_rank, double *part,
+                         int *nblocks, cudaStream_t s);
+cudaError_t launch_polar(int dtype, int d, int64_t n, const void *Y, void *X, int64_t rows_local,
+                         int64_t tiles_per_rank, int *err, cudaStream_t s);
+cudaError_t launch_objective_final(int d, int T, const double *res, int npart, const double *a_fro2,
+                                   double *F, cudaStream_t s);
+cudaError_t launch_metrics(int dtype, int d, int64_t n, const void *X, const void *Z, int64_t rows_local,
+                           int64_t tiles_per_rank, double *part, int *nblocks, cudaStream_t s);
+cudaError_t launch_metrics_final(int d, int64_t n, const double *grams, double *out3, cudaStream_t s);
+
+}  // namespace nsrgs

@@ -1,0 +1,493 @@
+// panel.cu — the NS-RGS hot path: one streaming pass of the A shard per launch.
+//
+//   B = A_shard . X            (Alg. 2 "G_i^t = sum_{j!=i}(X_i^t - A_ij X_j^t)")
+//   G_i = (n-1) X_i - B_i      (A_ii = 0)
+//   P_i = (G_i - X_i G_i^T X_i)/2,  F_i = X_i - eta P_i
+//   X_i^{t+1} = S(F_i): K steps S <- 1/2 S (3I - S^T S)
+//
+// Design: persistent grid, one CTA per SM, 8 consumer warps + 1 TMA
+// producer warp.  Work unit = (row panel of ROWS = 8*RT rows, column split).  The producer
+// streams A tiles (ROWS x 128, 3-D tensor map over (col-in-rank-slice, rank slice, row)) and
+// the matching X tile (d x 128, contiguous in the tile layout) into an mbarrier ring with an
+// L2 evict-first policy on A and evict-last on X.  Each consumer warp owns RT rows (= whole
+// nodes); lane l owns columns 4l..4l+3 of every tile and keeps RT x d fp32 accumulators in
+// registers, so every X value read from smem is reused RT times and A is read from smem once
+// with conflict-free 128-bit loads.  At the end of a panel the warp reduces its accumulators
+// with shuffles and runs the per-node epilogue entry-parallel in warp-private smem; no B is
+// ever written to HBM.  fp64 partials for the objective / Gram matrices are reduced
+// deterministically (fixed order, last-CTA pattern).
+#include <cuda.h>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace nsrgs {
+
+template <typename T, int D>
+struct PanelCfg {
+  static constexpr int RT = (sizeof(T) == 4)
+                                ? (D == 2 ? 12 : D == 3 ? 12 : D == 4 ? 12 : D == 5 ? 10 : D == 6 ? 12
+                                   : D == 7 ? 14 : D == 8 ? 8 : D == 9 ? 9 : 10)
+                                : (D == 2 ? 6 : D == 3 ? 6 : D == 4 ? 4 : D == 5 ? 5 : 6);
+  static_assert(RT % D == 0, "warp rows must be whole nodes");
+  static constexpr int NPW = RT / D;
+  static constexpr int ROWS = RT * kWarps;
+  static constexpr int NODES = ROWS / D;
+  static constexpr int A_BYTES = ROWS * kColTile * (int)sizeof(T);
+  static constexpr int X_BYTES = D * kColTile * (int)sizeof(T);
+  static constexpr int STAGE_BYTES = A_BYTES + X_BYTES;
+  static constexpr int E = NPW * D * D;          // epilogue entries per warp
+  static constexpr int EPL = (E + 31) / 32;      // entries per lane
+  static constexpr int DD = D * D;
+  static constexpr int DDL = (DD + 31) / 32;     // Gram entries per lane
+  static constexpr int NPART = 2 * DD + 2;
+  // shared memory after the stages
+  static constexpr int BAR_BYTES = 2 * 8 * 8;                         // up to 8 stages
+  static constexpr int SCR_T = 5 * E;                                 // sX sG sH sS sM
+  static constexpr int SCR_BYTES = kWarps * (SCR_T * (int)sizeof(T)) + kWarps * 2 * DD * 8 + kWarps * 2 * 8 + 64;
+  static constexpr int BUDGET = 220 * 1024;
+  static constexpr int STAGES_RAW = (BUDGET - 1024 - BAR_BYTES - SCR_BYTES) / STAGE_BYTES;
+  static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
+  static_assert(STAGES >= 2, "need a double-buffered ring");
+  static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + BAR_BYTES + SCR_BYTES;
+};
+
+template <typename T> __device__ __forceinline__ T tfma(T a, T b, T c) { return fma(a, b, c); }
+
+template <typename T> __device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+template <typename T, int D, int MODE>
+__global__ void __launch_bounds__(kThreads, 1)
+    panel_kernel(const __grid_constant__ CUtensorMap tmA, const PanelParams p) {
+  using C = PanelCfg<T, D>;
+  using V = typename Vec4<T>::type;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t *empty = full + 8;
+  T *scr_all = reinterpret_cast<T *>(smem + C::STAGES * C::STAGE_BYTES + C::BAR_BYTES);
+  double *gram_all = reinterpret_cast<double *>(reinterpret_cast<uint8_t *>(scr_all) + kWarps * C::SCR_T * sizeof(T));
+  double *red = gram_all + kWarps * 2 * C::DD;       // [kWarps][2]
+  int *flag = reinterpret_cast<int *>(red + kWarps * 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kWarps);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  const T *Xg = static_cast<const T *>(p.X);
+
+  // ------------------------------------------------------------------ producer warp
+  if (warp == kWarps) {
+    if (lane == 0) {
+      prefetch_tmap(&tmA);
+      const uint64_t pol_a = policy_evict_first(), pol_x = policy_evict_last();
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+        const int panel = u / p.splits, split = u - panel * p.splits;
+        const int t0 = split * p.tiles_per_split;
+        const int t1 = min(p.total_tiles, t0 + p.tiles_per_split);
+        const int row0 = panel * C::ROWS;
+        for (int t = t0; t < t1; ++t) {
+          const int g = t / (int)p.tiles_per_rank, jt = t - g * (int)p.tiles_per_rank;
+          mbar_wait(&empty[stage], phase ^ 1u);
+          uint8_t *sb = smem + stage * C::STAGE_BYTES;
+          mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
+          tma_load_3d(sb, &tmA, &full[stage], jt * kColTile, g, row0, pol_a);
+          bulk_load(sb + C::A_BYTES, Xg + (int64_t)t * D * kColTile, C::X_BYTES, &full[stage], pol_x);
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1u; }
+        }
+      }
+    }
+    return;
+  }
+
+  // ------------------------------------------------------------------ consumer warps
+  T *sX = scr_all + warp * C::SCR_T;
+  T *sG = sX + C::E;
+  T *sH = sG + C::E;
+  T *sS = sH + C::E;
+  T *sM = sS + C::E;
+  double *gram1 = gram_all + warp * 2 * C::DD;
+  double *gram2 = gram1 + C::DD;
+#pragma unroll
+  for (int m = 0; m < C::DDL; ++m) {
+    const int e = lane + 32 * m;
+    if (e < C::DD) { gram1[e] = 0.0; gram2[e] = 0.0; }
+  }
+  double s_own = 0.0, xb = 0.0;     // sum_i ||X_i^T X_i||^2, <X, B>
+  float ns_region = 0.f;
+  int err = 0;
+  const T coef = (T)p.coef, eta = (T)p.eta;
+
+  int stage = 0;
+  uint32_t phase = 0;
+  for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+    const int panel = u / p.splits, split = u - panel * p.splits;
+    const int t0 = split * p.tiles_per_split;
+    const int t1 = min(p.total_tiles, t0 + p.tiles_per_split);
+
+    T acc[C::RT][D];
+#pragma unroll
+    for (int r = 0; r < C::RT; ++r)
+#pragma unroll
+      for (int k = 0; k < D; ++k) acc[r][k] = T(0);
+
+    for (int t = t0; t < t1; ++t) {
+      mbar_wait(&full[stage], phase);
+      const T *As = reinterpret_cast<const T *>(smem + stage * C::STAGE_BYTES) + (warp * C::RT) * kColTile + lane * 4;
+      const T *Xs = reinterpret_cast<const T *>(smem + stage * C::STAGE_BYTES + C::A_BYTES) + lane * 4;
+      V xv[D];
+#pragma unroll
+      for (int k = 0; k < D; ++k) xv[k] = *reinterpret_cast<const V *>(Xs + k * kColTile);
+#pragma unroll
+      for (int r = 0; r < C::RT; ++r) {
+        const V a = *reinterpret_cast<const V *>(As + r * kColTile);
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+          T v = acc[r][k];
+          v = tfma(a.x, xv[k].x, v);
+          v = tfma(a.y, xv[k].y, v);
+          v = tfma(a.z, xv[k].z, v);
+          v = tfma(a.w, xv[k].w, v);
+          acc[r][k] = v;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[stage]);
+      if (++stage == C::STAGES) { stage = 0; phase ^= 1u; }
+    }
+
+    // ---- reduce the lane-partial sums: every lane ends with the full B rows of the warp
+#pragma unroll
+    for (int r = 0; r < C::RT; ++r)
+#pragma unroll
+      for (int k = 0; k < D; ++k) acc[r][k] = warp_sum(acc[r][k]);
+
+    if (p.splits > 1) {
+      T *bp = static_cast<T *>(p.Bpart) + ((int64_t)u * C::ROWS + warp * C::RT) * D;
+#pragma unroll
+      for (int r = 0; r < C::RT; ++r)
+#pragma unroll
+        for (int k = 0; k < D; ++k)
+          if (((r * D + k) & 31) == lane) __stcg(bp + r * D + k, acc[r][k]);
+      __threadfence();
+      named_bar_sync(1, kWarps * 32);
+      if (threadIdx.x == 0) {
+        const unsigned prev = atomicAdd(&p.panel_cnt[panel], 1u);
+        *flag = (prev == (unsigned)(p.splits - 1));
+      }
+      named_bar_sync(1, kWarps * 32);
+      const int last = *flag;
+      named_bar_sync(1, kWarps * 32);   // everyone read flag before it is rewritten
+      if (!last) continue;
+      __threadfence();
+      if (threadIdx.x == 0) p.panel_cnt[panel] = 0u;   // ready for the next launch
+      const T *bq = static_cast<const T *>(p.Bpart) + ((int64_t)panel * p.splits * C::ROWS + warp * C::RT) * D;
+#pragma unroll
+      for (int m = 0; m < C::EPL; ++m) {
+        const int e = lane + 32 * m;
+        if (e < C::E) {
+          T v = T(0);
+          for (int s = 0; s < p.splits; ++s) v += __ldcg(bq + (int64_t)s * C::ROWS * D + e);
+          sG[e] = v;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int r = 0; r < C::RT; ++r)
+#pragma unroll
+        for (int k = 0; k < D; ++k)
+          if (((r * D + k) & 31) == lane) sG[r * D + k] = acc[r][k];
+    }
+
+    // ---- per-node epilogue, entry-parallel in warp-private smem.
+    // Entry e = (q, a, b): node q of the warp, row a, column b; flat index e = (q*D + a)*D + b,
+    // which equals the accumulator index r*D + k with r = q*D + a (row of the panel), k = b.
+    const int64_t node_base = (int64_t)panel * C::NODES + warp * C::NPW;   // local node of q = 0
+    const int64_t rem = p.n_local - node_base;
+    const int nvalid = rem <= 0 ? 0 : (rem < C::NPW ? (int)rem : C::NPW);
+#pragma unroll
+    for (int m = 0; m < C::EPL; ++m) {
+      const int e = lane + 32 * m;
+      if (e < C::E) {
+        const int q = e / C::DD, a = (e / D) % D, b = e % D;
+        T x = T(0);
+        if (q < nvalid) {
+          const int64_t c = (p.node0 + node_base + q) * D + a;
+          x = Xg[tile_index(c, b, D, p.rows_local, p.tiles_per_rank)];
+        }
+        sX[e] = x;
+      }
+    }
+    __syncwarp();
+
+    if constexpr (MODE == kModeProduct) {
+      // W = A Y rows -> Xout; Gram partials W^T W and Y^T W (Cholesky-QR of the sweep).
+      T *Wout = static_cast<T *>(p.Xout);
+#pragma unroll
+      for (int m = 0; m < C::EPL; ++m) {
+        const int e = lane + 32 * m;
+        if (e < C::E) {
+          const int q = e / C::DD, a = (e / D) % D, b = e % D;
+          if (q < nvalid) {
+            const int64_t c = (p.node0 + node_base + q) * D + a;
+            Wout[tile_index(c, b, D, p.rows_local, p.tiles_per_rank)] = sG[e];
+          }
+        }
+      }
+#pragma unroll
+      for (int m = 0; m < C::DDL; ++m) {
+        const int e2 = lane + 32 * m;
+        if (e2 < C::DD) {
+          const int a = e2 / D, b = e2 % D;
+          double g1 = 0.0, g2 = 0.0;
+          for (int q = 0; q < nvalid; ++q)
+#pragma unroll
+            for (int k = 0; k < D; ++k) {
+              const double w_ka = (double)sG[(q * D + k) * D + a], w_kb = (double)sG[(q * D + k) * D + b];
+              g1 += w_ka * w_kb;
+              g2 += (double)sX[(q * D + k) * D + a] * w_kb;
+            }
+          gram1[e2] += g1;
+          gram2[e2] += g2;
+        }
+      }
+      __syncwarp();
+      continue;
+    } else {
+      // <X, B> and the X Gram terms of the objective expansion.
+#pragma unroll
+      for (int m = 0; m < C::EPL; ++m) {
+        const int e = lane + 32 * m;
+        if (e < C::E && e / C::DD < nvalid) xb += (double)sX[e] * (double)sG[e];
+      }
+#pragma unroll
+      for (int m = 0; m < C::DDL; ++m) {
+        const int e2 = lane + 32 * m;
+        if (e2 < C::DD) {
+          const int a = e2 / D, b = e2 % D;
+          double g1 = 0.0;
+          for (int q = 0; q < nvalid; ++q) {
+            double v = 0.0;
+#pragma unroll
+            for (int k = 0; k < D; ++k)
+              v += (double)sX[(q * D + k) * D + a] * (double)sX[(q * D + k) * D + b];
+            g1 += v;
+            s_own += v * v;
+          }
+          gram1[e2] += g1;
+        }
+      }
+      if constexpr (MODE == kModeObjective) {
+        __syncwarp();
+        continue;
+      }
+      // G = (n-1) X - B   (in place in sG)
+#pragma unroll
+      for (int m = 0; m < C::EPL; ++m) {
+        const int e = lane + 32 * m;
+        if (e < C::E) sG[e] = coef * sX[e] - sG[e];
+      }
+      __syncwarp();
+      // H = G^T X
+#pragma unroll
+      for (int m = 0; m < C::EPL; ++m) {
+        const int e = lane + 32 * m;
+        if (e < C::E) {
+          const int q = e / C::DD, a = (e / D) % D, b = e % D;
+          const T *Gq = sG + q * C::DD, *Xq = sX + q * C::DD;
+          T h = T(0);
+#pragma unroll
+          for (int k = 0; k < D; ++k) h = tfma(Gq[k * D + a], Xq[k * D + b], h);
+          sH[e] = h;
+        }
+      }
+      __syncwarp();
+      // P = (G - X H)/2,  F = X - eta P
+#pragma unroll
+      for (int m = 0; m < C::EPL; ++m) {
+        const int e = lane + 32 * m;
+        if (e < C::E) {
+          const int q = e / C::DD, a = (e / D) % D, b = e % D;
+          const T *Hq = sH + q * C::DD, *Xq = sX + q * C::DD;
+          T xh = T(0);
+#pragma unroll
+          for (int k = 0; k < D; ++k) xh = tfma(Xq[a * D + k], Hq[k * D + b], xh);
+          const T P = T(0.5) * (sG[e] - xh);
+          sS[e] = sX[e] - eta * P;
+        }
+      }
+      __syncwarp();
+      // Algorithm 1: K Newton-Schulz steps S <- 1/2 S (3I - S^T S) = 1.5 S - 0.5 S (S^T S)
+      for (int it = 0; it < p.K; ++it) {
+#pragma unroll
+        for (int m = 0; m < C::EPL; ++m) {
+          const int e = lane + 32 * m;
+          if (e < C::E) {
+            const int q = e / C::DD, a = (e / D) % D, b = e % D;
+            const T *Sq = sS + q * C::DD;
+            T v = T(0);
+#pragma unroll
+            for (int k = 0; k < D; ++k) v = tfma(Sq[k * D + a], Sq[k * D + b], v);
+            sM[e] = v;
+          }
+        }
+        __syncwarp();
+        if (it == 0 && lane < nvalid) {   // ||I - F^T F||_F of node `lane` (PAPER.md:465 eq:conclusion:sigma)
+          const T *Mq = sM + lane * C::DD;
+          float acc2 = 0.f;
+          for (int e2 = 0; e2 < C::DD; ++e2) {
+            const float dv = (float)((e2 / D == e2 % D ? T(1) : T(0)) - Mq[e2]);
+            acc2 += dv * dv;
+          }
+          ns_region = fmaxf(ns_region, sqrtf(acc2));
+        }
+        T snew[C::EPL];
+#pragma unroll
+        for (int m = 0; m < C::EPL; ++m) {
+          const int e = lane + 32 * m;
+          snew[m] = T(0);
+          if (e < C::E) {
+            const int q = e / C::DD, a = (e / D) % D, b = e % D;
+            const T *Sq = sS + q * C::DD, *Mq = sM + q * C::DD;
+            T v = T(0);
+#pragma unroll
+            for (int k = 0; k < D; ++k) v = tfma(Sq[a * D + k], Mq[k * D + b], v);
+            snew[m] = T(1.5) * sS[e] - T(0.5) * v;
+          }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int m = 0; m < C::EPL; ++m) {
+          const int e = lane + 32 * m;
+          if (e < C::E) sS[e] = snew[m];
+        }
+        __syncwarp();
+      }
+      // divergence guard: non-finite or ||S||_F > 10 sqrt(d)
+      if (lane < nvalid) {
+        const T *Sq = sS + lane * C::DD;
+        double f2 = 0.0;
+        for (int e2 = 0; e2 < C::DD; ++e2) f2 += (double)Sq[e2] * (double)Sq[e2];
+        if (!(f2 <= 100.0 * D)) err |= kErrDivergence;
+      }
+      T *Xo = static_cast<T *>(p.Xout);
+#pragma unroll
+      for (int m = 0; m < C::EPL; ++m) {
+        const int e = lane + 32 * m;
+        if (e < C::E) {
+          const int q = e / C::DD, a = (e / D) % D, b = e % D;
+          if (q < nvalid) {
+            const int64_t c = (p.node0 + node_base + q) * D + a;
+            Xo[tile_index(c, b, D, p.rows_local, p.tiles_per_rank)] = sS[e];
+          }
+        }
+      }
+      __syncwarp();
+    }
+  }
+
+  // ------------------------------------------------------------------ CTA + grid reduction
+  if (err) atomicOr(p.err, err);
+  if (MODE == kModeRgs) {
+    float mx = ns_region;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 0 && mx > 0.f) atomicMax(p.ns_region, __float_as_uint(mx));
+  }
+  s_own = warp_sum(s_own);
+  xb = warp_sum(xb);
+  if (lane == 0) { red[warp * 2] = s_own; red[warp * 2 + 1] = xb; }
+  named_bar_sync(1, kWarps * 32);
+  double *cp = p.cta_part + (int64_t)blockIdx.x * C::NPART;
+  for (int i = threadIdx.x; i < C::NPART; i += kWarps * 32) {
+    double v = 0.0;
+    if (i < 2 * C::DD) {
+      for (int w = 0; w < kWarps; ++w) v += gram_all[w * 2 * C::DD + i];
+    } else {
+      for (int w = 0; w < kWarps; ++w) v += red[w * 2 + (i - 2 * C::DD)];
+    }
+    __stcg(cp + i, v);
+  }
+  __threadfence();
+  named_bar_sync(1, kWarps * 32);
+  if (threadIdx.x == 0) *flag = (atomicAdd(p.done_cnt, 1u) == gridDim.x - 1);
+  named_bar_sync(1, kWarps * 32);
+  if (*flag) {
+    __threadfence();
+    for (int i = threadIdx.x; i < C::NPART; i += kWarps * 32) {
+      double v = 0.0;
+      for (int b = 0; b < (int)gridDim.x; ++b) v += __ldcg(p.cta_part + (int64_t)b * C::NPART + i);
+      p.result[i] = v;
+    }
+    if (threadIdx.x == 0) *p.done_cnt = 0u;
+  }
+}
+
+// ------------------------------------------------------------------ host-side launchers
+template <typename T, int D, int MODE>
+static cudaError_t launch_impl(const CUtensorMap *tm, const PanelParams &p, int grid, cudaStream_t s) {
+  using C = PanelCfg<T, D>;
+  auto kern = panel_kernel<T, D, MODE>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  kern<<<grid, kThreads, C::SMEM, s>>>(*tm, p);
+  return cudaGetLastError();
+}
+
+template <typename T, int D>
+static PanelShape shape_impl() {
+  using C = PanelCfg<T, D>;
+  return PanelShape{C::ROWS, C::NODES, C::STAGES, C::SMEM, C::NPART, kThreads};
+}
+
+#define NSRGS_PANEL_CASE(T, D)                                                               \
+  case D:                                                                                    \
+    if (shape_only) { *shape = shape_impl<T, D>(); return cudaSuccess; }                     \
+    if (mode == kModeRgs) return launch_impl<T, D, kModeRgs>(tm, *p, grid, s);               \
+    if (mode == kModeObjective) return launch_impl<T, D, kModeObjective>(tm, *p, grid, s);   \
+    return launch_impl<T, D, kModeProduct>(tm, *p, grid, s);
+
+cudaError_t panel_dispatch(int dtype, int d, int mode, bool shape_only, PanelShape *shape,
+                           const CUtensorMap *tm, const PanelParams *p, int grid, cudaStream_t s) {
+  if (dtype == 0) {
+    switch (d) {
+      NSRGS_PANEL_CASE(float, 2)
+      NSRGS_PANEL_CASE(float, 3)
+      NSRGS_PANEL_CASE(float, 4)
+      NSRGS_PANEL_CASE(float, 5)
+      NSRGS_PANEL_CASE(float, 6)
+      NSRGS_PANEL_CASE(float, 7)
+      NSRGS_PANEL_CASE(float, 8)
+      NSRGS_PANEL_CASE(float, 9)
+      NSRGS_PANEL_CASE(float, 10)
+      default: return cudaErrorInvalidValue;
+    }
+  } else {
+    switch (d) {
+      NSRGS_PANEL_CASE(double, 2)
+      NSRGS_PANEL_CASE(double, 3)
+      NSRGS_PANEL_CASE(double, 4)
+      NSRGS_PANEL_CASE(double, 5)
+      NSRGS_PANEL_CASE(double, 6)
+      default: return cudaErrorInvalidValue;
+    }
+  }
+}
+
+}  // namespace nsrgs

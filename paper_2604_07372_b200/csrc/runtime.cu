@@ -1,0 +1,729 @@
+// runtime.cu — libnsrgs.so host runtime and C-ABI (include/nsrgs.h).
+//
+// One nsrgs_ctx per (process, GPU).  The context owns: the two X buffers in the tile layout
+// (double-buffered iterate), fp64 partial / result buffers, the split-K scratch, the device
+// error word, the TMA tensor map of the A shard and (world > 1) an NCCL communicator created
+// from a caller-broadcast unique id.  NCCL is loaded lazily with dlopen (the already-loaded
+// libnccl.so.2 of the process is preferred), so single-GPU use has no NCCL dependency.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/nsrgs.h"
+#include "common.cuh"
+#include "kernels.h"
+
+using namespace nsrgs;
+
+// ------------------------------------------------------------------------------ NCCL (dlopen)
+namespace {
+struct NcclApi {
+  bool tried = false, ok = false;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId *) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*AllGather)(const void *, void *, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  const char *(*GetErrorString)(ncclResult_t) = nullptr;
+};
+NcclApi g_nccl;
+
+bool load_nccl() {
+  if (g_nccl.tried) return g_nccl.ok;
+  g_nccl.tried = true;
+  void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) return false;
+#define NSRGS_SYM(f, name) g_nccl.f = reinterpret_cast<decltype(g_nccl.f)>(dlsym(h, name))
+  NSRGS_SYM(GetUniqueId, "ncclGetUniqueId");
+  NSRGS_SYM(CommInitRank, "ncclCommInitRank");
+  NSRGS_SYM(AllGather, "ncclAllGather");
+  NSRGS_SYM(AllReduce, "ncclAllReduce");
+  NSRGS_SYM(CommDestroy, "ncclCommDestroy");
+  NSRGS_SYM(GetErrorString, "ncclGetErrorString");
+#undef NSRGS_SYM
+  g_nccl.ok = g_nccl.GetUniqueId && g_nccl.CommInitRank && g_nccl.AllGather && g_nccl.AllReduce &&
+              g_nccl.CommDestroy && g_nccl.GetErrorString;
+  return g_nccl.ok;
+}
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                   const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+int plan_impl(int64_t n, int32_t d, int32_t world, int32_t rank, nsrgs_plan_t *out, std::string *why) {
+  auto fail = [&](const char *m) {
+    if (why) *why = m;
+    return (int)NSRGS_ERR_INVALID_ARG;
+  };
+  if (!out) return fail("plan: out is NULL");
+  if (n < 2) return fail("n must be >= 2");
+  if (d < 2 || d > 10) return fail("d must be in [2, 10] (d = 1: O(1) has a trivial tangent space, SPEC.md:295)");
+  if (world < 1 || rank < 0 || rank >= world) return fail("need world >= 1 and 0 <= rank < world");
+  if (n % world) return fail("n must be divisible by world (row-block sharding by node)");
+  out->n_local = n / world;
+  out->node0 = (int64_t)rank * out->n_local;
+  out->rows_local = out->n_local * d;
+  out->row0 = out->node0 * d;
+  out->col_tile = kColTile;
+  out->tiles_per_rank = ceil_div(out->rows_local, kColTile);
+  out->x_slice_elems = out->tiles_per_rank * d * kColTile;
+  out->x_elems = (int64_t)world * out->x_slice_elems;
+  return NSRGS_OK;
+}
+
+template <typename T>
+void pack_host_t(int64_t n, int d, const nsrgs_plan_t &pl, T *stack, T *tiled, bool unpack) {
+  const int64_t N = n * d;
+  if (!unpack) std::memset(tiled, 0, sizeof(T) * pl.x_elems);
+  for (int64_t c = 0; c < N; ++c)
+    for (int k = 0; k < d; ++k) {
+      const int64_t t = tile_index(c, k, d, pl.rows_local, pl.tiles_per_rank);
+      if (unpack) stack[c * d + k] = tiled[t]; else tiled[t] = stack[c * d + k];
+    }
+}
+}  // namespace
+
+// ------------------------------------------------------------------------------ context
+struct nsrgs_ctx {
+  int64_t n = 0, N = 0;
+  int d = 0, dtype = 0, rank = 0, world = 1, device = 0;
+  size_t esz = 4;
+  nsrgs_plan_t plan{};
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  // A shard
+  void *A = nullptr;
+  int64_t lda = 0;
+  bool own_A = false, have_A = false;
+  CUtensorMap tmA;
+  double a_fro2 = 0.0;
+  // iterate
+  void *X[2] = {nullptr, nullptr};
+  int cur = 0;
+  bool have_X = false;
+  void *stage = nullptr;   // n*d*d elements (host<->device staging for set/get/Z)
+  // panel launch shape
+  PanelShape shape{};
+  int sm_count = 0, grid = 0, panels = 0, splits = 1, tiles_per_split = 0, total_tiles = 0, units = 0;
+  // scratch
+  double *cta_part = nullptr;   // grid * npart
+  unsigned *counters = nullptr; // [0] done_cnt, [1..panels] panel counters
+  void *Bpart = nullptr;
+  double *res = nullptr;        // res_cap * npart
+  int res_cap = 0;
+  double *red_part = nullptr;   // generic reduction partials
+  int64_t red_cap = 0;
+  double *small = nullptr;      // [0] a_fro2 | [1] chg2 | [8..8+2DD) MC | [256..) F trace / metrics
+  int64_t small_cap = 0;
+  int *err = nullptr;
+  unsigned *ns_region = nullptr;
+  // NCCL
+  ncclComm_t comm = nullptr;
+  // stats / timing
+  bool timing = false;
+  std::vector<cudaEvent_t> ev;
+  int ev_used = 0;
+  double panel_ms = 0.0;
+  int64_t panel_launches = 0, kernel_launches = 0;
+  double ns_region_max = 0.0;
+  std::string msg;
+};
+
+namespace {
+int set_err(nsrgs_ctx *c, int code, const char *fmt, ...) {
+  if (c) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    c->msg = buf;
+  }
+  return code;
+}
+
+#define CUDA_TRY(c, expr)                                                                        \
+  do {                                                                                           \
+    cudaError_t e_ = (expr);                                                                     \
+    if (e_ != cudaSuccess)                                                                       \
+      return set_err((c), e_ == cudaErrorMemoryAllocation ? NSRGS_ERR_OOM : NSRGS_ERR_CUDA,      \
+                     "%s: %s (%s:%d)", #expr, cudaGetErrorString(e_), __FILE__, __LINE__);      \
+  } while (0)
+
+#define NCCL_TRY(c, expr)                                                                        \
+  do {                                                                                           \
+    ncclResult_t r_ = (expr);                                                                    \
+    if (r_ != ncclSuccess)                                                                       \
+      return set_err((c), NSRGS_ERR_NCCL, "%s: %s", #expr, g_nccl.GetErrorString(r_));           \
+  } while (0)
+
+#define NSRGS_TRY(expr)              \
+  do {                               \
+    int s_ = (expr);                 \
+    if (s_ != NSRGS_OK) return s_;   \
+  } while (0)
+
+ncclDataType_t nccl_type(const nsrgs_ctx *c) { return c->dtype == NSRGS_F32 ? ncclFloat32 : ncclFloat64; }
+
+int enter(nsrgs_ctx *c) {
+  if (!c) return NSRGS_ERR_INVALID_ARG;
+  c->msg.clear();
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  return NSRGS_OK;
+}
+
+int sync_and_check(nsrgs_ctx *c, int *flags_out = nullptr) {
+  int flags = 0;
+  CUDA_TRY(c, cudaMemcpyAsync(&flags, c->err, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  if (flags) CUDA_TRY(c, cudaMemsetAsync(c->err, 0, sizeof(int), c->stream));
+  if (flags_out) *flags_out = flags;
+  if (c->timing && c->ev_used) {
+    for (int i = 0; i + 1 < c->ev_used; i += 2) {
+      float ms = 0.f;
+      CUDA_TRY(c, cudaEventElapsedTime(&ms, c->ev[i], c->ev[i + 1]));
+      c->panel_ms += ms;
+    }
+    c->ev_used = 0;
+  }
+  return NSRGS_OK;
+}
+
+int allreduce_sum(nsrgs_ctx *c, double *buf, size_t count) {
+  if (c->world == 1 || count == 0) return NSRGS_OK;
+  NCCL_TRY(c, g_nccl.AllReduce(buf, buf, count, ncclFloat64, ncclSum, c->comm, c->stream));
+  return NSRGS_OK;
+}
+
+int allgather_X(nsrgs_ctx *c, void *buf) {
+  if (c->world == 1) return NSRGS_OK;
+  const size_t cnt = (size_t)c->plan.x_slice_elems;
+  char *base = static_cast<char *>(buf);
+  NCCL_TRY(c, g_nccl.AllGather(base + (size_t)c->rank * cnt * c->esz, base, cnt, nccl_type(c), c->comm, c->stream));
+  return NSRGS_OK;
+}
+
+int ensure_red(nsrgs_ctx *c, int64_t count) {
+  if (count <= c->red_cap) return NSRGS_OK;
+  if (c->red_part) cudaFree(c->red_part);
+  c->red_part = nullptr;
+  CUDA_TRY(c, cudaMalloc(&c->red_part, sizeof(double) * count));
+  c->red_cap = count;
+  return NSRGS_OK;
+}
+
+int ensure_res(nsrgs_ctx *c, int slots) {
+  if (slots <= c->res_cap) return NSRGS_OK;
+  if (c->res) cudaFree(c->res);
+  c->res = nullptr;
+  const int cap = std::max(slots, 2 * c->res_cap);
+  CUDA_TRY(c, cudaMalloc(&c->res, sizeof(double) * (size_t)cap * c->shape.npart));
+  c->res_cap = cap;
+  return NSRGS_OK;
+}
+
+int ensure_small(nsrgs_ctx *c, int64_t count) {
+  if (count <= c->small_cap) return NSRGS_OK;
+  double *nb = nullptr;
+  CUDA_TRY(c, cudaMalloc(&nb, sizeof(double) * count));
+  CUDA_TRY(c, cudaMemsetAsync(nb, 0, sizeof(double) * count, c->stream));
+  if (c->small) {
+    CUDA_TRY(c, cudaMemcpyAsync(nb, c->small, sizeof(double) * c->small_cap, cudaMemcpyDeviceToDevice, c->stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    cudaFree(c->small);
+  }
+  c->small = nb;
+  c->small_cap = count;
+  return NSRGS_OK;
+}
+constexpr int kSmallFro = 0, kSmallChg = 1, kSmallMC = 8, kSmallOut = 256;
+
+int build_tmap(nsrgs_ctx *c) {
+  static EncodeTiledFn encode = nullptr;
+  if (!encode) {
+    void *fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    CUDA_TRY(c, cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+    if (!fn || q != cudaDriverEntryPointSuccess)
+      return set_err(c, NSRGS_ERR_CUDA, "cuTensorMapEncodeTiled not available from the driver");
+    encode = reinterpret_cast<EncodeTiledFn>(fn);
+  }
+  const cuuint64_t Nr = (cuuint64_t)c->plan.rows_local;
+  cuuint64_t dims[3] = {c->world == 1 ? (cuuint64_t)c->N : Nr, (cuuint64_t)c->world, (cuuint64_t)c->plan.rows_local};
+  cuuint64_t strides[2] = {c->world == 1 ? (cuuint64_t)(c->lda * c->esz) : (cuuint64_t)(Nr * c->esz),
+                           (cuuint64_t)(c->lda * c->esz)};
+  cuuint32_t box[3] = {(cuuint32_t)kColTile, 1u, (cuuint32_t)c->shape.rows};
+  cuuint32_t estr[3] = {1u, 1u, 1u};
+  CUresult r = encode(&c->tmA, c->dtype == NSRGS_F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64,
+                      3, c->A, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_err(c, NSRGS_ERR_CUDA, "cuTensorMapEncodeTiled failed (CUresult %d)", (int)r);
+  return NSRGS_OK;
+}
+
+// One panel-kernel launch: X[src] -> out (mode), partials into res slot.
+int launch_panel(nsrgs_ctx *c, int mode, const void *Xin, void *Xout, double *result, double eta, int K) {
+  PanelParams p{};
+  p.X = Xin;
+  p.Xout = Xout;
+  p.Bpart = c->Bpart;
+  p.panel_cnt = c->counters + 1;
+  p.cta_part = c->cta_part;
+  p.done_cnt = c->counters;
+  p.result = result;
+  p.err = c->err;
+  p.ns_region = c->ns_region;
+  p.n = c->n;
+  p.n_local = c->plan.n_local;
+  p.node0 = c->plan.node0;
+  p.rows_local = c->plan.rows_local;
+  p.tiles_per_rank = c->plan.tiles_per_rank;
+  p.world = c->world;
+  p.rank = c->rank;
+  p.panels = c->panels;
+  p.splits = c->splits;
+  p.tiles_per_split = c->tiles_per_split;
+  p.total_tiles = c->total_tiles;
+  p.units = c->units;
+  p.coef = (double)(c->n - 1);
+  p.eta = eta;
+  p.K = K;
+  if (c->timing) {
+    while ((int)c->ev.size() < c->ev_used + 2) {
+      cudaEvent_t e;
+      CUDA_TRY(c, cudaEventCreate(&e));
+      c->ev.push_back(e);
+    }
+    CUDA_TRY(c, cudaEventRecord(c->ev[c->ev_used], c->stream));
+  }
+  CUDA_TRY(c, panel_dispatch(c->dtype, c->d, mode, false, nullptr, &c->tmA, &p, c->grid, c->stream));
+  if (c->timing) {
+    CUDA_TRY(c, cudaEventRecord(c->ev[c->ev_used + 1], c->stream));
+    c->ev_used += 2;
+  }
+  c->panel_launches++;
+  c->kernel_launches++;
+  return NSRGS_OK;
+}
+
+int objective_from_res(nsrgs_ctx *c, int T, double *host_out) {
+  NSRGS_TRY(ensure_small(c, kSmallOut + std::max(T, 8)));
+  CUDA_TRY(c, launch_objective_final(c->d, T, c->res, c->shape.npart, c->small + kSmallFro, c->small + kSmallOut,
+                                     c->stream));
+  c->kernel_launches++;
+  if (host_out)
+    CUDA_TRY(c, cudaMemcpyAsync(host_out, c->small + kSmallOut, sizeof(double) * T, cudaMemcpyDeviceToHost, c->stream));
+  return NSRGS_OK;
+}
+
+int fro2_finish(nsrgs_ctx *c, int nblocks) {
+  CUDA_TRY(c, launch_reduce(c->red_part, nblocks, 1, c->small + kSmallFro, c->stream));
+  c->kernel_launches++;
+  NSRGS_TRY(allreduce_sum(c, c->small + kSmallFro, 1));
+  CUDA_TRY(c, cudaMemcpyAsync(&c->a_fro2, c->small + kSmallFro, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  NSRGS_TRY(sync_and_check(c));
+  return NSRGS_OK;
+}
+
+int require_ready(nsrgs_ctx *c, bool need_X) {
+  if (!c->have_A) return set_err(c, NSRGS_ERR_STATE, "no A: call nsrgs_generate or nsrgs_attach_A first");
+  if (need_X && !c->have_X) return set_err(c, NSRGS_ERR_STATE, "no iterate: call nsrgs_init_spectral or nsrgs_set_X");
+  return NSRGS_OK;
+}
+}  // namespace
+
+// ------------------------------------------------------------------------------ C-ABI
+extern "C" {
+
+int nsrgs_version(void) { return NSRGS_VERSION; }
+
+int nsrgs_plan(int64_t n, int32_t d, int32_t world, int32_t rank, nsrgs_plan_t *out) {
+  return plan_impl(n, d, world, rank, out, nullptr);
+}
+
+int nsrgs_pack_host(int64_t n, int32_t d, int32_t world, int32_t dtype, const void *stack, void *tiled) {
+  nsrgs_plan_t pl;
+  int s = plan_impl(n, d, world, 0, &pl, nullptr);
+  if (s) return s;
+  if (!stack || !tiled) return NSRGS_ERR_INVALID_ARG;
+  if (dtype == NSRGS_F32) pack_host_t<float>(n, d, pl, (float *)stack, (float *)tiled, false);
+  else if (dtype == NSRGS_F64) pack_host_t<double>(n, d, pl, (double *)stack, (double *)tiled, false);
+  else return NSRGS_ERR_INVALID_ARG;
+  return NSRGS_OK;
+}
+
+int nsrgs_unpack_host(int64_t n, int32_t d, int32_t world, int32_t dtype, const void *tiled, void *stack) {
+  nsrgs_plan_t pl;
+  int s = plan_impl(n, d, world, 0, &pl, nullptr);
+  if (s) return s;
+  if (!stack || !tiled) return NSRGS_ERR_INVALID_ARG;
+  if (dtype == NSRGS_F32) pack_host_t<float>(n, d, pl, (float *)stack, (float *)tiled, true);
+  else if (dtype == NSRGS_F64) pack_host_t<double>(n, d, pl, (double *)stack, (double *)tiled, true);
+  else return NSRGS_ERR_INVALID_ARG;
+  return NSRGS_OK;
+}
+
+int nsrgs_get_nccl_unique_id(void *out128) {
+  if (!out128) return NSRGS_ERR_INVALID_ARG;
+  if (!load_nccl()) return NSRGS_ERR_NCCL;
+  ncclUniqueId id;
+  if (g_nccl.GetUniqueId(&id) != ncclSuccess) return NSRGS_ERR_NCCL;
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+  std::memcpy(out128, &id, 128);
+  return NSRGS_OK;
+}
+
+static thread_local std::string g_create_msg;
+
+const char *nsrgs_last_error(const nsrgs_ctx *ctx) { return ctx ? ctx->msg.c_str() : g_create_msg.c_str(); }
+
+int nsrgs_destroy(nsrgs_ctx *c) {
+  if (!c) return NSRGS_OK;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(c->comm);
+  for (auto e : c->ev) cudaEventDestroy(e);
+  void *bufs[] = {c->X[0], c->X[1], c->stage, c->cta_part, c->counters, c->Bpart, c->res, c->red_part, c->small,
+                  c->err, c->ns_region};
+  for (void *b : bufs)
+    if (b) cudaFree(b);
+  if (c->own_A && c->A) cudaFree(c->A);
+  if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+  return NSRGS_OK;
+}
+
+int nsrgs_create(const nsrgs_desc *desc, nsrgs_ctx **out) {
+  if (!out) return NSRGS_ERR_INVALID_ARG;
+  *out = nullptr;
+  if (!desc) return NSRGS_ERR_INVALID_ARG;
+  nsrgs_ctx *c = new nsrgs_ctx();
+  std::string why;
+  // nsrgs_last_error(NULL) reports why a create failed
+  auto bail = [&](int code, const char *m = nullptr) {
+    g_create_msg = m ? m : (why.empty() ? c->msg : why);
+    nsrgs_destroy(c);
+    return code;
+  };
+  g_create_msg.clear();
+  if (desc->dtype != NSRGS_F32 && desc->dtype != NSRGS_F64) return bail(NSRGS_ERR_INVALID_ARG, "dtype must be F32 or F64");
+  int s = plan_impl(desc->n, desc->d, desc->world, desc->rank, &c->plan, &why);
+  if (s) return bail(s);
+  if (desc->dtype == NSRGS_F64 && desc->d > 6) return bail(NSRGS_ERR_INVALID_ARG, "F64 supports d in [2, 6]");
+  if ((desc->world > 1) != (desc->nccl_unique_id != nullptr))
+    return bail(NSRGS_ERR_INVALID_ARG, "nccl_unique_id must be given iff world > 1");
+  c->n = desc->n;
+  c->d = desc->d;
+  c->N = desc->n * desc->d;
+  c->dtype = desc->dtype;
+  c->esz = desc->dtype == NSRGS_F32 ? 4 : 8;
+  c->rank = desc->rank;
+  c->world = desc->world;
+  c->device = desc->device;
+  if (c->world > 1 && (c->plan.rows_local * (int64_t)c->esz) % 16)
+    return bail(NSRGS_ERR_INVALID_ARG, "world > 1 needs (n/world)*d*sizeof(dtype) % 16 == 0");
+  if (cudaSetDevice(c->device) != cudaSuccess) return bail(NSRGS_ERR_CUDA, "cudaSetDevice failed (no GPU?)");
+  if (desc->cuda_stream) {
+    c->stream = static_cast<cudaStream_t>(desc->cuda_stream);
+  } else {
+    if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) return bail(NSRGS_ERR_CUDA);
+    c->own_stream = true;
+  }
+  cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, c->device);
+  panel_dispatch(c->dtype, c->d, 0, true, &c->shape, nullptr, nullptr, 0, nullptr);
+  // launch shape: work units = (row panel, column split)
+  c->panels = (int)ceil_div(c->plan.rows_local, c->shape.rows);
+  c->total_tiles = (int)(c->world * c->plan.tiles_per_rank);
+  int splits = 1;
+  if (c->panels < c->sm_count) splits = (int)std::min<int64_t>(c->total_tiles, ceil_div(2 * c->sm_count, c->panels));
+  c->tiles_per_split = (int)ceil_div(c->total_tiles, splits);
+  c->splits = (int)ceil_div(c->total_tiles, c->tiles_per_split);
+  c->units = c->panels * c->splits;
+  c->grid = std::min(c->units, c->sm_count);
+  auto alloc = [&](void **p, size_t bytes) {
+    cudaError_t e = cudaMalloc(p, bytes);
+    if (e != cudaSuccess) return false;
+    return cudaMemsetAsync(*p, 0, bytes, c->stream) == cudaSuccess;
+  };
+  const size_t xb = c->esz * (size_t)c->plan.x_elems;
+  bool ok = alloc(&c->X[0], xb) && alloc(&c->X[1], xb) && alloc(&c->stage, c->esz * (size_t)(c->n * c->d * c->d)) &&
+            alloc((void **)&c->cta_part, sizeof(double) * c->grid * c->shape.npart) &&
+            alloc((void **)&c->counters, sizeof(unsigned) * (c->panels + 1)) &&
+            alloc((void **)&c->err, sizeof(int)) && alloc((void **)&c->ns_region, sizeof(unsigned));
+  if (ok && c->splits > 1) ok = alloc(&c->Bpart, c->esz * (size_t)c->units * c->shape.rows * c->d);
+  if (!ok) return bail(NSRGS_ERR_OOM, "device allocation failed");
+  if (ensure_res(c, 128) || ensure_small(c, kSmallOut + 256)) return bail(NSRGS_ERR_OOM);
+  if (c->world > 1) {
+    if (!load_nccl()) return bail(NSRGS_ERR_NCCL, "libnccl.so.2 not loadable");
+    ncclUniqueId id;
+    std::memcpy(&id, desc->nccl_unique_id, sizeof id);
+    if (g_nccl.CommInitRank(&c->comm, c->world, id, c->rank) != ncclSuccess) return bail(NSRGS_ERR_NCCL, "ncclCommInitRank failed");
+  }
+  if (cudaStreamSynchronize(c->stream) != cudaSuccess) return bail(NSRGS_ERR_CUDA);
+  *out = c;
+  return NSRGS_OK;
+}
+
+int nsrgs_attach_A(nsrgs_ctx *c, const void *A_shard_dev, int64_t lda) {
+  NSRGS_TRY(enter(c));
+  if (!A_shard_dev || lda < c->N || (lda * (int64_t)c->esz) % 16 || (reinterpret_cast<uintptr_t>(A_shard_dev) % 16))
+    return set_err(c, NSRGS_ERR_INVALID_ARG, "attach_A: need non-NULL 16-byte aligned A, lda >= n d, lda*esz %% 16 == 0");
+  if (c->own_A && c->A) cudaFree(c->A);
+  c->A = const_cast<void *>(A_shard_dev);
+  c->lda = lda;
+  c->own_A = false;
+  NSRGS_TRY(build_tmap(c));
+  int nb = 0;
+  NSRGS_TRY(ensure_red(c, 8 * 4096));
+  CUDA_TRY(c, launch_sumsq(c->dtype, c->A, c->plan.rows_local, c->N, c->lda, c->red_part, &nb, c->stream));
+  c->kernel_launches++;
+  NSRGS_TRY(fro2_finish(c, nb));
+  c->have_A = true;
+  return NSRGS_OK;
+}
+
+int nsrgs_generate(nsrgs_ctx *c, uint64_t seed, double sigma, void *Z_out_host) {
+  NSRGS_TRY(enter(c));
+  if (!(sigma >= 0.0) || !std::isfinite(sigma)) return set_err(c, NSRGS_ERR_INVALID_ARG, "sigma must be finite, >= 0");
+  const int64_t align = 16 / (int64_t)c->esz;
+  const int64_t lda = ceil_div(c->N, align) * align;
+  if (!(c->own_A && c->A && c->lda == lda)) {
+    if (c->own_A && c->A) cudaFree(c->A);
+    c->A = nullptr;
+    c->own_A = false;
+    CUDA_TRY(c, cudaMalloc(&c->A, c->esz * (size_t)c->plan.rows_local * (size_t)lda));
+    c->own_A = true;
+    c->lda = lda;
+    if (lda != c->N)
+      CUDA_TRY(c, cudaMemsetAsync(c->A, 0, c->esz * (size_t)c->plan.rows_local * (size_t)lda, c->stream));
+  }
+  double *Z64 = nullptr;
+  CUDA_TRY(c, cudaMalloc(&Z64, sizeof(double) * (size_t)(c->n * c->d * c->d)));
+  CUDA_TRY(c, launch_gen_Z(c->dtype, c->d, c->n, seed, Z64, Z_out_host ? c->stage : nullptr, c->stream));
+  c->kernel_launches += Z_out_host ? 2 : 1;
+  const int64_t nbx = ceil_div(c->n, 128), nby = std::min<int64_t>(c->plan.n_local, 32768);
+  NSRGS_TRY(ensure_red(c, nbx * nby));
+  int nb = 0;
+  CUDA_TRY(c, launch_gen_A(c->dtype, c->d, c->n, c->plan.node0, c->plan.n_local, seed, sigma, Z64, c->A, c->lda,
+                           c->red_part, &nb, c->stream));
+  c->kernel_launches++;
+  if (Z_out_host)
+    CUDA_TRY(c, cudaMemcpyAsync(Z_out_host, c->stage, c->esz * (size_t)(c->n * c->d * c->d), cudaMemcpyDeviceToHost,
+                                c->stream));
+  NSRGS_TRY(build_tmap(c));
+  int s = fro2_finish(c, nb);
+  cudaFree(Z64);
+  if (s) return s;
+  c->have_A = true;
+  return NSRGS_OK;
+}
+
+int nsrgs_copy_A_rows(nsrgs_ctx *c, int64_t row0, int64_t nrows, void *out_host) {
+  NSRGS_TRY(enter(c));
+  if (!c->have_A) return set_err(c, NSRGS_ERR_STATE, "no A");
+  if (!out_host || row0 < 0 || nrows < 0 || row0 + nrows > c->plan.rows_local)
+    return set_err(c, NSRGS_ERR_INVALID_ARG, "copy_A_rows: bad range");
+  CUDA_TRY(c, cudaMemcpy2DAsync(out_host, c->esz * c->N, static_cast<char *>(c->A) + c->esz * row0 * c->lda,
+                                c->esz * c->lda, c->esz * c->N, nrows, cudaMemcpyDeviceToHost, c->stream));
+  return sync_and_check(c);
+}
+
+int nsrgs_set_X(nsrgs_ctx *c, const void *X, int on_device) {
+  NSRGS_TRY(enter(c));
+  if (!X) return set_err(c, NSRGS_ERR_INVALID_ARG, "set_X: NULL");
+  const size_t bytes = c->esz * (size_t)(c->n * c->d * c->d);
+  const void *src = X;
+  if (!on_device) {
+    CUDA_TRY(c, cudaMemcpyAsync(c->stage, X, bytes, cudaMemcpyHostToDevice, c->stream));
+    src = c->stage;
+  }
+  CUDA_TRY(c, launch_pack(c->dtype, c->d, c->n, src, c->X[c->cur], c->plan.rows_local, c->plan.tiles_per_rank, 0,
+                          c->stream));
+  c->kernel_launches++;
+  NSRGS_TRY(sync_and_check(c));
+  c->have_X = true;
+  return NSRGS_OK;
+}
+
+int nsrgs_get_X(nsrgs_ctx *c, void *X, int on_device) {
+  NSRGS_TRY(enter(c));
+  if (!X) return set_err(c, NSRGS_ERR_INVALID_ARG, "get_X: NULL");
+  if (!c->have_X) return set_err(c, NSRGS_ERR_STATE, "no iterate");
+  const size_t bytes = c->esz * (size_t)(c->n * c->d * c->d);
+  void *dst = on_device ? X : c->stage;
+  CUDA_TRY(c, launch_pack(c->dtype, c->d, c->n, dst, c->X[c->cur], c->plan.rows_local, c->plan.tiles_per_rank, 1,
+                          c->stream));
+  c->kernel_launches++;
+  if (!on_device) CUDA_TRY(c, cudaMemcpyAsync(X, c->stage, bytes, cudaMemcpyDeviceToHost, c->stream));
+  return sync_and_check(c);
+}
+
+int nsrgs_init_spectral(nsrgs_ctx *c, uint64_t seed, int max_sweeps, double tol, int *sweeps_used) {
+  NSRGS_TRY(enter(c));
+  NSRGS_TRY(require_ready(c, false));
+  if (max_sweeps < 1 || !(tol > 0.0)) return set_err(c, NSRGS_ERR_INVALID_ARG, "init_spectral: max_sweeps >= 1, tol > 0");
+  const int DD = c->d * c->d;
+  CUDA_TRY(c, launch_gen_Y0(c->dtype, c->d, c->n, seed, c->X[c->cur], c->plan.rows_local, c->plan.tiles_per_rank,
+                            c->stream));
+  c->kernel_launches++;
+  const int64_t nbs = ceil_div(c->plan.rows_local, 256);
+  NSRGS_TRY(ensure_red(c, nbs));
+  int sweeps = 0;
+  bool converged = false;
+  for (sweeps = 1; sweeps <= max_sweeps; ++sweeps) {
+    void *Y = c->X[c->cur], *W = c->X[1 - c->cur];
+    NSRGS_TRY(launch_panel(c, kModeProduct, Y, W, c->res, 0.0, 0));
+    NSRGS_TRY(allreduce_sum(c, c->res, 2 * DD));
+    CUDA_TRY(c, launch_chol(c->d, c->res, c->small + kSmallMC, c->err, c->stream));
+    int nb = 0;
+    CUDA_TRY(c, launch_scale(c->dtype, c->d, c->plan.node0, c->plan.n_local, c->small + kSmallMC, W, Y,
+                             c->plan.rows_local, c->plan.tiles_per_rank, c->red_part, &nb, c->stream));
+    CUDA_TRY(c, launch_reduce(c->red_part, nb, 1, c->small + kSmallChg, c->stream));
+    c->kernel_launches += 3;
+    NSRGS_TRY(allreduce_sum(c, c->small + kSmallChg, 1));
+    NSRGS_TRY(allgather_X(c, W));
+    c->cur = 1 - c->cur;
+    double chg2 = 0.0;
+    CUDA_TRY(c, cudaMemcpyAsync(&chg2, c->small + kSmallChg, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    int flags = 0;
+    NSRGS_TRY(sync_and_check(c, &flags));
+    if (flags & kErrSingular) return set_err(c, NSRGS_ERR_SINGULAR, "Cholesky of Y^T Y failed at sweep %d", sweeps);
+    if (!std::isfinite(chg2)) return set_err(c, NSRGS_ERR_NONFINITE, "non-finite subspace change at sweep %d", sweeps);
+    if (sweeps >= 2 && std::sqrt(chg2) < tol) { converged = true; break; }
+  }
+  if (sweeps > max_sweeps) sweeps = max_sweeps;
+  CUDA_TRY(c, launch_polar(c->dtype, c->d, c->n, c->X[c->cur], c->X[1 - c->cur], c->plan.rows_local,
+                           c->plan.tiles_per_rank, c->err, c->stream));
+  c->kernel_launches++;
+  c->cur = 1 - c->cur;
+  c->have_X = true;
+  int flags = 0;
+  NSRGS_TRY(sync_and_check(c, &flags));
+  if (sweeps_used) *sweeps_used = sweeps;
+  if (flags & kErrSingular) return set_err(c, NSRGS_ERR_SINGULAR, "init polar: Newton-Schulz did not converge (singular Y_i)");
+  if (!converged)
+    return set_err(c, NSRGS_ERR_EIG_NOT_CONVERGED, "subspace iteration: tol %.3g not reached in %d sweeps", tol, max_sweeps);
+  return NSRGS_OK;
+}
+
+static int run_impl(nsrgs_ctx *c, int T, double eta, int K, double *trace) {
+  NSRGS_TRY(require_ready(c, true));
+  if (T < 0 || K < 0 || !(eta > 0.0) || !std::isfinite(eta))
+    return set_err(c, NSRGS_ERR_INVALID_ARG, "run: need T >= 0, K >= 0, eta > 0");
+  if (T == 0) return NSRGS_OK;
+  NSRGS_TRY(ensure_res(c, T));
+  for (int t = 0; t < T; ++t) {
+    NSRGS_TRY(launch_panel(c, kModeRgs, c->X[c->cur], c->X[1 - c->cur], c->res + (size_t)t * c->shape.npart, eta, K));
+    NSRGS_TRY(allgather_X(c, c->X[1 - c->cur]));
+    c->cur = 1 - c->cur;
+  }
+  if (trace) {
+    NSRGS_TRY(allreduce_sum(c, c->res, (size_t)T * c->shape.npart));
+    NSRGS_TRY(objective_from_res(c, T, trace));
+  }
+  unsigned nr = 0;
+  CUDA_TRY(c, cudaMemcpyAsync(&nr, c->ns_region, sizeof(unsigned), cudaMemcpyDeviceToHost, c->stream));
+  int flags = 0;
+  NSRGS_TRY(sync_and_check(c, &flags));
+  float nrf;
+  std::memcpy(&nrf, &nr, 4);
+  c->ns_region_max = std::max(c->ns_region_max, (double)nrf);
+  if (flags & kErrDivergence)
+    return set_err(c, NSRGS_ERR_DIVERGENCE, "Newton-Schulz retraction diverged (||S||_F > 10 sqrt(d) or non-finite)");
+  if (trace)
+    for (int t = 0; t < T; ++t)
+      if (!std::isfinite(trace[t])) return set_err(c, NSRGS_ERR_NONFINITE, "objective non-finite at t = %d", t);
+  return NSRGS_OK;
+}
+
+int nsrgs_step(nsrgs_ctx *c, double eta, int K, double *objective_before) {
+  NSRGS_TRY(enter(c));
+  return run_impl(c, 1, eta, K, objective_before);
+}
+
+int nsrgs_run(nsrgs_ctx *c, int T, double eta, int K, double *objective_trace) {
+  NSRGS_TRY(enter(c));
+  return run_impl(c, T, eta, K, objective_trace);
+}
+
+int nsrgs_objective(nsrgs_ctx *c, double *F_out) {
+  NSRGS_TRY(enter(c));
+  NSRGS_TRY(require_ready(c, true));
+  if (!F_out) return set_err(c, NSRGS_ERR_INVALID_ARG, "objective: NULL out");
+  NSRGS_TRY(launch_panel(c, kModeObjective, c->X[c->cur], nullptr, c->res, 0.0, 0));
+  NSRGS_TRY(allreduce_sum(c, c->res, c->shape.npart));
+  NSRGS_TRY(objective_from_res(c, 1, F_out));
+  NSRGS_TRY(sync_and_check(c));
+  if (!std::isfinite(*F_out)) return set_err(c, NSRGS_ERR_NONFINITE, "objective non-finite");
+  return NSRGS_OK;
+}
+
+int nsrgs_alignment_error(nsrgs_ctx *c, const void *Z, int Z_on_device, double out[3]) {
+  NSRGS_TRY(enter(c));
+  if (!c->have_X) return set_err(c, NSRGS_ERR_STATE, "no iterate");
+  if (!Z || !out) return set_err(c, NSRGS_ERR_INVALID_ARG, "alignment_error: NULL argument");
+  const void *Zd = Z;
+  if (!Z_on_device) {
+    CUDA_TRY(c, cudaMemcpyAsync(c->stage, Z, c->esz * (size_t)(c->n * c->d * c->d), cudaMemcpyHostToDevice, c->stream));
+    Zd = c->stage;
+  }
+  const int w = 3 * c->d * c->d;
+  NSRGS_TRY(ensure_red(c, (ceil_div(c->n, 256) + 1) * w));
+  NSRGS_TRY(ensure_small(c, kSmallOut + w + 8));
+  int nb = 0;
+  CUDA_TRY(c, launch_metrics(c->dtype, c->d, c->n, c->X[c->cur], Zd, c->plan.rows_local, c->plan.tiles_per_rank,
+                             c->red_part, &nb, c->stream));
+  CUDA_TRY(c, launch_reduce(c->red_part, nb, w, c->small + kSmallOut + 8, c->stream));
+  CUDA_TRY(c, launch_metrics_final(c->d, c->n, c->small + kSmallOut + 8, c->small + kSmallOut, c->stream));
+  c->kernel_launches += 3;
+  CUDA_TRY(c, cudaMemcpyAsync(out, c->small + kSmallOut, 3 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  NSRGS_TRY(sync_and_check(c));
+  if (!std::isfinite(out[0]) || !std::isfinite(out[1])) return set_err(c, NSRGS_ERR_NONFINITE, "non-finite metrics");
+  return NSRGS_OK;
+}
+
+int nsrgs_get_stats(nsrgs_ctx *c, nsrgs_stats_t *o) {
+  if (!c || !o) return NSRGS_ERR_INVALID_ARG;
+  o->grid = c->grid;
+  o->threads = c->shape.threads;
+  o->stages = c->shape.stages;
+  o->rows_per_panel = c->shape.rows;
+  o->splits = c->splits;
+  o->panels = c->panels;
+  o->smem_bytes = c->shape.smem;
+  o->panel_ms_total = c->panel_ms;
+  o->panel_launches = c->panel_launches;
+  o->kernel_launches = c->kernel_launches;
+  o->ns_region_max = c->ns_region_max;
+  o->a_fro2 = c->a_fro2;
+  return NSRGS_OK;
+}
+
+int nsrgs_reset_stats(nsrgs_ctx *c, int enable_panel_timing) {
+  NSRGS_TRY(enter(c));
+  NSRGS_TRY(sync_and_check(c));
+  c->timing = enable_panel_timing != 0;
+  c->panel_ms = 0.0;
+  c->panel_launches = 0;
+  c->kernel_launches = 0;
+  c->ns_region_max = 0.0;
+  c->ev_used = 0;
+  CUDA_TRY(c, cudaMemsetAsync(c->ns_region, 0, sizeof(unsigned), c->stream));
+  return sync_and_check(c);
+}
+
+}  // extern "C"

@@ -1,0 +1,246 @@
+"""Thin ctypes binding of libnsrgs.so (include/nsrgs.h).
+
+Argument marshalling only: every step of the NS-RGS path runs in the library's CUDA
+kernels.  PyTorch is used for the CUDA stream handle and (optionally) device tensors;
+host arrays are NumPy.  There is no CPU fallback: if libnsrgs.so is missing, importing
+this module raises.
+"""
+from __future__ import annotations
+
+import ctypes as ct
+import os
+
+import numpy as np
+
+_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libnsrgs.so")
+if not os.path.exists(_LIB_PATH):
+    raise ImportError(f"libnsrgs.so not built ({_LIB_PATH}); run `python -m paper_2604_07372_b200.build` "
+                      "or __graft_entry__.build() — there is no CPU fallback")
+_lib = ct.CDLL(_LIB_PATH)
+
+F32, F64 = 0, 1
+STATUS = {0: "OK", 1: "INVALID_ARG", 2: "STATE", 3: "CUDA", 4: "NCCL", 5: "OOM", 6: "DIVERGENCE",
+          7: "SINGULAR", 8: "EIG_NOT_CONVERGED", 9: "NONFINITE"}
+
+
+class NSRGSError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"nsrgs {STATUS.get(status, status)}: {msg}")
+        self.status = status
+        self.name = STATUS.get(status, str(status))
+
+
+class Desc(ct.Structure):
+    _fields_ = [("n", ct.c_int64), ("d", ct.c_int32), ("dtype", ct.c_int32), ("rank", ct.c_int32),
+                ("world", ct.c_int32), ("device", ct.c_int32), ("nccl_unique_id", ct.c_void_p),
+                ("cuda_stream", ct.c_void_p)]
+
+
+class Plan(ct.Structure):
+    _fields_ = [(k, ct.c_int64) for k in ("n_local", "node0", "rows_local", "row0", "col_tile",
+                                          "tiles_per_rank", "x_elems", "x_slice_elems")]
+
+
+class Stats(ct.Structure):
+    _fields_ = [("grid", ct.c_int32), ("threads", ct.c_int32), ("stages", ct.c_int32),
+                ("rows_per_panel", ct.c_int32), ("splits", ct.c_int32), ("panels", ct.c_int64),
+                ("smem_bytes", ct.c_int64), ("panel_ms_total", ct.c_double), ("panel_launches", ct.c_int64),
+                ("kernel_launches", ct.c_int64), ("ns_region_max", ct.c_double), ("a_fro2", ct.c_double)]
+
+
+_P = ct.c_void_p
+_SIGS = {
+    "nsrgs_version": ([], ct.c_int),
+    "nsrgs_plan": ([ct.c_int64, ct.c_int32, ct.c_int32, ct.c_int32, ct.POINTER(Plan)], ct.c_int),
+    "nsrgs_pack_host": ([ct.c_int64, ct.c_int32, ct.c_int32, ct.c_int32, _P, _P], ct.c_int),
+    "nsrgs_unpack_host": ([ct.c_int64, ct.c_int32, ct.c_int32, ct.c_int32, _P, _P], ct.c_int),
+    "nsrgs_get_nccl_unique_id": ([_P], ct.c_int),
+    "nsrgs_create": ([ct.POINTER(Desc), ct.POINTER(_P)], ct.c_int),
+    "nsrgs_destroy": ([_P], ct.c_int),
+    "nsrgs_last_error": ([_P], ct.c_char_p),
+    "nsrgs_attach_A": ([_P, _P, ct.c_int64], ct.c_int),
+    "nsrgs_generate": ([_P, ct.c_uint64, ct.c_double, _P], ct.c_int),
+    "nsrgs_copy_A_rows": ([_P, ct.c_int64, ct.c_int64, _P], ct.c_int),
+    "nsrgs_init_spectral": ([_P, ct.c_uint64, ct.c_int, ct.c_double, ct.POINTER(ct.c_int)], ct.c_int),
+    "nsrgs_step": ([_P, ct.c_double, ct.c_int, ct.POINTER(ct.c_double)], ct.c_int),
+    "nsrgs_run": ([_P, ct.c_int, ct.c_double, ct.c_int, ct.POINTER(ct.c_double)], ct.c_int),
+    "nsrgs_objective": ([_P, ct.POINTER(ct.c_double)], ct.c_int),
+    "nsrgs_alignment_error": ([_P, _P, ct.c_int, ct.POINTER(ct.c_double)], ct.c_int),
+    "nsrgs_set_X": ([_P, _P, ct.c_int], ct.c_int),
+    "nsrgs_get_X": ([_P, _P, ct.c_int], ct.c_int),
+    "nsrgs_get_stats": ([_P, ct.POINTER(Stats)], ct.c_int),
+    "nsrgs_reset_stats": ([_P, ct.c_int], ct.c_int),
+}
+for _name, (_args, _res) in _SIGS.items():
+    _f = getattr(_lib, _name)
+    _f.argtypes = _args
+    _f.restype = _res
+
+EXPORTED = tuple(_SIGS)
+
+
+def _np_dtype(dtype: int):
+    return np.float32 if dtype == F32 else np.float64
+
+
+def version() -> int:
+    return _lib.nsrgs_version()
+
+
+def plan(n: int, d: int, world: int = 1, rank: int = 0) -> dict:
+    p = Plan()
+    s = _lib.nsrgs_plan(n, d, world, rank, ct.byref(p))
+    if s:
+        raise NSRGSError(s, "unsupported (n, d, world, rank)")
+    return {k: getattr(p, k) for k, _ in Plan._fields_}
+
+
+def pack_host(stack: np.ndarray, n: int, d: int, world: int) -> np.ndarray:
+    """nd x d stack -> device tile layout (host arrays; see nsrgs_plan)."""
+    dt = F32 if stack.dtype == np.float32 else F64
+    stack = np.ascontiguousarray(stack)
+    out = np.empty(plan(n, d, world)["x_elems"], dtype=stack.dtype)
+    s = _lib.nsrgs_pack_host(n, d, world, dt, stack.ctypes.data, out.ctypes.data)
+    if s:
+        raise NSRGSError(s, "pack_host")
+    return out
+
+
+def unpack_host(tiled: np.ndarray, n: int, d: int, world: int) -> np.ndarray:
+    dt = F32 if tiled.dtype == np.float32 else F64
+    tiled = np.ascontiguousarray(tiled)
+    out = np.empty((n * d, d), dtype=tiled.dtype)
+    s = _lib.nsrgs_unpack_host(n, d, world, dt, tiled.ctypes.data, out.ctypes.data)
+    if s:
+        raise NSRGSError(s, "unpack_host")
+    return out
+
+
+def get_nccl_unique_id() -> bytes:
+    buf = ct.create_string_buffer(128)
+    s = _lib.nsrgs_get_nccl_unique_id(buf)
+    if s:
+        raise NSRGSError(s, "ncclGetUniqueId")
+    return buf.raw
+
+
+class Solver:
+    """One NS-RGS context (one per process / GPU).  Methods mirror the C-ABI names."""
+
+    def __init__(self, n: int, d: int, dtype: int = F32, rank: int = 0, world: int = 1, device: int = 0,
+                 nccl_id: bytes | None = None, stream=None):
+        import torch  # CUDA stream handle only
+
+        if stream is None:
+            stream = torch.cuda.current_stream(device)
+        self.n, self.d, self.dtype, self.rank, self.world, self.device = n, d, dtype, rank, world, device
+        self.np_dtype = _np_dtype(dtype)
+        self._stream = stream
+        self._id = ct.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
+        desc = Desc(n, d, dtype, rank, world, device, ct.cast(self._id, _P) if self._id is not None else None,
+                    _P(stream.cuda_stream))
+        h = _P()
+        s = _lib.nsrgs_create(ct.byref(desc), ct.byref(h))
+        if s:
+            raise NSRGSError(s, _lib.nsrgs_last_error(None).decode())
+        self._h = h
+
+    # ------------------------------------------------------------------ plumbing
+    def _check(self, s: int):
+        if s:
+            raise NSRGSError(s, _lib.nsrgs_last_error(self._h).decode())
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.nsrgs_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    @staticmethod
+    def _ptr(x):
+        """(pointer, on_device) of a NumPy array or torch tensor (contiguous)."""
+        if isinstance(x, np.ndarray):
+            assert x.flags["C_CONTIGUOUS"]
+            return x.ctypes.data, 0
+        assert x.is_contiguous()
+        return x.data_ptr(), int(x.is_cuda)
+
+    # ------------------------------------------------------------------ C-ABI calls
+    def generate(self, seed: int, sigma: float, want_Z: bool = True):
+        Z = np.empty((self.n, self.d, self.d), dtype=self.np_dtype) if want_Z else None
+        self._check(_lib.nsrgs_generate(self._h, seed, sigma, Z.ctypes.data if want_Z else None))
+        return Z
+
+    def attach_A(self, A_shard, lda: int | None = None):
+        ptr, dev = self._ptr(A_shard)
+        assert dev, "attach_A needs a device tensor"
+        self._A_ref = A_shard
+        self._check(_lib.nsrgs_attach_A(self._h, ptr, lda if lda is not None else A_shard.stride(0)))
+
+    def copy_A_rows(self, row0: int, nrows: int) -> np.ndarray:
+        out = np.empty((nrows, self.n * self.d), dtype=self.np_dtype)
+        self._check(_lib.nsrgs_copy_A_rows(self._h, row0, nrows, out.ctypes.data))
+        return out
+
+    def init_spectral(self, seed: int = 0, max_sweeps: int = 200, tol: float = 1e-5, allow_unconverged=False) -> int:
+        sw = ct.c_int(0)
+        s = _lib.nsrgs_init_spectral(self._h, seed, max_sweeps, tol, ct.byref(sw))
+        if s == 8 and allow_unconverged:
+            return sw.value
+        self._check(s)
+        return sw.value
+
+    def step(self, eta: float, K: int) -> float:
+        f = ct.c_double(0.0)
+        self._check(_lib.nsrgs_step(self._h, eta, K, ct.byref(f)))
+        return f.value
+
+    def run(self, T: int, eta: float, K: int, trace: bool = True):
+        buf = (ct.c_double * max(T, 1))() if trace else None
+        self._check(_lib.nsrgs_run(self._h, T, eta, K, buf))
+        return np.array(buf[:T]) if trace else None
+
+    def objective(self) -> float:
+        f = ct.c_double(0.0)
+        self._check(_lib.nsrgs_objective(self._h, ct.byref(f)))
+        return f.value
+
+    def alignment_error(self, Z):
+        out = (ct.c_double * 3)()
+        if isinstance(Z, np.ndarray):
+            Z = np.ascontiguousarray(Z, dtype=self.np_dtype)
+        ptr, dev = self._ptr(Z)
+        self._check(_lib.nsrgs_alignment_error(self._h, ptr, dev, out))
+        return tuple(out)
+
+    def set_X(self, X):
+        if isinstance(X, np.ndarray):
+            X = np.ascontiguousarray(X, dtype=self.np_dtype)
+        ptr, dev = self._ptr(X)
+        self._check(_lib.nsrgs_set_X(self._h, ptr, dev))
+
+    def get_X(self, out=None) -> np.ndarray:
+        if out is None:
+            out = np.empty((self.n, self.d, self.d), dtype=self.np_dtype)
+        ptr, dev = self._ptr(out)
+        self._check(_lib.nsrgs_get_X(self._h, ptr, dev))
+        return out
+
+    def stats(self) -> dict:
+        st = Stats()
+        self._check(_lib.nsrgs_get_stats(self._h, ct.byref(st)))
+        return {k: getattr(st, k) for k, _ in Stats._fields_}
+
+    def reset_stats(self, timing: bool = False):
+        self._check(_lib.nsrgs_reset_stats(self._h, int(timing)))
