@@ -1,0 +1,317 @@
+"""NS-RGS benchmark (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--impl reference]
+
+One "step" = one whole pass of the hot path on the resident synthetic instance of the chosen
+BASELINE.json config: spectral initialisation (subspace iteration on the panel A.X kernel +
+scaled-NS polar), T NS-RGS iterations (fused A.X + gradient/projection/step + K-step
+Newton-Schulz retraction, fused fp64 objective trace) and the alignment metrics.
+value = T * K_steps / (max over ranks of the device time of K_steps solves)  [NS-RGS it/s].
+
+--impl reference times the fp64 oracle (oracle/, as it stands) on the host cores on a bounded
+sample of the same workload (a panel of nodes' block rows; scaled to whole-problem it/s).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {  # BASELINE.json "configs" (seed 0 everywhere, eta = 1/n)
+    "c1": dict(n=100, d=3, sigma=0.5, T=50, K=3),
+    "c2": dict(n=2000, d=3, sigma=0.5, T=100, K=5),
+    "c3": dict(n=20000, d=5, sigma=0.3 * np.sqrt(20000) / 5, T=100, K=5),
+    "c4": dict(n=12000, d=10, sigma=0.2 * np.sqrt(12000) / 10, T=100, K=6),
+    "c5": dict(n=40000, d=5, sigma=0.3 * np.sqrt(40000) / 5, T=100, K=5),
+}
+METRIC = "NS-RGS iterations/sec and effective HBM GB/s (% of roofline) at 1/2/4/8 B200"
+INIT_TOL, INIT_MAX_SWEEPS = 1e-5, 100
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            j = json.load(f)
+        return float(j["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy read+write)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def _traffic(cfg_name):
+    """dram bytes per panel launch from the committed ncu --set full summary, if any."""
+    p = os.path.join(ROOT, "profiles", "ncu_full_summary.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            j = json.load(f)
+        v = j.get(cfg_name, {}).get("dram_bytes_per_launch")
+        return float(v) if v else None
+    return None
+
+
+class Clocks:
+    """nvidia-smi sampler for the timed region (clocks + throttle reasons)."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,power.draw")
+
+    def __init__(self, device):
+        self.device, self.rows, self.proc = device, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), "--query-gpu=" + self.Q,
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 7:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if r[2 + k].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def _dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ------------------------------------------------------------------------------------ oracle
+def _oracle_sample(cfg, nodes_sample, budget_s):
+    """Time oracle.nsrgs.step_rows (Algorithm 2 restricted to a panel of nodes) on this host.
+    Returns (it/s scaled to the whole problem, seconds per sample pass, passes, threads)."""
+    from threadpoolctl import threadpool_info
+
+    from oracle import instance as inst
+    from oracle import nsrgs as ons
+
+    n, d = cfg["n"], cfg["d"]
+    Z = inst.ground_truth(0, n, d)
+    nodes = np.arange(nodes_sample)
+    R = inst.measurement_rows(0, Z, cfg["sigma"], nodes)       # fp32-rounded A rows, fp64 (untimed)
+    X = Z.copy()
+    passes, t0 = 0, time.perf_counter()
+    while True:
+        ons.step_rows(R, X, nodes, 1.0 / n, cfg["K"])
+        passes += 1
+        el = time.perf_counter() - t0
+        if el >= budget_s or passes >= 10000:
+            break
+    per = el / passes
+    threads = max([p.get("num_threads", 1) for p in threadpool_info()] or [1])
+    return (nodes_sample / n) / per, per, passes, threads
+
+
+def run_reference(args, cfg):
+    world, rank, _ = _dist_env()
+    if rank != 0:
+        return
+    n = cfg["n"]
+    m = max(1, min(n, args.sample_nodes))
+    from oracle import instance as inst
+    from oracle import nsrgs as ons
+    from threadpoolctl import threadpool_info
+
+    Z = inst.ground_truth(0, n, cfg["d"])
+    nodes = np.arange(m)
+    R = inst.measurement_rows(0, Z, cfg["sigma"], nodes)
+    for _ in range(args.warmup):
+        ons.step_rows(R, Z, nodes, 1.0 / n, cfg["K"])
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        ons.step_rows(R, Z, nodes, 1.0 / n, cfg["K"])
+    el = time.perf_counter() - t0
+    per = el / args.steps
+    value = (m / n) / per
+    threads = max([p.get("num_threads", 1) for p in threadpool_info()] or [1])
+    sample = (f"oracle.nsrgs.step_rows on {m} of {n} nodes ({m * cfg['d']} of {n * cfg['d']} A rows, fp64), "
+              f"one sample per step; it/s = ({m}/{n}) / seconds per sample")
+    line = {"metric": METRIC, "value": value, "unit": "it/s", "impl": "reference", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": per * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": _config_dict(args, cfg, world),
+            "cpu_baseline": {"value": value, "unit": "it/s", "cores": threads, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": "it/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def _config_dict(args, cfg, world):
+    n, d = cfg["n"], cfg["d"]
+    return {"workload": f"{args.config}: n={n} d={d} sigma={cfg['sigma']:.4f} T={cfg['T']} K={cfg['K']} "
+                        f"eta=1/n seed=0; step = spectral init (tol {INIT_TOL}) + T NS-RGS iterations "
+                        f"(fused objective trace) + alignment metrics",
+            "n": n, "d": d, "N": n * d, "A_bytes_total": 4 * (n * d) ** 2, "parallelism": f"row-block x{world}",
+            "l2": "inputs larger than L2 (A shard >> 126 MB); no flush needed" if 4 * (n * d) ** 2 / world > 2e8
+            else "A shard fits near L2; numbers are L2-assisted (report only)"}
+
+
+# ------------------------------------------------------------------------------------ GPU arm
+def run_gpu(args, cfg):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2604_07372_b200 import nsrgs
+
+    world, rank, local = _dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        idt = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            idt.copy_(torch.frombuffer(bytearray(nsrgs.get_nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(idt, 0)
+        nid = bytes(idt.cpu().numpy().tobytes())
+    else:
+        nid = None
+    n, d, T, K = cfg["n"], cfg["d"], cfg["T"], cfg["K"]
+    eta = 1.0 / n
+    stream = torch.cuda.Stream()
+    s = nsrgs.Solver(n, d, nsrgs.F32, rank=rank, world=world, device=local, nccl_id=nid, stream=stream)
+    Zh = s.generate(0, cfg["sigma"])                     # A shard generated on the device, resident
+    Zd = torch.from_numpy(Zh).to(f"cuda:{local}")
+    Zpin = torch.from_numpy(Zh).pin_memory()
+    Xpin = torch.empty((n, d, d), dtype=torch.float32).pin_memory()
+
+    def solve(e2e=False):
+        sw = s.init_spectral(0, INIT_MAX_SWEEPS, INIT_TOL, allow_unconverged=True)
+        tr = s.run(T, eta, K, trace=True)
+        if e2e:
+            s.get_X(Xpin)                                # D2H of the result (pinned)
+            met = s.alignment_error(Zpin.numpy())        # H2D of the ground truth (pinned)
+        else:
+            met = s.alignment_error(Zd)
+        return sw, tr, met
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def timed(k, e2e):
+        barrier()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        out = None
+        for _ in range(k):
+            out = solve(e2e)
+        ev1.record(stream)
+        barrier()
+        ms = ev0.elapsed_time(ev1)
+        if world > 1:
+            t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms, out
+
+    for _ in range(args.warmup):
+        solve()
+    s.reset_stats(timing=True)
+    with Clocks(local) as clk:
+        ms, (sweeps, trace, met) = timed(args.steps, e2e=False)
+    st = s.stats()
+    clocks = clk.summary()
+    s.reset_stats(timing=False)
+    ms_e2e, _ = timed(args.steps, e2e=True)
+
+    N = n * d
+    rows_local = N // world
+    value = T * args.steps / (ms / 1e3)
+    e2e_value = T * args.steps / (ms_e2e / 1e3)
+    peak, peak_kind = _peaks()
+    bytes_launch = 4 * rows_local * N + 4 * N * d + 4 * rows_local * d
+    avg_ms = st["panel_ms_total"] / max(1, st["panel_launches"])
+    achieved = bytes_launch / (avg_ms / 1e3) / 1e9
+    passes = st["panel_launches"] / args.steps                              # A passes per solve
+    eff_gbs = passes * 4 * rows_local * N * args.steps / (ms / 1e3) / 1e9 * world
+    if rank != 0:
+        s.close()
+        return
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        v, per, passes_c, threads = _oracle_sample(cfg, args.sample_nodes, args.cpu_budget)
+        cpu = {"value": v, "unit": "it/s", "cores": threads, "kind": "oracle",
+               "sample": f"oracle.nsrgs.step_rows on {args.sample_nodes} of {n} nodes "
+                         f"({args.sample_nodes * d} of {N} A rows, fp64), {passes_c} passes in "
+                         f"{passes_c * per:.1f} s; it/s = ({args.sample_nodes}/{n}) / s_per_pass"}
+    traffic = _traffic(args.config)
+    line = {
+        "metric": METRIC, "value": value, "unit": "it/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (on-device Philox instance, PAPER.md §4.1 model)",
+        "config": {**_config_dict(args, cfg, world), "init_sweeps": sweeps},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "peak_kind": peak_kind, "kernel": "panel_kernel (fused A.X + epilogue)",
+                     "bytes_per_launch": bytes_launch, "avg_launch_ms": avg_ms,
+                     "frac_of_nominal_8TBs": achieved / 8000.0},
+        "effective_gbs": eff_gbs, "a_passes_per_step": passes,
+        "e2e": {"value": e2e_value, "unit": "it/s", "h2d_bytes_per_step": 4 * n * d * d,
+                "d2h_bytes_per_step": 4 * n * d * d + 8 * T + 24},
+        "gpu_launches": st["kernel_launches"],
+        "clocks": clocks,
+        "result": {"rel_err": met[0], "d_F": met[1], "mse": met[2], "F_first": float(trace[0]),
+                   "F_last": float(trace[-1]), "ns_region_max": st["ns_region_max"]},
+        "launch": {"grid": st["grid"], "threads": st["threads"], "stages": st["stages"],
+                   "rows_per_panel": st["rows_per_panel"], "splits": st["splits"], "smem": st["smem_bytes"]},
+    }
+    if cpu:
+        line["cpu_baseline"] = cpu
+    print(json.dumps(line), flush=True)
+    s.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default=None, help="c1..c5 (default: c3 at 1-4 GPUs, c5 at 8)")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--sample-nodes", type=int, default=50)
+    ap.add_argument("--cpu-budget", type=float, default=10.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.config is None:
+        args.config = "c3"
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_gpu(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

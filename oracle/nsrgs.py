@@ -78,6 +78,23 @@ def step(A: np.ndarray, X: np.ndarray, mu: float, Ts: int, retraction: str = "ns
     return Xn, F, G
 
 
+def step_rows(A_rows: np.ndarray, X: np.ndarray, nodes, mu: float, Ts: int) -> np.ndarray:
+    """Algorithm 2's update for the listed nodes only, given just their block
+    rows of A (shape (len(nodes)*d, nd)): the same arithmetic as ``step`` restricted to rows
+    i in `nodes` (Jacobi, reads X^t only).  Used for sampled parity at sizes where the dense A
+    does not fit the host, and for the bounded-sample CPU baseline."""
+    n, d, _ = X.shape
+    Xs = stack(X)
+    out = []
+    for k, i in enumerate(nodes):
+        Ai = A_rows[k * d:(k + 1) * d]
+        Aii = Ai[:, i * d:(i + 1) * d]
+        G = (n - 1) * X[i] - (Ai @ Xs - Aii @ X[i])          # sum_{j != i}(X_i - A_ij X_j)
+        F = X[i] - mu * tangent_project(X[i], G)
+        out.append(newton_schulz(F, Ts))
+    return np.stack(out)
+
+
 def step_bruteforce(A, X, mu, Ts):
     """Algorithm 2's inner loop written with explicit Python loops over i, j and matrix
     entries (no numpy matmul).  The oracle's own oracle for n <= 8."""

@@ -44,7 +44,8 @@ struct PanelCfg {
   // shared memory after the stages
   static constexpr int BAR_BYTES = 2 * 8 * 8;                         // up to 8 stages
   static constexpr int SCR_T = 5 * E;                                 // sX sG sH sS sM
-  static constexpr int SCR_BYTES = kWarps * (SCR_T * (int)sizeof(T)) + kWarps * 2 * DD * 8 + kWarps * 2 * 8 + 64;
+  static constexpr int SCR_T_BYTES = (kWarps * SCR_T * (int)sizeof(T) + 15) / 16 * 16;   // keep doubles aligned
+  static constexpr int SCR_BYTES = SCR_T_BYTES + kWarps * 2 * DD * 8 + kWarps * 2 * 8 + 64;
   static constexpr int BUDGET = 220 * 1024;
   static constexpr int STAGES_RAW = (BUDGET - 1024 - BAR_BYTES - SCR_BYTES) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
@@ -70,7 +71,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + C::STAGES * C::STAGE_BYTES);
   uint64_t *empty = full + 8;
   T *scr_all = reinterpret_cast<T *>(smem + C::STAGES * C::STAGE_BYTES + C::BAR_BYTES);
-  double *gram_all = reinterpret_cast<double *>(reinterpret_cast<uint8_t *>(scr_all) + kWarps * C::SCR_T * sizeof(T));
+  double *gram_all = reinterpret_cast<double *>(reinterpret_cast<uint8_t *>(scr_all) + C::SCR_T_BYTES);
   double *red = gram_all + kWarps * 2 * C::DD;       // [kWarps][2]
   int *flag = reinterpret_cast<int *>(red + kWarps * 2);
 
@@ -129,6 +130,31 @@ __global__ void __launch_bounds__(kThreads, 1)
   float ns_region = 0.f;
   int err = 0;
   const T coef = (T)p.coef, eta = (T)p.eta;
+
+  // Split-K: the CTA that runs a panel's epilogue depends on arrival order, so its fp64
+  // partials go to a per-(panel, warp) slot (summed later in fixed order) for bitwise
+  // determinism.  Without splits the static schedule makes per-CTA sums deterministic.
+  auto flush_panel = [&](int panel) {
+    if (p.splits > 1) {
+      __syncwarp();
+      const double so = warp_sum(s_own), xs = warp_sum(xb);
+      double *slot = p.cta_part + ((int64_t)panel * kWarps + warp) * C::NPART;
+#pragma unroll
+      for (int m = 0; m < C::DDL; ++m) {
+        const int e = lane + 32 * m;
+        if (e < C::DD) {
+          __stcg(slot + e, gram1[e]);
+          __stcg(slot + C::DD + e, gram2[e]);
+          gram1[e] = 0.0;
+          gram2[e] = 0.0;
+        }
+      }
+      if (lane == 0) { __stcg(slot + 2 * C::DD, so); __stcg(slot + 2 * C::DD + 1, xs); }
+      s_own = 0.0;
+      xb = 0.0;
+      __syncwarp();
+    }
+  };
 
   int stage = 0;
   uint32_t phase = 0;
@@ -263,7 +289,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           gram2[e2] += g2;
         }
       }
-      __syncwarp();
+      flush_panel(panel);
       continue;
     } else {
       // <X, B> and the X Gram terms of the objective expansion.
@@ -290,7 +316,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       if constexpr (MODE == kModeObjective) {
-        __syncwarp();
+        flush_panel(panel);
         continue;
       }
       // G = (n-1) X - B   (in place in sG)
@@ -394,6 +420,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
+      flush_panel(panel);
       __syncwarp();
     }
   }
@@ -406,19 +433,21 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     if (lane == 0 && mx > 0.f) atomicMax(p.ns_region, __float_as_uint(mx));
   }
-  s_own = warp_sum(s_own);
-  xb = warp_sum(xb);
-  if (lane == 0) { red[warp * 2] = s_own; red[warp * 2 + 1] = xb; }
-  named_bar_sync(1, kWarps * 32);
-  double *cp = p.cta_part + (int64_t)blockIdx.x * C::NPART;
-  for (int i = threadIdx.x; i < C::NPART; i += kWarps * 32) {
-    double v = 0.0;
-    if (i < 2 * C::DD) {
-      for (int w = 0; w < kWarps; ++w) v += gram_all[w * 2 * C::DD + i];
-    } else {
-      for (int w = 0; w < kWarps; ++w) v += red[w * 2 + (i - 2 * C::DD)];
+  if (p.splits == 1) {
+    s_own = warp_sum(s_own);
+    xb = warp_sum(xb);
+    if (lane == 0) { red[warp * 2] = s_own; red[warp * 2 + 1] = xb; }
+    named_bar_sync(1, kWarps * 32);
+    double *cp = p.cta_part + (int64_t)blockIdx.x * C::NPART;
+    for (int i = threadIdx.x; i < C::NPART; i += kWarps * 32) {
+      double v = 0.0;
+      if (i < 2 * C::DD) {
+        for (int w = 0; w < kWarps; ++w) v += gram_all[w * 2 * C::DD + i];
+      } else {
+        for (int w = 0; w < kWarps; ++w) v += red[w * 2 + (i - 2 * C::DD)];
+      }
+      __stcg(cp + i, v);
     }
-    __stcg(cp + i, v);
   }
   __threadfence();
   named_bar_sync(1, kWarps * 32);
@@ -428,7 +457,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     __threadfence();
     for (int i = threadIdx.x; i < C::NPART; i += kWarps * 32) {
       double v = 0.0;
-      for (int b = 0; b < (int)gridDim.x; ++b) v += __ldcg(p.cta_part + (int64_t)b * C::NPART + i);
+      const int nslots = p.splits > 1 ? p.panels * kWarps : (int)gridDim.x;
+      for (int b = 0; b < nslots; ++b) v += __ldcg(p.cta_part + (int64_t)b * C::NPART + i);
       p.result[i] = v;
     }
     if (threadIdx.x == 0) *p.done_cnt = 0u;

@@ -461,7 +461,7 @@ int nsrgs_create(const nsrgs_desc *desc, nsrgs_ctx **out) {
   };
   const size_t xb = c->esz * (size_t)c->plan.x_elems;
   bool ok = alloc(&c->X[0], xb) && alloc(&c->X[1], xb) && alloc(&c->stage, c->esz * (size_t)(c->n * c->d * c->d)) &&
-            alloc((void **)&c->cta_part, sizeof(double) * c->grid * c->shape.npart) &&
+            alloc((void **)&c->cta_part, sizeof(double) * std::max(c->grid, c->panels * kWarps) * c->shape.npart) &&
             alloc((void **)&c->counters, sizeof(unsigned) * (c->panels + 1)) &&
             alloc((void **)&c->err, sizeof(int)) && alloc((void **)&c->ns_region, sizeof(unsigned));
   if (ok && c->splits > 1) ok = alloc(&c->Bpart, c->esz * (size_t)c->units * c->shape.rows * c->d);

@@ -1,0 +1,27 @@
+"""Helpers shared by the -m gpu parity tests: oracle-side per-node step (sampled parity) and
+rotation-aligned comparison.  Everything here calls only oracle/ (NumPy fp64)."""
+import numpy as np
+
+from oracle import nsrgs as ons
+
+
+def rel_fro(a, b):
+    return float(np.linalg.norm(np.asarray(a, np.float64) - np.asarray(b, np.float64)) / np.linalg.norm(b))
+
+
+def rel_mod_rotation(X, Xref):
+    """min_Q ||X - Xref Q||_F / ||Xref||_F (Q* = sgn(Xref^T X))."""
+    d = X.shape[-1]
+    Xs, Rs = np.asarray(X, np.float64).reshape(-1, d), np.asarray(Xref, np.float64).reshape(-1, d)
+    Q = ons.sgn(Rs.T @ Xs)
+    return float(np.linalg.norm(Xs - Rs @ Q) / np.linalg.norm(Rs))
+
+
+def oracle_node_step(A_rows, X, nodes, mu, Ts):
+    return ons.step_rows(A_rows, X, nodes, mu, Ts)
+
+
+def oracle_iterate_near(Z, noise, seed):
+    """An oracle-side iterate X = sgn(Z_i + noise * N(0,1)) (blockwise), fp64."""
+    rng = np.random.default_rng(seed)
+    return ons.sgn(Z + noise * rng.standard_normal(Z.shape))

@@ -1,0 +1,271 @@
+"""GPU parity: libnsrgs.so (through the C-ABI binding) vs the fp64 oracle on identical
+seeded inputs.  Tolerances:
+  * one step from a shared X^t: relative Frobenius <= 1e-6 (fp32), 1e-12 (fp64);
+  * T steps from a shared X^0: <= 1e-4 (north star), end to end modulo the global O(d)
+    rotation (reading R7) <= 1e-4, alignment metrics within 1e-3 relative;
+  * generator: fp32 values within 1 ulp (rare libm-vs-CUDA transcendental ulps), Z to 1e-12.
+"""
+import numpy as np
+import pytest
+
+from oracle import instance as inst
+from oracle import metrics as mt
+from oracle import nsrgs as ons
+from tests.gpu_helpers import oracle_iterate_near, oracle_node_step, rel_fro, rel_mod_rotation
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def nsrgs():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2604_07372_b200 import nsrgs as mod
+
+    return mod
+
+
+def _dt(nsrgs, dtype):
+    return (nsrgs.F32, np.float32) if dtype == "f32" else (nsrgs.F64, np.float64)
+
+
+# ---------------------------------------------------------------------------- generator (a0)
+@pytest.mark.parametrize("n,d,sigma,dtype", [(100, 3, 0.5, "f32"), (100, 3, 0.5, "f64"), (37, 5, 1.3, "f32"),
+                                             (21, 10, 0.7, "f32"), (9, 2, 2.0, "f64"), (40, 7, 0.0, "f32")])
+def test_generator_matches_oracle(nsrgs, n, d, sigma, dtype):
+    code, npdt = _dt(nsrgs, dtype)
+    s = nsrgs.Solver(n, d, code)
+    Zg = s.generate(11, sigma)
+    Z = inst.ground_truth(11, n, d)
+    assert np.max(np.abs(Zg.astype(np.float64) - Z)) <= (1e-12 if dtype == "f64" else 6e-8)
+    A = inst.measurement_matrix(11, Z, sigma, dtype=npdt)
+    Ag = s.copy_A_rows(0, n * d).astype(np.float64)
+    diff = np.abs(Ag - A)
+    if dtype == "f64":
+        assert diff.max() <= 1e-13 * max(1.0, np.abs(A).max())
+    else:
+        ulp = np.spacing(np.abs(A).astype(np.float32)).astype(np.float64)
+        assert np.all(diff <= ulp)                  # at most one fp32 ulp
+        assert np.count_nonzero(diff) <= max(2, A.size // 10000)
+    st = s.stats()
+    assert abs(st["a_fro2"] - np.sum(Ag * Ag)) <= 1e-12 * np.sum(Ag * Ag)
+    s.close()
+
+
+def test_generator_sampled_rows_c2(nsrgs):
+    n, d, sigma = 2000, 3, 2.0
+    s = nsrgs.Solver(n, d)
+    s.generate(0, sigma, want_Z=False)
+    Z = inst.ground_truth(0, n, d)
+    nodes = [0, 1, 777, 1024, 1999]
+    R = inst.measurement_rows(0, Z, sigma, nodes)
+    for k, i in enumerate(nodes):
+        G = s.copy_A_rows(i * d, d).astype(np.float64)
+        ulp = np.spacing(np.abs(R[k * d:(k + 1) * d]).astype(np.float32)).astype(np.float64)
+        assert np.all(np.abs(G - R[k * d:(k + 1) * d]) <= ulp)
+    s.close()
+
+
+# ---------------------------------------------------------------------------- one step (a3-a6)
+STEP_CASES = [  # n, d, sigma, K, dtype   (ragged N, tiny n, every d, split-K and plain paths)
+    (2, 2, 0.3, 3, "f32"), (7, 3, 0.5, 5, "f32"), (100, 3, 0.5, 3, "f32"), (100, 3, 0.5, 3, "f64"),
+    (43, 5, 1.0, 5, "f32"), (60, 10, 0.8, 6, "f32"), (37, 7, 0.6, 4, "f32"), (50, 4, 1.5, 2, "f32"),
+    (33, 6, 0.9, 5, "f64"), (29, 9, 0.4, 3, "f32"), (31, 8, 0.7, 4, "f32"), (26, 2, 0.2, 1, "f64"),
+    (500, 3, 2.0, 5, "f32"), (45, 6, 0.5, 0, "f32"), (64, 5, 0.5, 12, "f64"),
+]
+
+
+@pytest.mark.parametrize("n,d,sigma,K,dtype", STEP_CASES)
+def test_step_from_shared_iterate(nsrgs, n, d, sigma, K, dtype):
+    code, npdt = _dt(nsrgs, dtype)
+    s = nsrgs.Solver(n, d, code)
+    s.generate(5, sigma, want_Z=False)
+    Z = inst.ground_truth(5, n, d)
+    A = inst.measurement_matrix(5, Z, sigma, dtype=npdt)
+    X = oracle_iterate_near(Z, 0.2, 1).astype(npdt)
+    s.set_X(X)
+    eta = 1.0 / n
+    f_gpu = s.step(eta, K)
+    Xo, _, _ = ons.step(A, X.astype(np.float64), eta, K)
+    tol = 1e-6 if dtype == "f32" else 1e-12
+    assert rel_fro(s.get_X(), Xo) <= tol
+    fo = ons.objective(A, X.astype(np.float64))
+    assert abs(f_gpu - fo) <= (2e-6 if dtype == "f32" else 1e-10) * fo
+    s.close()
+
+
+@pytest.mark.parametrize("n,d,sigma,K,T,dtype", [(100, 3, 0.5, 3, 50, "f32"), (100, 3, 0.5, 3, 50, "f64"),
+                                                 (80, 5, 1.0, 5, 30, "f32"), (40, 10, 0.5, 6, 20, "f32")])
+def test_T_steps_from_shared_X0_and_objective_trace(nsrgs, n, d, sigma, K, T, dtype):
+    code, npdt = _dt(nsrgs, dtype)
+    s = nsrgs.Solver(n, d, code)
+    s.generate(0, sigma, want_Z=False)
+    Z = inst.ground_truth(0, n, d)
+    A = inst.measurement_matrix(0, Z, sigma, dtype=npdt)
+    X0, _, _ = ons.spectral_init(A, d)
+    X0 = X0.astype(npdt)
+    s.set_X(X0)
+    trace = s.run(T, 1.0 / n, K)
+    Xo, to = ons.run(A, X0.astype(np.float64), T, 1.0 / n, K, trace_objective=True)
+    assert rel_fro(s.get_X(), Xo) <= (1e-4 if dtype == "f32" else 1e-11)
+    to = np.array(to)
+    assert np.max(np.abs(trace - to) / to) <= (2e-6 if dtype == "f32" else 1e-10)
+    assert s.objective() == pytest.approx(ons.objective(A, Xo), rel=2e-6 if dtype == "f32" else 1e-10)
+    s.close()
+
+
+def test_attach_oracle_matrix(nsrgs):
+    """A supplied by the oracle (never touched by the CUDA generator) through attach_A."""
+    import torch
+
+    n, d, sigma, K = 90, 4, 0.7, 4
+    Z = inst.ground_truth(3, n, d)
+    A = inst.measurement_matrix(3, Z, sigma).astype(np.float32)
+    Ad = torch.from_numpy(A).cuda()
+    s = nsrgs.Solver(n, d)
+    s.attach_A(Ad)
+    X = oracle_iterate_near(Z, 0.1, 2).astype(np.float32)
+    s.set_X(X)
+    s.run(5, 1.0 / n, K, trace=False)
+    Xo = ons.run(A.astype(np.float64), X.astype(np.float64), 5, 1.0 / n, K)
+    assert rel_fro(s.get_X(), Xo) <= 1e-6
+    assert s.stats()["a_fro2"] == pytest.approx(float(np.sum(A.astype(np.float64) ** 2)), rel=1e-12)
+    s.close()
+
+
+# ---------------------------------------------------------------------------- spectral init + end to end
+@pytest.mark.parametrize("n,d,sigma,K,T,dtype", [(100, 3, 0.5, 3, 50, "f32"), (100, 3, 0.5, 3, 50, "f64"),
+                                                 (2000, 3, 0.5, 5, 100, "f32"), (2000, 3, 2.0, 5, 100, "f32"),
+                                                 (2000, 3, 8.0, 5, 100, "f32")])
+def test_end_to_end_modulo_rotation(nsrgs, n, d, sigma, K, T, dtype):
+    """BASELINE c1 (fp32 and fp64) and c2 (sigma in {0.5, 2, 8}): spectral init + T iterations."""
+    code, npdt = _dt(nsrgs, dtype)
+    s = nsrgs.Solver(n, d, code)
+    Zg = s.generate(0, sigma)
+    Z = inst.ground_truth(0, n, d)
+    A = inst.measurement_matrix(0, Z, sigma, dtype=npdt)
+    s.init_spectral(0, 400, 1e-6 if dtype == "f32" else 1e-12, allow_unconverged=(dtype == "f32"))
+    if n <= 200:
+        X0, _, _ = ons.spectral_init(A, d, "eigh")
+    else:
+        X0, _, _ = ons.spectral_init(A, d, "subspace", Y0=inst.initial_subspace(0, n, d), tol=1e-12)
+    assert rel_mod_rotation(s.get_X(), X0) <= (1e-4 if dtype == "f32" else 1e-10)
+    s.run(T, 1.0 / n, K, trace=False)
+    Xo = ons.run(A, X0, T, 1.0 / n, K)
+    assert rel_mod_rotation(s.get_X(), Xo) <= 1e-4
+    r_gpu = np.array(s.alignment_error(Zg))
+    r_orc = np.array(mt.alignment_error(Xo, Z))
+    assert np.all(np.abs(r_gpu - r_orc) <= 1e-3 * r_orc)
+    # first-order closed form Rel.Err ~ sigma sqrt((d-1)/n), +-10% sanity band
+    assert abs(r_gpu[0] - sigma * np.sqrt((d - 1) / n)) <= 0.1 * r_gpu[0]
+    s.close()
+
+
+def test_alignment_metrics_on_oracle_iterate(nsrgs):
+    n, d = 300, 5
+    Z = inst.ground_truth(4, n, d)
+    X = oracle_iterate_near(Z, 0.3, 9)
+    s = nsrgs.Solver(n, d, nsrgs.F64)
+    s.generate(4, 1.0, want_Z=False)
+    s.set_X(X)
+    r = np.array(s.alignment_error(Z))
+    ro = np.array(mt.alignment_error(X, Z))
+    assert np.all(np.abs(r - ro) <= 1e-10 * ro)
+    s.close()
+
+
+# ---------------------------------------------------------------------------- edge cases
+def test_noiseless_exact_recovery(nsrgs):
+    n, d = 200, 3
+    s = nsrgs.Solver(n, d)
+    Z = s.generate(1, 0.0)
+    s.init_spectral(1, 100, 1e-6, allow_unconverged=True)
+    s.run(5, 1.0 / n, 5, trace=False)
+    rel, dF, mse = s.alignment_error(Z)
+    assert rel < 1e-5 and dF < 1e-4 * np.sqrt(n * d)
+
+
+def test_divergence_and_state_errors(nsrgs):
+    n, d = 50, 3
+    s = nsrgs.Solver(n, d)
+    with pytest.raises(nsrgs.NSRGSError) as e:
+        s.step(1.0 / n, 3)
+    assert e.value.name == "STATE"
+    Z = s.generate(2, 0.3)
+    s.set_X((10.0 * Z).astype(np.float32))     # far outside the NS region (sigma > sqrt 3)
+    with pytest.raises(nsrgs.NSRGSError) as e:
+        s.run(2, 1.0 / n, 8)
+    assert e.value.name == "DIVERGENCE"
+    bad = Z.copy()
+    bad[3, 1, 1] = np.nan
+    s.set_X(bad)
+    with pytest.raises(nsrgs.NSRGSError) as e:
+        s.step(1.0 / n, 3)
+    assert e.value.name in ("DIVERGENCE", "NONFINITE")
+    s.close()
+
+
+@pytest.mark.parametrize("kw", [dict(n=1, d=3), dict(n=10, d=1), dict(n=10, d=11), dict(n=10, d=7, dtype=1)])
+def test_create_rejects_unsupported(nsrgs, kw):
+    with pytest.raises(nsrgs.NSRGSError) as e:
+        nsrgs.Solver(**kw)
+    assert e.value.name == "INVALID_ARG"
+
+
+def test_deterministic_bitwise(nsrgs):
+    n, d = 700, 5
+    out = []
+    for _ in range(2):
+        s = nsrgs.Solver(n, d)
+        s.generate(8, 1.0, want_Z=False)
+        s.init_spectral(8, 50, 1e-5, allow_unconverged=True)
+        tr = s.run(10, 1.0 / n, 5)
+        out.append((s.get_X(), tr))
+        s.close()
+    assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1])
+
+
+# ---------------------------------------------------------------------------- full sizes, sampled
+FULL = {  # BASELINE.json configs[2], configs[3] in the launch configuration bench.py times
+    "c3": (20000, 5, 0.3 * np.sqrt(20000) / 5, 5),
+    "c4": (12000, 10, 0.2 * np.sqrt(12000) / 10, 6),
+    "mid": (6000, 3, 1.0, 5),       # panels >= #SMs: no split-K
+}
+
+
+@pytest.mark.parametrize("cfg", ["mid", "c3", "c4"])
+def test_full_size_sampled_step(nsrgs, cfg):
+    n, d, sigma, K = FULL[cfg]
+    s = nsrgs.Solver(n, d)
+    s.generate(0, sigma, want_Z=False)
+    Z = inst.ground_truth(0, n, d)
+    X = oracle_iterate_near(Z, 0.05, 3).astype(np.float32)
+    s.set_X(X)
+    s.step(1.0 / n, K)
+    Xg = s.get_X()
+    nodes = np.unique(np.r_[0, n - 1, np.random.default_rng(1).integers(0, n, 14)])
+    R = inst.measurement_rows(0, Z, sigma, nodes)
+    Xo = oracle_node_step(R, X.astype(np.float64), nodes, 1.0 / n, K)
+    assert rel_fro(Xg[nodes], Xo) <= 1e-5
+    s.close()
+
+
+@pytest.mark.parametrize("cfg", ["c3", "c4"])
+def test_full_size_run_properties(nsrgs, cfg):
+    n, d, sigma, K = FULL[cfg]
+    s = nsrgs.Solver(n, d)
+    Z = s.generate(0, sigma)
+    s.init_spectral(0, 100, 1e-5, allow_unconverged=True)
+    s.reset_stats()
+    tr = s.run(100, 1.0 / n, K)
+    st = s.stats()
+    assert st["ns_region_max"] < 1.0                     # eq:conclusion:sigma
+    assert np.all(np.diff(tr) <= 1e-6 * tr[0])           # F non-increasing up to fp32 noise
+    X = s.get_X().astype(np.float64)
+    assert np.max(np.abs(np.einsum("nka,nkb->nab", X, X) - np.eye(d))) < 1e-5   # X in O(d)^n
+    rel, dF, mse = s.alignment_error(Z)
+    assert abs(rel - sigma * np.sqrt((d - 1) / n)) <= 0.1 * rel
+    assert abs(mse - dF ** 2 / n) <= 1e-9 * mse
+    s.close()

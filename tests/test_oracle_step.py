@@ -138,3 +138,14 @@ def test_ns_region_and_descent():
         f = ns.objective(A, X)
         assert f <= f_prev * (1 + 1e-13)
         f_prev = f
+
+
+def test_step_rows_equals_full_step():
+    n, d, sigma = 30, 4, 0.9
+    Z = inst.ground_truth(8, n, d)
+    A = inst.measurement_matrix(8, Z, sigma)
+    X = _stack_haar(np.random.default_rng(5), n, d)
+    Xfull, _, _ = ns.step(A, X, 1.0 / n, 3)
+    nodes = [0, 7, 29]
+    R = inst.measurement_rows(8, Z, sigma, nodes)
+    assert np.max(np.abs(ns.step_rows(R, X, nodes, 1.0 / n, 3) - Xfull[nodes])) < 1e-13
