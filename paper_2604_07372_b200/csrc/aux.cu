@@ -146,8 +146,22 @@ __global__ void sumsq_kernel(const T *A, int64_t rows, int64_t cols, int64_t lda
   if (threadIdx.x == 0) part[(int64_t)blockIdx.y * gridDim.x + blockIdx.x] = t;
 }
 
-// out[i] = sum_b part[b * width + i], fixed order (deterministic).
+// out[i] = sum_b part[b * width + i] in a fixed order (deterministic).  width == 1: 1024
+// threads take strided slices, then a fixed-shape tree; width > 1: one thread per column.
 __global__ void reduce_kernel(const double *part, int nblocks, int width, double *out) {
+  if (width == 1) {
+    __shared__ double sh[1024];
+    double v = 0.0;
+    for (int b = threadIdx.x; b < nblocks; b += blockDim.x) v += part[b];
+    sh[threadIdx.x] = v;
+    __syncthreads();
+    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+      if ((int)threadIdx.x < s) sh[threadIdx.x] += sh[threadIdx.x + s];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) out[0] = sh[0];
+    return;
+  }
   for (int i = threadIdx.x; i < width; i += blockDim.x) {
     double v = 0.0;
     for (int b = 0; b < nblocks; ++b) v += part[(int64_t)b * width + i];
@@ -473,7 +487,7 @@ cudaError_t launch_sumsq(int dtype, const void *A, int64_t rows, int64_t cols, i
 }
 
 cudaError_t launch_reduce(const double *part, int nblocks, int width, double *out, cudaStream_t s) {
-  reduce_kernel<<<1, 256, 0, s>>>(part, nblocks, width, out);
+  reduce_kernel<<<1, width == 1 ? 1024 : 256, 0, s>>>(part, nblocks, width, out);
   return cudaGetLastError();
 }
 
