@@ -283,7 +283,8 @@ def run_gpu(args, cfg):
         "result": {"rel_err": met[0], "d_F": met[1], "mse": met[2], "F_first": float(trace[0]),
                    "F_last": float(trace[-1]), "ns_region_max": st["ns_region_max"]},
         "launch": {"grid": st["grid"], "threads": st["threads"], "stages": st["stages"],
-                   "rows_per_panel": st["rows_per_panel"], "splits": st["splits"], "smem": st["smem_bytes"]},
+                   "rows_per_panel": st["rows_per_panel"], "panels": st["panels"],
+                   "cut_panels": st["cut_panels"], "smem": st["smem_bytes"]},
     }
     if cpu:
         line["cpu_baseline"] = cpu

@@ -162,7 +162,8 @@ int nsrgs_get_X(nsrgs_ctx *ctx, void *X, int on_device);
 
 /* Launch configuration + measurement hooks (bench / tests).  */
 typedef struct {
-  int32_t grid, threads, stages, rows_per_panel, splits;   /* panel kernel launch shape      */
+  int32_t grid, threads, stages, rows_per_panel;     /* panel kernel launch shape              */
+  int32_t cut_panels;   /* panels split across CTAs by the stream-K schedule (combined in order) */
   int64_t panels, smem_bytes;
   double panel_ms_total;        /* summed CUDA-event time of panel kernel launches since reset */
   int64_t panel_launches;       /* number of panel kernel launches since reset                 */

@@ -16,9 +16,9 @@ constexpr int kThreads = 32 * (kWarps + 1);   // + 1 TMA producer warp
 struct PanelParams {
   const void *X;        // tile layout, input iterate X^t (or Y for the subspace sweep)
   void *Xout;           // tile layout, output X^{t+1} (RGS) or W = A Y (PRODUCT)
-  void *Bpart;          // split-K partials [unit][rows_per_panel][d] (splits > 1)
-  unsigned *panel_cnt;  // split-K arrival counters [panels]
-  double *cta_part;     // per-CTA fp64 partials [grid][npart]
+  void *Bpart;          // stream-K partial B of cut panels [grid][2][rows_per_panel][d]
+  unsigned *panel_cnt;  // arrival counters of cut panels [panels]
+  double *cta_part;     // fp64 partials: [grid][npart] per CTA, then [grid][npart] cut panels (zeroed once)
   unsigned *done_cnt;   // CTA arrival counter for the last-CTA reduction
   double *result;       // npart doubles: reduced partials of this launch
   int *err;             // device error word (bit flags, see kErr*)
@@ -27,7 +27,8 @@ struct PanelParams {
   int64_t n_local, node0, rows_local;
   int64_t tiles_per_rank;
   int world, rank;
-  int panels, splits, tiles_per_split, total_tiles, units;
+  int panels, total_tiles;   // total_tiles = column tiles per panel (all ranks' slices)
+  int64_t steps;             // stream-K work = panels * total_tiles
   double coef;          // n - 1   (identity term of G_i)
   double eta;           // step size mu
   int K;                // Newton-Schulz steps (Algorithm 1)

@@ -45,7 +45,7 @@ struct PanelCfg {
   static constexpr int BAR_BYTES = 2 * 8 * 8;                         // up to 8 stages
   static constexpr int SCR_T = 5 * E;                                 // sX sG sH sS sM
   static constexpr int SCR_T_BYTES = (kWarps * SCR_T * (int)sizeof(T) + 15) / 16 * 16;   // keep doubles aligned
-  static constexpr int SCR_BYTES = SCR_T_BYTES + kWarps * 2 * DD * 8 + kWarps * 2 * 8 + 64;
+  static constexpr int SCR_BYTES = SCR_T_BYTES + kWarps * 2 * DD * 8 + kWarps * 2 * 8 + kWarps * NPART * 8 + 64;
   static constexpr int BUDGET = 220 * 1024;
   static constexpr int STAGES_RAW = (BUDGET - 1024 - BAR_BYTES - SCR_BYTES) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
@@ -61,6 +61,17 @@ template <typename T> __device__ __forceinline__ T warp_sum(T v) {
   return v;
 }
 
+// Stream-K schedule: the panels x tiles steps are cut into gridDim.x equal contiguous ranges.
+__device__ __forceinline__ int64_t sk_bound(int64_t W, int G, int b) { return W * b / G; }
+// CTA whose range contains step s: max b with sk_bound(b) <= s.
+__device__ __forceinline__ int sk_owner(int64_t s, int64_t W, int G) { return (int)(((s + 1) * G + W - 1) / W - 1); }
+// Column-tile order within a panel: this rank's own X slice first (ready earliest under P > 1).
+__device__ __forceinline__ int tile_of_step(int t, const PanelParams &p) {
+  const int tpr = (int)p.tiles_per_rank;
+  const int g = t / tpr;
+  return ((g + p.rank) % p.world) * tpr + (t - g * tpr);
+}
+
 template <typename T, int D, int MODE>
 __global__ void __launch_bounds__(kThreads, 1)
     panel_kernel(const __grid_constant__ CUtensorMap tmA, const PanelParams p) {
@@ -73,7 +84,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   T *scr_all = reinterpret_cast<T *>(smem + C::STAGES * C::STAGE_BYTES + C::BAR_BYTES);
   double *gram_all = reinterpret_cast<double *>(reinterpret_cast<uint8_t *>(scr_all) + C::SCR_T_BYTES);
   double *red = gram_all + kWarps * 2 * C::DD;       // [kWarps][2]
-  int *flag = reinterpret_cast<int *>(red + kWarps * 2);
+  double *xred = red + kWarps * 2;                   // [kWarps][NPART] cut-panel pre-reduction
+  int *flag = reinterpret_cast<int *>(xred + kWarps * C::NPART);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -94,20 +106,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t pol_a = policy_evict_first(), pol_x = policy_evict_last();
       int stage = 0;
       uint32_t phase = 0;
-      for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
-        const int panel = u / p.splits, split = u - panel * p.splits;
-        const int t0 = split * p.tiles_per_split;
-        const int t1 = min(p.total_tiles, t0 + p.tiles_per_split);
-        const int row0 = panel * C::ROWS;
-        for (int t = t0; t < t1; ++t) {
-          const int g = t / (int)p.tiles_per_rank, jt = t - g * (int)p.tiles_per_rank;
-          mbar_wait(&empty[stage], phase ^ 1u);
-          uint8_t *sb = smem + stage * C::STAGE_BYTES;
-          mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
-          tma_load_3d(sb, &tmA, &full[stage], jt * kColTile, g, row0, pol_a);
-          bulk_load(sb + C::A_BYTES, Xg + (int64_t)t * D * kColTile, C::X_BYTES, &full[stage], pol_x);
-          if (++stage == C::STAGES) { stage = 0; phase ^= 1u; }
-        }
+      const int64_t s_end = sk_bound(p.steps, gridDim.x, blockIdx.x + 1);
+      for (int64_t st = sk_bound(p.steps, gridDim.x, blockIdx.x); st < s_end; ++st) {
+        const int panel = (int)(st / p.total_tiles), t = (int)(st - (int64_t)panel * p.total_tiles);
+        const int tt = tile_of_step(t, p);
+        const int g = tt / (int)p.tiles_per_rank, jt = tt - g * (int)p.tiles_per_rank;
+        mbar_wait(&empty[stage], phase ^ 1u);
+        uint8_t *sb = smem + stage * C::STAGE_BYTES;
+        mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
+        tma_load_3d(sb, &tmA, &full[stage], jt * kColTile, g, panel * C::ROWS, pol_a);
+        bulk_load(sb + C::A_BYTES, Xg + (int64_t)tt * D * kColTile, C::X_BYTES, &full[stage], pol_x);
+        if (++stage == C::STAGES) { stage = 0; phase ^= 1u; }
       }
     }
     return;
@@ -131,37 +140,57 @@ __global__ void __launch_bounds__(kThreads, 1)
   int err = 0;
   const T coef = (T)p.coef, eta = (T)p.eta;
 
-  // Split-K: the CTA that runs a panel's epilogue depends on arrival order, so its fp64
-  // partials go to a per-(panel, warp) slot (summed later in fixed order) for bitwise
-  // determinism.  Without splits the static schedule makes per-CTA sums deterministic.
-  auto flush_panel = [&](int panel) {
-    if (p.splits > 1) {
-      __syncwarp();
-      const double so = warp_sum(s_own), xs = warp_sum(xb);
-      double *slot = p.cta_part + ((int64_t)panel * kWarps + warp) * C::NPART;
+  // Objective / Gram partials.  A panel whose tiles all lie in this CTA's stream-K range is
+  // finished here by construction (static) and accumulates into the per-CTA running sums; a
+  // panel cut by a CTA boundary is finished by whichever covering CTA arrives last, so its
+  // contribution goes to a per-(panel, warp) slot and is summed later in a fixed order
+  // (bitwise-deterministic results).
+  auto commit = [&](bool split_panel, int panel, const double *g1, const double *g2, double so, double xs) {
+    if (!split_panel) {
 #pragma unroll
       for (int m = 0; m < C::DDL; ++m) {
         const int e = lane + 32 * m;
-        if (e < C::DD) {
-          __stcg(slot + e, gram1[e]);
-          __stcg(slot + C::DD + e, gram2[e]);
-          gram1[e] = 0.0;
-          gram2[e] = 0.0;
-        }
+        if (e < C::DD) { gram1[e] += g1[m]; gram2[e] += g2[m]; }
       }
-      if (lane == 0) { __stcg(slot + 2 * C::DD, so); __stcg(slot + 2 * C::DD + 1, xs); }
-      s_own = 0.0;
-      xb = 0.0;
-      __syncwarp();
+      s_own += so;
+      xb += xs;
+      return;
     }
+    // all consumer warps finish the same cut panel together: pre-reduce across warps in smem
+    // (fixed warp order), one global slot per cut panel, indexed by the first CTA whose range
+    // starts inside it.
+    so = warp_sum(so);
+    xs = warp_sum(xs);
+    double *xw = xred + warp * C::NPART;
+#pragma unroll
+    for (int m = 0; m < C::DDL; ++m) {
+      const int e = lane + 32 * m;
+      if (e < C::DD) { xw[e] = g1[m]; xw[C::DD + e] = g2[m]; }
+    }
+    if (lane == 0) { xw[2 * C::DD] = so; xw[2 * C::DD + 1] = xs; }
+    named_bar_sync(1, kWarps * 32);
+    const int slot_cta = sk_owner((int64_t)panel * p.total_tiles, p.steps, gridDim.x) + 1;
+    double *slot = p.cta_part + ((int64_t)gridDim.x + slot_cta) * C::NPART;
+    for (int i = threadIdx.x; i < C::NPART; i += kWarps * 32) {
+      double v = 0.0;
+      for (int w = 0; w < kWarps; ++w) v += xred[w * C::NPART + i];
+      __stcg(slot + i, v);
+    }
+    named_bar_sync(1, kWarps * 32);
   };
 
   int stage = 0;
   uint32_t phase = 0;
-  for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
-    const int panel = u / p.splits, split = u - panel * p.splits;
-    const int t0 = split * p.tiles_per_split;
-    const int t1 = min(p.total_tiles, t0 + p.tiles_per_split);
+  const int64_t my_s0 = sk_bound(p.steps, gridDim.x, blockIdx.x);
+  const int64_t my_s1 = sk_bound(p.steps, gridDim.x, blockIdx.x + 1);
+  const int first_panel = (int)(my_s0 / p.total_tiles);
+  for (int64_t st = my_s0; st < my_s1;) {
+    const int panel = (int)(st / p.total_tiles);
+    const int t0 = (int)(st - (int64_t)panel * p.total_tiles);
+    const int64_t t1l = t0 + (my_s1 - st);
+    const int t1 = t1l < p.total_tiles ? (int)t1l : p.total_tiles;
+    st += t1 - t0;
+    const bool split_panel = !(t0 == 0 && t1 == p.total_tiles);
 
     T acc[C::RT][D];
 #pragma unroll
@@ -200,18 +229,23 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
       for (int k = 0; k < D; ++k) acc[r][k] = warp_sum(acc[r][k]);
 
-    if (p.splits > 1) {
-      T *bp = static_cast<T *>(p.Bpart) + ((int64_t)u * C::ROWS + warp * C::RT) * D;
+    if (split_panel) {
+      // partial B of this segment -> slot (CTA, first|last segment); the last covering CTA
+      // to arrive sums all segments in CTA order and runs the epilogue.
+      const int which = (panel == first_panel) ? 0 : 1;
+      T *bp = static_cast<T *>(p.Bpart) + (((int64_t)blockIdx.x * 2 + which) * C::ROWS + warp * C::RT) * D;
 #pragma unroll
       for (int r = 0; r < C::RT; ++r)
 #pragma unroll
         for (int k = 0; k < D; ++k)
           if (((r * D + k) & 31) == lane) __stcg(bp + r * D + k, acc[r][k]);
       __threadfence();
+      const int c_lo = sk_owner((int64_t)panel * p.total_tiles, p.steps, gridDim.x);
+      const int c_hi = sk_owner((int64_t)(panel + 1) * p.total_tiles - 1, p.steps, gridDim.x);
       named_bar_sync(1, kWarps * 32);
       if (threadIdx.x == 0) {
         const unsigned prev = atomicAdd(&p.panel_cnt[panel], 1u);
-        *flag = (prev == (unsigned)(p.splits - 1));
+        *flag = (prev == (unsigned)(c_hi - c_lo));
       }
       named_bar_sync(1, kWarps * 32);
       const int last = *flag;
@@ -219,13 +253,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (!last) continue;
       __threadfence();
       if (threadIdx.x == 0) p.panel_cnt[panel] = 0u;   // ready for the next launch
-      const T *bq = static_cast<const T *>(p.Bpart) + ((int64_t)panel * p.splits * C::ROWS + warp * C::RT) * D;
 #pragma unroll
       for (int m = 0; m < C::EPL; ++m) {
         const int e = lane + 32 * m;
         if (e < C::E) {
           T v = T(0);
-          for (int s = 0; s < p.splits; ++s) v += __ldcg(bq + (int64_t)s * C::ROWS * D + e);
+          for (int cb = c_lo; cb <= c_hi; ++cb) {
+            const int w2 = (panel == (int)(sk_bound(p.steps, gridDim.x, cb) / p.total_tiles)) ? 0 : 1;
+            v += __ldcg(static_cast<const T *>(p.Bpart) + (((int64_t)cb * 2 + w2) * C::ROWS + warp * C::RT) * D + e);
+          }
           sG[e] = v;
         }
       }
@@ -272,12 +308,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
+      double g1s[C::DDL], g2s[C::DDL];
 #pragma unroll
       for (int m = 0; m < C::DDL; ++m) {
         const int e2 = lane + 32 * m;
+        double g1 = 0.0, g2 = 0.0;
         if (e2 < C::DD) {
           const int a = e2 / D, b = e2 % D;
-          double g1 = 0.0, g2 = 0.0;
           for (int q = 0; q < nvalid; ++q)
 #pragma unroll
             for (int k = 0; k < D; ++k) {
@@ -285,38 +322,43 @@ __global__ void __launch_bounds__(kThreads, 1)
               g1 += w_ka * w_kb;
               g2 += (double)sX[(q * D + k) * D + a] * w_kb;
             }
-          gram1[e2] += g1;
-          gram2[e2] += g2;
         }
+        g1s[m] = g1;
+        g2s[m] = g2;
       }
-      flush_panel(panel);
+      commit(split_panel, panel, g1s, g2s, 0.0, 0.0);
+      __syncwarp();
       continue;
     } else {
       // <X, B> and the X Gram terms of the objective expansion.
+      double xs = 0.0, so = 0.0;
 #pragma unroll
       for (int m = 0; m < C::EPL; ++m) {
         const int e = lane + 32 * m;
-        if (e < C::E && e / C::DD < nvalid) xb += (double)sX[e] * (double)sG[e];
+        if (e < C::E && e / C::DD < nvalid) xs += (double)sX[e] * (double)sG[e];
       }
+      double g1s[C::DDL], g2s[C::DDL];
 #pragma unroll
       for (int m = 0; m < C::DDL; ++m) {
         const int e2 = lane + 32 * m;
+        double g1 = 0.0;
         if (e2 < C::DD) {
           const int a = e2 / D, b = e2 % D;
-          double g1 = 0.0;
           for (int q = 0; q < nvalid; ++q) {
             double v = 0.0;
 #pragma unroll
             for (int k = 0; k < D; ++k)
               v += (double)sX[(q * D + k) * D + a] * (double)sX[(q * D + k) * D + b];
             g1 += v;
-            s_own += v * v;
+            so += v * v;
           }
-          gram1[e2] += g1;
         }
+        g1s[m] = g1;
+        g2s[m] = 0.0;
       }
+      commit(split_panel, panel, g1s, g2s, so, xs);
       if constexpr (MODE == kModeObjective) {
-        flush_panel(panel);
+        __syncwarp();
         continue;
       }
       // G = (n-1) X - B   (in place in sG)
@@ -420,7 +462,6 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
-      flush_panel(panel);
       __syncwarp();
     }
   }
@@ -433,21 +474,19 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     if (lane == 0 && mx > 0.f) atomicMax(p.ns_region, __float_as_uint(mx));
   }
-  if (p.splits == 1) {
-    s_own = warp_sum(s_own);
-    xb = warp_sum(xb);
-    if (lane == 0) { red[warp * 2] = s_own; red[warp * 2 + 1] = xb; }
-    named_bar_sync(1, kWarps * 32);
-    double *cp = p.cta_part + (int64_t)blockIdx.x * C::NPART;
-    for (int i = threadIdx.x; i < C::NPART; i += kWarps * 32) {
-      double v = 0.0;
-      if (i < 2 * C::DD) {
-        for (int w = 0; w < kWarps; ++w) v += gram_all[w * 2 * C::DD + i];
-      } else {
-        for (int w = 0; w < kWarps; ++w) v += red[w * 2 + (i - 2 * C::DD)];
-      }
-      __stcg(cp + i, v);
+  s_own = warp_sum(s_own);
+  xb = warp_sum(xb);
+  if (lane == 0) { red[warp * 2] = s_own; red[warp * 2 + 1] = xb; }
+  named_bar_sync(1, kWarps * 32);
+  double *cp = p.cta_part + (int64_t)blockIdx.x * C::NPART;
+  for (int i = threadIdx.x; i < C::NPART; i += kWarps * 32) {
+    double v = 0.0;
+    if (i < 2 * C::DD) {
+      for (int w = 0; w < kWarps; ++w) v += gram_all[w * 2 * C::DD + i];
+    } else {
+      for (int w = 0; w < kWarps; ++w) v += red[w * 2 + (i - 2 * C::DD)];
     }
+    __stcg(cp + i, v);
   }
   __threadfence();
   named_bar_sync(1, kWarps * 32);
@@ -455,11 +494,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   named_bar_sync(1, kWarps * 32);
   if (*flag) {
     __threadfence();
-    for (int i = threadIdx.x; i < C::NPART; i += kWarps * 32) {
+    // slots [0, G): per-CTA sums; [G, 2G): cut panels (unused slots stay zero).  Warp w sums
+    // columns w, w + kWarps, ...: lane j takes slots j, j + 32, ... in order, then a fixed
+    // butterfly — deterministic.
+    const int nslots = 2 * (int)gridDim.x;
+    for (int i = warp; i < C::NPART; i += kWarps) {
       double v = 0.0;
-      const int nslots = p.splits > 1 ? p.panels * kWarps : (int)gridDim.x;
-      for (int b = 0; b < nslots; ++b) v += __ldcg(p.cta_part + (int64_t)b * C::NPART + i);
-      p.result[i] = v;
+      for (int b = lane; b < nslots; b += 32) v += __ldcg(p.cta_part + (int64_t)b * C::NPART + i);
+      v = warp_sum(v);
+      if (lane == 0) p.result[i] = v;
     }
     if (threadIdx.x == 0) *p.done_cnt = 0u;
   }

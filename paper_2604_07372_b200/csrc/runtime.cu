@@ -118,7 +118,8 @@ struct nsrgs_ctx {
   void *stage = nullptr;   // n*d*d elements (host<->device staging for set/get/Z)
   // panel launch shape
   PanelShape shape{};
-  int sm_count = 0, grid = 0, panels = 0, splits = 1, tiles_per_split = 0, total_tiles = 0, units = 0;
+  int sm_count = 0, grid = 0, panels = 0, total_tiles = 0;
+  int64_t steps = 0;
   // scratch
   double *cta_part = nullptr;   // grid * npart
   unsigned *counters = nullptr; // [0] done_cnt, [1..panels] panel counters
@@ -295,10 +296,8 @@ int launch_panel(nsrgs_ctx *c, int mode, const void *Xin, void *Xout, double *re
   p.world = c->world;
   p.rank = c->rank;
   p.panels = c->panels;
-  p.splits = c->splits;
-  p.tiles_per_split = c->tiles_per_split;
   p.total_tiles = c->total_tiles;
-  p.units = c->units;
+  p.steps = c->steps;
   p.coef = (double)(c->n - 1);
   p.eta = eta;
   p.K = K;
@@ -445,15 +444,11 @@ int nsrgs_create(const nsrgs_desc *desc, nsrgs_ctx **out) {
   }
   cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, c->device);
   panel_dispatch(c->dtype, c->d, 0, true, &c->shape, nullptr, nullptr, 0, nullptr);
-  // launch shape: work units = (row panel, column split)
+  // launch shape: stream-K over panels x column tiles, one persistent CTA per SM
   c->panels = (int)ceil_div(c->plan.rows_local, c->shape.rows);
   c->total_tiles = (int)(c->world * c->plan.tiles_per_rank);
-  int splits = 1;
-  if (c->panels < c->sm_count) splits = (int)std::min<int64_t>(c->total_tiles, ceil_div(2 * c->sm_count, c->panels));
-  c->tiles_per_split = (int)ceil_div(c->total_tiles, splits);
-  c->splits = (int)ceil_div(c->total_tiles, c->tiles_per_split);
-  c->units = c->panels * c->splits;
-  c->grid = std::min(c->units, c->sm_count);
+  c->steps = (int64_t)c->panels * c->total_tiles;
+  c->grid = (int)std::min<int64_t>(c->steps, c->sm_count);
   auto alloc = [&](void **p, size_t bytes) {
     cudaError_t e = cudaMalloc(p, bytes);
     if (e != cudaSuccess) return false;
@@ -461,10 +456,10 @@ int nsrgs_create(const nsrgs_desc *desc, nsrgs_ctx **out) {
   };
   const size_t xb = c->esz * (size_t)c->plan.x_elems;
   bool ok = alloc(&c->X[0], xb) && alloc(&c->X[1], xb) && alloc(&c->stage, c->esz * (size_t)(c->n * c->d * c->d)) &&
-            alloc((void **)&c->cta_part, sizeof(double) * std::max(c->grid, c->panels * kWarps) * c->shape.npart) &&
+            alloc((void **)&c->cta_part, sizeof(double) * (size_t)c->grid * 2 * c->shape.npart) &&
             alloc((void **)&c->counters, sizeof(unsigned) * (c->panels + 1)) &&
             alloc((void **)&c->err, sizeof(int)) && alloc((void **)&c->ns_region, sizeof(unsigned));
-  if (ok && c->splits > 1) ok = alloc(&c->Bpart, c->esz * (size_t)c->units * c->shape.rows * c->d);
+  if (ok) ok = alloc(&c->Bpart, c->esz * (size_t)c->grid * 2 * c->shape.rows * c->d);
   if (!ok) return bail(NSRGS_ERR_OOM, "device allocation failed");
   if (ensure_res(c, 128) || ensure_small(c, kSmallOut + 256)) return bail(NSRGS_ERR_OOM);
   if (c->world > 1) {
@@ -702,7 +697,13 @@ int nsrgs_get_stats(nsrgs_ctx *c, nsrgs_stats_t *o) {
   o->threads = c->shape.threads;
   o->stages = c->shape.stages;
   o->rows_per_panel = c->shape.rows;
-  o->splits = c->splits;
+  int cut = 0;
+  int64_t last_panel = -1;
+  for (int b = 1; b < c->grid; ++b) {
+    const int64_t sb = c->steps * b / c->grid;
+    if (sb % c->total_tiles && sb / c->total_tiles != last_panel) { ++cut; last_panel = sb / c->total_tiles; }
+  }
+  o->cut_panels = cut;
   o->panels = c->panels;
   o->smem_bytes = c->shape.smem;
   o->panel_ms_total = c->panel_ms;

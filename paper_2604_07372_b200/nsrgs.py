@@ -43,7 +43,7 @@ class Plan(ct.Structure):
 
 class Stats(ct.Structure):
     _fields_ = [("grid", ct.c_int32), ("threads", ct.c_int32), ("stages", ct.c_int32),
-                ("rows_per_panel", ct.c_int32), ("splits", ct.c_int32), ("panels", ct.c_int64),
+                ("rows_per_panel", ct.c_int32), ("cut_panels", ct.c_int32), ("panels", ct.c_int64),
                 ("smem_bytes", ct.c_int64), ("panel_ms_total", ct.c_double), ("panel_launches", ct.c_int64),
                 ("kernel_launches", ct.c_int64), ("ns_region_max", ct.c_double), ("a_fro2", ct.c_double)]
 
