@@ -80,17 +80,17 @@ typedef struct {
   int64_t row0;         /* first owned A row = node0 * d                                      */
   int64_t col_tile;     /* X/A column tile width (elements) of the device layout = 128        */
   int64_t tiles_per_rank; /* ceil(rows_local / col_tile)                                       */
-  int64_t x_elems;      /* elements of one device X buffer = world*tiles_per_rank*d*col_tile  */
+  int64_t x_elems;      /* elements of one device X buffer = world*tiles_per_rank*dp*col_tile */
   int64_t x_slice_elems;/* elements of one rank's contiguous X slice (NCCL all-gather count)  */
 } nsrgs_plan_t;
 
 int nsrgs_version(void);
 
 /* Pure host: the sharding plan of (n, d, world, rank).  Returns INVALID_ARG if the
- * combination is not supported.  Device X layout ("tile layout"): element
- * (row c of the nd x d stack, component k) lives at
- *   ((g * tiles_per_rank + j) * d + k) * col_tile + o,  g = c / rows_local,
- *   j = (c % rows_local) / col_tile, o = (c % rows_local) % col_tile;
+ * combination is not supported.  Device X layout ("tile layout"): with
+ * dp = d rounded up to even, element (row c of the nd x d stack, component k) lives at
+ *   ((g * tiles_per_rank + j) * dp + (k & ~1)) * col_tile + 2 * o + (k & 1),
+ *   g = c / rows_local, j = (c % rows_local) / col_tile, o = (c % rows_local) % col_tile;
  * padding entries are zero.  */
 int nsrgs_plan(int64_t n, int32_t d, int32_t world, int32_t rank, nsrgs_plan_t *out);
 

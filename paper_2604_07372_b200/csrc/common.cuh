@@ -38,13 +38,19 @@ constexpr int kErrDivergence = 1;   // ||S||_F > 10 sqrt(d) or non-finite after 
 constexpr int kErrSingular = 2;     // init polar did not converge / Cholesky failed
 constexpr int kErrNonfinite = 4;
 
-// Element of the tile layout for stack row c (0 <= c < N) and component k.
+// Tile layout of X: the N stack rows of one rank's slice are cut into column
+// tiles of 128; tile (g, j) holds dp = d rounded up to even components as dp/2 pair-blocks of
+// 128 x 2 values, component pairs (2kp, 2kp+1) interleaved, so a lane's two adjacent columns
+// of one component pair come in one 128-bit load and feed FFMA2 directly.  Element (row c,
+// component k) of the nd x d stack:
 __host__ __device__ inline int64_t tile_index(int64_t c, int k, int d, int64_t rows_local,
                                               int64_t tiles_per_rank) {
+  const int dp = (d + 1) & ~1;
   int64_t g = c / rows_local, cl = c - g * rows_local;
   int64_t j = cl / kColTile, o = cl - j * kColTile;
-  return ((g * tiles_per_rank + j) * d + k) * kColTile + o;
+  return ((g * tiles_per_rank + j) * dp + (k & ~1)) * kColTile + 2 * o + (k & 1);
 }
+__host__ __device__ constexpr int padded_d(int d) { return (d + 1) & ~1; }
 
 // ------------------------------------------------------------------------------------------
 // Philox4x32-10 (Salmon et al., SC'11).  Same definition as oracle/instance.py, written

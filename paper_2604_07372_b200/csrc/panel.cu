@@ -27,14 +27,16 @@ template <typename T, int D>
 struct PanelCfg {
   static constexpr int RT = (sizeof(T) == 4)
                                 ? (D == 2 ? 12 : D == 3 ? 12 : D == 4 ? 12 : D == 5 ? 10 : D == 6 ? 12
-                                   : D == 7 ? 14 : D == 8 ? 8 : D == 9 ? 9 : 10)
+                                   : D == 7 ? 7 : D == 8 ? 8 : D == 9 ? 9 : 10)
                                 : (D == 2 ? 6 : D == 3 ? 6 : D == 4 ? 4 : D == 5 ? 5 : 6);
   static_assert(RT % D == 0, "warp rows must be whole nodes");
   static constexpr int NPW = RT / D;
   static constexpr int ROWS = RT * kWarps;
   static constexpr int NODES = ROWS / D;
   static constexpr int A_BYTES = ROWS * kColTile * (int)sizeof(T);
-  static constexpr int X_BYTES = D * kColTile * (int)sizeof(T);
+  static constexpr int DP = padded_d(D);           // components incl. the zero pad (even)
+  static constexpr int KP = DP / 2;                // component pairs
+  static constexpr int X_BYTES = DP * kColTile * (int)sizeof(T);
   static constexpr int STAGE_BYTES = A_BYTES + X_BYTES;
   static constexpr int E = NPW * D * D;          // epilogue entries per warp
   static constexpr int EPL = (E + 31) / 32;      // entries per lane
@@ -54,6 +56,21 @@ struct PanelCfg {
 };
 
 template <typename T> __device__ __forceinline__ T tfma(T a, T b, T c) { return fma(a, b, c); }
+
+__device__ __forceinline__ uint64_t pack2(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void unpack2(uint64_t v, float &lo, float &hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+// d = a * b + c on two packed fp32 lanes (sm_100a FFMA2; round-to-nearest like fmaf)
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
 
 template <typename T> __device__ __forceinline__ T warp_sum(T v) {
 #pragma unroll
@@ -115,7 +132,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint8_t *sb = smem + stage * C::STAGE_BYTES;
         mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
         tma_load_3d(sb, &tmA, &full[stage], jt * kColTile, g, panel * C::ROWS, pol_a);
-        bulk_load(sb + C::A_BYTES, Xg + (int64_t)tt * D * kColTile, C::X_BYTES, &full[stage], pol_x);
+        bulk_load(sb + C::A_BYTES, Xg + (int64_t)tt * C::DP * kColTile, C::X_BYTES, &full[stage], pol_x);
         if (++stage == C::STAGES) { stage = 0; phase ^= 1u; }
       }
     }
@@ -192,35 +209,90 @@ __global__ void __launch_bounds__(kThreads, 1)
     st += t1 - t0;
     const bool split_panel = !(t0 == 0 && t1 == p.total_tiles);
 
+    // Lane l owns columns {2l, 2l+1, 64+2l, 65+2l} of each 128-column tile: A row pieces are
+    // conflict-free 64-bit smem loads, X component pairs conflict-free 128-bit loads.
     T acc[C::RT][D];
+    if constexpr (sizeof(T) == 4) {
+      // fp32: packed FFMA2 on component pairs (acc[r][2kp], acc[r][2kp+1]) += (x_2kp, x_2kp+1) * a
+      uint64_t acc2[C::RT][C::KP];
 #pragma unroll
-    for (int r = 0; r < C::RT; ++r)
+      for (int r = 0; r < C::RT; ++r)
 #pragma unroll
-      for (int k = 0; k < D; ++k) acc[r][k] = T(0);
-
-    for (int t = t0; t < t1; ++t) {
-      mbar_wait(&full[stage], phase);
-      const T *As = reinterpret_cast<const T *>(smem + stage * C::STAGE_BYTES) + (warp * C::RT) * kColTile + lane * 4;
-      const T *Xs = reinterpret_cast<const T *>(smem + stage * C::STAGE_BYTES + C::A_BYTES) + lane * 4;
-      V xv[D];
+        for (int kp = 0; kp < C::KP; ++kp) acc2[r][kp] = 0ull;
+      for (int t = t0; t < t1; ++t) {
+        mbar_wait(&full[stage], phase);
+        const float *As = reinterpret_cast<const float *>(smem + stage * C::STAGE_BYTES) + (warp * C::RT) * kColTile + 2 * lane;
+        const float *Xs = reinterpret_cast<const float *>(smem + stage * C::STAGE_BYTES + C::A_BYTES) + 4 * lane;
+        uint64_t xp[C::KP][4];   // pairs for the lane's 4 columns
 #pragma unroll
-      for (int k = 0; k < D; ++k) xv[k] = *reinterpret_cast<const V *>(Xs + k * kColTile);
-#pragma unroll
-      for (int r = 0; r < C::RT; ++r) {
-        const V a = *reinterpret_cast<const V *>(As + r * kColTile);
-#pragma unroll
-        for (int k = 0; k < D; ++k) {
-          T v = acc[r][k];
-          v = tfma(a.x, xv[k].x, v);
-          v = tfma(a.y, xv[k].y, v);
-          v = tfma(a.z, xv[k].z, v);
-          v = tfma(a.w, xv[k].w, v);
-          acc[r][k] = v;
+        for (int kp = 0; kp < C::KP; ++kp) {
+          const ulonglong2 lo = *reinterpret_cast<const ulonglong2 *>(Xs + kp * 2 * kColTile);
+          const ulonglong2 hi = *reinterpret_cast<const ulonglong2 *>(Xs + kp * 2 * kColTile + kColTile);
+          xp[kp][0] = lo.x; xp[kp][1] = lo.y; xp[kp][2] = hi.x; xp[kp][3] = hi.y;
         }
+#pragma unroll
+        for (int r = 0; r < C::RT; ++r) {
+          const float2 a0 = *reinterpret_cast<const float2 *>(As + r * kColTile);
+          const float2 a1 = *reinterpret_cast<const float2 *>(As + r * kColTile + 64);
+          const uint64_t b0 = pack2(a0.x, a0.x), b1 = pack2(a0.y, a0.y);
+          const uint64_t b2 = pack2(a1.x, a1.x), b3 = pack2(a1.y, a1.y);
+#pragma unroll
+          for (int kp = 0; kp < C::KP; ++kp) {
+            uint64_t v = acc2[r][kp];
+            v = ffma2(xp[kp][0], b0, v);
+            v = ffma2(xp[kp][1], b1, v);
+            v = ffma2(xp[kp][2], b2, v);
+            v = ffma2(xp[kp][3], b3, v);
+            acc2[r][kp] = v;
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[stage]);
+        if (++stage == C::STAGES) { stage = 0; phase ^= 1u; }
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[stage]);
-      if (++stage == C::STAGES) { stage = 0; phase ^= 1u; }
+#pragma unroll
+      for (int r = 0; r < C::RT; ++r)
+#pragma unroll
+        for (int kp = 0; kp < C::KP; ++kp) {
+          float lo, hi;
+          unpack2(acc2[r][kp], lo, hi);
+          acc[r][2 * kp] = (T)lo;
+          if (2 * kp + 1 < D) acc[r][2 * kp + 1] = (T)hi;
+        }
+    } else {
+#pragma unroll
+      for (int r = 0; r < C::RT; ++r)
+#pragma unroll
+        for (int k = 0; k < D; ++k) acc[r][k] = T(0);
+      for (int t = t0; t < t1; ++t) {
+        mbar_wait(&full[stage], phase);
+        const T *As = reinterpret_cast<const T *>(smem + stage * C::STAGE_BYTES) + (warp * C::RT) * kColTile + 2 * lane;
+        const T *Xs = reinterpret_cast<const T *>(smem + stage * C::STAGE_BYTES + C::A_BYTES) + 4 * lane;
+        T xv[C::DP][4];
+#pragma unroll
+        for (int kp = 0; kp < C::KP; ++kp) {
+          const V lo = *reinterpret_cast<const V *>(Xs + kp * 2 * kColTile);
+          const V hi = *reinterpret_cast<const V *>(Xs + kp * 2 * kColTile + kColTile);
+          xv[2 * kp][0] = lo.x; xv[2 * kp + 1][0] = lo.y; xv[2 * kp][1] = lo.z; xv[2 * kp + 1][1] = lo.w;
+          xv[2 * kp][2] = hi.x; xv[2 * kp + 1][2] = hi.y; xv[2 * kp][3] = hi.z; xv[2 * kp + 1][3] = hi.w;
+        }
+#pragma unroll
+        for (int r = 0; r < C::RT; ++r) {
+          T a[4];
+          a[0] = As[r * kColTile]; a[1] = As[r * kColTile + 1];
+          a[2] = As[r * kColTile + 64]; a[3] = As[r * kColTile + 65];
+#pragma unroll
+          for (int k = 0; k < D; ++k) {
+            T v = acc[r][k];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) v = tfma(a[j], xv[k][j], v);
+            acc[r][k] = v;
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[stage]);
+        if (++stage == C::STAGES) { stage = 0; phase ^= 1u; }
+      }
     }
 
     // ---- reduce the lane-partial sums: every lane ends with the full B rows of the warp

@@ -42,9 +42,10 @@ def test_exports_every_declared_symbol(nsrgs):
 
 def _tile_index(c, k, d, rows_local, tpr, CT=128):
     # the layout formula as written in include/nsrgs.h (nsrgs_plan comment)
+    dp = d + (d % 2)
     g, cl = divmod(c, rows_local)
     j, o = divmod(cl, CT)
-    return ((g * tpr + j) * d + k) * CT + o
+    return ((g * tpr + j) * dp + (k - k % 2)) * CT + 2 * o + k % 2
 
 
 @pytest.mark.parametrize("n,d,world", [(2, 2, 1), (100, 3, 1), (100, 3, 4), (43, 5, 1), (20000, 5, 8),
@@ -57,6 +58,7 @@ def test_plan_partitions_rows(nsrgs, n, d, world):
         assert p["rows_local"] == p["n_local"] * d and p["row0"] == p["node0"] * d
         assert p["tiles_per_rank"] == -(-p["rows_local"] // 128)
         assert p["x_slice_elems"] * world == p["x_elems"]
+        assert p["x_slice_elems"] == p["tiles_per_rank"] * (d + d % 2) * 128
         rows.append((p["row0"], p["row0"] + p["rows_local"]))
     assert rows[0][0] == 0 and rows[-1][1] == n * d
     assert all(a[1] == b[0] for a, b in zip(rows, rows[1:]))
