@@ -144,6 +144,55 @@ def run(A: np.ndarray, X0: np.ndarray, T: int, mu: float, Ts: int, retraction: s
     return (X, trace) if trace_objective else X
 
 
+# ----------------------------------------------------------------------------- GPM (comparison method)
+def gpm_step(A: np.ndarray, X: np.ndarray) -> np.ndarray:
+    """Generalized power method, the paper's comparison system (§4.1, cited from
+    Ling 2022): X_i^{t+1} = sgn(sum_{j != i} A_ij X_j^t) blockwise (definition as in SPEC.md:245-253;
+    DESIGN.md reading R17).  Jacobi, exact SVD sign."""
+    n, d, _ = X.shape
+    AX = unstack(A @ stack(X), d)
+    Aii = np.stack([A[i * d:(i + 1) * d, i * d:(i + 1) * d] for i in range(n)])
+    return sgn(AX - Aii @ X)
+
+
+def gpm_step_bruteforce(A, X):
+    """gpm_step with explicit Python loops for the block sums (the SVD sign is the library step)."""
+    n, d, _ = X.shape
+    out = []
+    for i in range(n):
+        S = [[0.0] * d for _ in range(d)]
+        for j in range(n):
+            if j == i:
+                continue
+            for a in range(d):
+                for b in range(d):
+                    S[a][b] += sum(A[i * d + a, j * d + k] * X[j][k][b] for k in range(d))
+        out.append(sgn(np.array(S)))
+    return np.array(out)
+
+
+def solve_protocol(A: np.ndarray, X0: np.ndarray, mu: float, Ts: int, algorithm: str = "ns_rgs",
+                   max_iter: int = 100, tol: float = 1e-8):
+    """The paper's experimental protocol (§4.1): iterate from X^0 until
+    R^t = (F(X^t) - F(X^{t+1})) / F(X^{t+1}) < tol or MaxIter iterations.  Returns
+    (X_final, iterations, [F(X^0), F(X^1), ...])."""
+    X = np.array(X0, dtype=np.float64, copy=True)
+    f = objective_expanded(A, X)
+    trace = [f]
+    it = 0
+    while it < max_iter:
+        Xn = step(A, X, mu, Ts)[0] if algorithm == "ns_rgs" else gpm_step(A, X)
+        fn = objective_expanded(A, Xn)
+        it += 1
+        X = Xn
+        trace.append(fn)
+        R = (f - fn) / fn
+        f = fn
+        if R < tol:
+            break
+    return X, it, trace
+
+
 # ----------------------------------------------------------------------------- spectral init
 def spectral_init(A: np.ndarray, d: int, method: str = "eigh", Y0=None, tol: float = 1e-13,
                   max_sweeps: int = 500):

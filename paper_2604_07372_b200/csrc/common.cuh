@@ -29,6 +29,7 @@ struct PanelParams {
   int world, rank;
   int panels, total_tiles;   // total_tiles = column tiles per panel (all ranks' slices)
   int64_t steps;             // stream-K work = panels * total_tiles
+  float a_keep;         // fraction of A accesses tagged L2 evict_last (A shard ~ L2 size), else evict_first
   double coef;          // n - 1   (identity term of G_i)
   double eta;           // step size mu
   int K;                // Newton-Schulz steps (Algorithm 1)
@@ -115,6 +116,13 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
 __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+// Fraction `f` of accesses evict_last, the rest evict_first (keeps a resident subset of a
+// stream that is slightly larger than L2 instead of thrashing all of it).
+__device__ __forceinline__ uint64_t policy_keep_fraction(float f) {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.L2::evict_first.b64 %0, %1;" : "=l"(p) : "f"(f));
   return p;
 }
 __device__ __forceinline__ uint64_t policy_evict_last() {

@@ -120,7 +120,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == kWarps) {
     if (lane == 0) {
       prefetch_tmap(&tmA);
-      const uint64_t pol_a = policy_evict_first(), pol_x = policy_evict_last();
+      const uint64_t pol_a = p.a_keep > 0.f ? policy_keep_fraction(p.a_keep) : policy_evict_first();
+      const uint64_t pol_x = policy_evict_last();
       int stage = 0;
       uint32_t phase = 0;
       const int64_t s_end = sk_bound(p.steps, gridDim.x, blockIdx.x + 1);

@@ -119,6 +119,7 @@ struct nsrgs_ctx {
   // panel launch shape
   PanelShape shape{};
   int sm_count = 0, grid = 0, panels = 0, total_tiles = 0;
+  float a_keep = 0.f;   // L2 evict_last fraction for A (only when the shard is within ~4x of L2)
   int64_t steps = 0;
   // scratch
   double *cta_part = nullptr;   // grid * npart
@@ -298,6 +299,7 @@ int launch_panel(nsrgs_ctx *c, int mode, const void *Xin, void *Xout, double *re
   p.panels = c->panels;
   p.total_tiles = c->total_tiles;
   p.steps = c->steps;
+  p.a_keep = c->a_keep;
   p.coef = (double)(c->n - 1);
   p.eta = eta;
   p.K = K;
@@ -449,6 +451,13 @@ int nsrgs_create(const nsrgs_desc *desc, nsrgs_ctx **out) {
   c->total_tiles = (int)(c->world * c->plan.tiles_per_rank);
   c->steps = (int64_t)c->panels * c->total_tiles;
   c->grid = (int)std::min<int64_t>(c->steps, c->sm_count);
+  {
+    int l2 = 0;
+    cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, c->device);
+    const double a_bytes = (double)c->esz * (double)c->plan.rows_local * (double)c->N;
+    const double keep = 0.7 * (double)l2 / std::max(1.0, a_bytes);
+    c->a_keep = a_bytes <= 4.0 * l2 ? (float)std::min(1.0, keep) : 0.f;
+  }
   auto alloc = [&](void **p, size_t bytes) {
     cudaError_t e = cudaMalloc(p, bytes);
     if (e != cudaSuccess) return false;

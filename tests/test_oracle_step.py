@@ -149,3 +149,49 @@ def test_step_rows_equals_full_step():
     nodes = [0, 7, 29]
     R = inst.measurement_rows(8, Z, sigma, nodes)
     assert np.max(np.abs(ns.step_rows(R, X, nodes, 1.0 / n, 3) - Xfull[nodes])) < 1e-13
+
+
+# ---------------------------------------------------------------- GPM (comparison method)
+@pytest.mark.parametrize("n,d", [(3, 2), (6, 3), (5, 4)])
+def test_gpm_matches_bruteforce(n, d):
+    rng = np.random.default_rng(n + 10 * d)
+    A = rng.standard_normal((n * d, n * d)); A = A + A.T
+    X = _stack_haar(rng, n, d)
+    assert np.max(np.abs(ns.gpm_step(A, X) - ns.gpm_step_bruteforce(A, X))) < 1e-12
+
+
+def test_gpm_fixed_point_and_orthogonality():
+    n, d = 25, 3
+    Z = inst.ground_truth(2, n, d)
+    A0 = inst.measurement_matrix(2, Z, 0.0, dtype=np.float64)
+    assert np.max(np.abs(ns.gpm_step(A0, Z) - Z)) < 1e-13          # sgn((n-1) Z_i) = Z_i
+    A = inst.measurement_matrix(2, Z, 1.5)
+    Xn = ns.gpm_step(A, _stack_haar(np.random.default_rng(0), n, d))
+    assert np.max(np.abs(np.einsum("nka,nkb->nab", Xn, Xn) - np.eye(d))) < 1e-13
+
+
+def test_gpm_gauge_equivariance():
+    n, d, sigma = 15, 3, 0.5
+    Z = inst.ground_truth(6, n, d)
+    A = inst.measurement_matrix(6, Z, sigma, dtype=np.float64)
+    rng = np.random.default_rng(4)
+    R = _stack_haar(rng, n, d)
+    D = np.zeros((n * d, n * d))
+    for i in range(n):
+        D[i * d:(i + 1) * d, i * d:(i + 1) * d] = R[i]
+    X = _stack_haar(rng, n, d)
+    Rt = np.transpose(R, (0, 2, 1))
+    assert np.max(np.abs(ns.gpm_step(D.T @ A @ D, Rt @ X) - Rt @ ns.gpm_step(A, X))) < 1e-12
+
+
+def test_solve_protocol_stops_on_relative_decrease():
+    n, d, sigma = 80, 3, 0.5
+    Z = inst.ground_truth(3, n, d)
+    A = inst.measurement_matrix(3, Z, sigma)
+    X0, _, _ = ns.spectral_init(A, d)
+    X, it, tr = ns.solve_protocol(A, X0, 1.0 / n, 1, "ns_rgs", max_iter=100, tol=1e-8)
+    assert it < 100 and len(tr) == it + 1
+    assert (tr[-2] - tr[-1]) / tr[-1] < 1e-8
+    assert all((tr[k] - tr[k + 1]) / tr[k + 1] >= 1e-8 for k in range(it - 1))
+    X1 = ns.run(A, X0, it, 1.0 / n, 1)
+    assert np.max(np.abs(X1 - X)) < 1e-14
