@@ -146,6 +146,20 @@ int nsrgs_step(nsrgs_ctx *ctx, double eta, int K, double *objective_before);
  * F(X^0..X^{T-1}).  Returns NSRGS_ERR_DIVERGENCE if any iteration left the NS region. */
 int nsrgs_run(nsrgs_ctx *ctx, int T, double eta, int K, double *objective_trace);
 
+/* GPM, the paper's comparison method (§4.1; definition):
+ * T iterations of X_i <- sgn(sum_{j!=i} A_ij X_j) on the same A pass, the sign taken by
+ * Newton-Schulz from B_i/||B_i||_F to convergence (no SVD).  objective_trace as nsrgs_run.
+ * Returns NSRGS_ERR_SINGULAR if a sign did not converge (rank-deficient B_i). */
+int nsrgs_gpm_run(nsrgs_ctx *ctx, int T, double *objective_trace);
+
+/* The paper's experimental protocol (§4.1): iterate `algorithm` from the
+ * current X^0 until R^t = (F(X^t) - F(X^{t+1}))/F(X^{t+1}) < stop_tol or max_iter iterations.
+ * On return X = X^{t_stop}; *iters_used = t_stop; objective_trace (host, nullable, length
+ * max_iter + 1) receives F(X^0..X^{t_stop}).  eta, K are used by NSRGS_ALG_NSRGS only. */
+typedef enum { NSRGS_ALG_NSRGS = 0, NSRGS_ALG_GPM = 1 } nsrgs_algorithm;
+int nsrgs_solve(nsrgs_ctx *ctx, int algorithm, int max_iter, double eta, int K, double stop_tol, int *iters_used,
+                double *objective_trace);
+
 /* F(X) of the current iterate (PAPER.md:70-72 Eq. def:f); one A pass. */
 int nsrgs_objective(nsrgs_ctx *ctx, double *F_out);
 

@@ -7,7 +7,7 @@
 
 namespace nsrgs {
 
-enum PanelMode { kModeRgs = 0, kModeObjective = 1, kModeProduct = 2 };
+enum PanelMode { kModeRgs = 0, kModeObjective = 1, kModeProduct = 2, kModeGpm = 3 };
 
 struct PanelShape {
   int rows, nodes, stages, smem, npart, threads;

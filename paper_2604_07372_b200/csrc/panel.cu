@@ -434,6 +434,76 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
         continue;
       }
+      if constexpr (MODE == kModeGpm) {
+        // GPM (comparison method): X_i <- sgn(B_i), B_i = sum_{j!=i} A_ij X_j, by
+        // Newton-Schulz from S_0 = B_i / ||B_i||_F (singular values in (0, 1]) to convergence.
+        T *inv = sM + C::E - C::NPW;   // scratch: per-node scale (sM is rewritten below)
+        if (lane < C::NPW) {
+          T f2 = T(0);
+          for (int e2 = 0; e2 < C::DD; ++e2) f2 += sG[lane * C::DD + e2] * sG[lane * C::DD + e2];
+          inv[lane] = f2 > T(0) ? T(1) / sqrt(f2) : T(0);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int m = 0; m < C::EPL; ++m) {
+          const int e = lane + 32 * m;
+          if (e < C::E) sS[e] = sG[e] * inv[e / C::DD];
+        }
+        __syncwarp();
+        const T tol = sizeof(T) == 4 ? T(2e-5) : T(1e-13);
+        int polish = 2;
+        bool conv = false;
+        for (int it = 0; it < 60; ++it) {
+#pragma unroll
+          for (int m = 0; m < C::EPL; ++m) {
+            const int e = lane + 32 * m;
+            if (e < C::E) {
+              const int q = e / C::DD, a = (e / D) % D, b = e % D;
+              const T *Sq = sS + q * C::DD;
+              T v = T(0);
+#pragma unroll
+              for (int k = 0; k < D; ++k) v = tfma(Sq[k * D + a], Sq[k * D + b], v);
+              sM[e] = v;
+            }
+          }
+          __syncwarp();
+          bool ok = true;
+          if (lane < nvalid) {
+            T dev = T(0);
+            for (int e2 = 0; e2 < C::DD; ++e2) {
+              const T dv = (e2 / D == e2 % D ? T(1) : T(0)) - sM[lane * C::DD + e2];
+              dev += dv * dv;
+            }
+            ok = sqrt(dev) <= tol;
+          }
+          if (__all_sync(0xffffffffu, ok)) {
+            conv = true;
+            if (polish-- == 0) break;
+          }
+          T snew[C::EPL];
+#pragma unroll
+          for (int m = 0; m < C::EPL; ++m) {
+            const int e = lane + 32 * m;
+            snew[m] = T(0);
+            if (e < C::E) {
+              const int q = e / C::DD, a = (e / D) % D, b = e % D;
+              const T *Sq = sS + q * C::DD, *Mq = sM + q * C::DD;
+              T v = T(0);
+#pragma unroll
+              for (int k = 0; k < D; ++k) v = tfma(Sq[a * D + k], Mq[k * D + b], v);
+              snew[m] = T(1.5) * sS[e] - T(0.5) * v;
+            }
+          }
+          __syncwarp();
+#pragma unroll
+          for (int m = 0; m < C::EPL; ++m) {
+            const int e = lane + 32 * m;
+            if (e < C::E) sS[e] = snew[m];
+          }
+          __syncwarp();
+        }
+        if (!conv && nvalid > 0) err |= kErrSingular;
+      } else {
       // G = (n-1) X - B   (in place in sG)
 #pragma unroll
       for (int m = 0; m < C::EPL; ++m) {
@@ -516,6 +586,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         __syncwarp();
       }
+      }  // MODE == kModeRgs
       // divergence guard: non-finite or ||S||_F > 10 sqrt(d)
       if (lane < nvalid) {
         const T *Sq = sS + lane * C::DD;
@@ -541,7 +612,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   // ------------------------------------------------------------------ CTA + grid reduction
   if (err) atomicOr(p.err, err);
-  if (MODE == kModeRgs) {
+  if (MODE == kModeRgs || MODE == kModeGpm) {
     float mx = ns_region;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
@@ -607,6 +678,7 @@ static PanelShape shape_impl() {
     if (shape_only) { *shape = shape_impl<T, D>(); return cudaSuccess; }                     \
     if (mode == kModeRgs) return launch_impl<T, D, kModeRgs>(tm, *p, grid, s);               \
     if (mode == kModeObjective) return launch_impl<T, D, kModeObjective>(tm, *p, grid, s);   \
+    if (mode == kModeGpm) return launch_impl<T, D, kModeGpm>(tm, *p, grid, s);               \
     return launch_impl<T, D, kModeProduct>(tm, *p, grid, s);
 
 cudaError_t panel_dispatch(int dtype, int d, int mode, bool shape_only, PanelShape *shape,

@@ -624,14 +624,22 @@ int nsrgs_init_spectral(nsrgs_ctx *c, uint64_t seed, int max_sweeps, double tol,
   return NSRGS_OK;
 }
 
-static int run_impl(nsrgs_ctx *c, int T, double eta, int K, double *trace) {
+static int check_run_flags(nsrgs_ctx *c, int flags) {
+  if (flags & kErrDivergence)
+    return set_err(c, NSRGS_ERR_DIVERGENCE, "Newton-Schulz retraction diverged (||S||_F > 10 sqrt(d) or non-finite)");
+  if (flags & kErrSingular)
+    return set_err(c, NSRGS_ERR_SINGULAR, "GPM: Newton-Schulz sign of B_i did not converge (rank-deficient block)");
+  return NSRGS_OK;
+}
+
+static int run_impl(nsrgs_ctx *c, int mode, int T, double eta, int K, double *trace) {
   NSRGS_TRY(require_ready(c, true));
-  if (T < 0 || K < 0 || !(eta > 0.0) || !std::isfinite(eta))
+  if (T < 0 || K < 0 || (mode == kModeRgs && (!(eta > 0.0) || !std::isfinite(eta))))
     return set_err(c, NSRGS_ERR_INVALID_ARG, "run: need T >= 0, K >= 0, eta > 0");
   if (T == 0) return NSRGS_OK;
   NSRGS_TRY(ensure_res(c, T));
   for (int t = 0; t < T; ++t) {
-    NSRGS_TRY(launch_panel(c, kModeRgs, c->X[c->cur], c->X[1 - c->cur], c->res + (size_t)t * c->shape.npart, eta, K));
+    NSRGS_TRY(launch_panel(c, mode, c->X[c->cur], c->X[1 - c->cur], c->res + (size_t)t * c->shape.npart, eta, K));
     NSRGS_TRY(allgather_X(c, c->X[1 - c->cur]));
     c->cur = 1 - c->cur;
   }
@@ -646,8 +654,7 @@ static int run_impl(nsrgs_ctx *c, int T, double eta, int K, double *trace) {
   float nrf;
   std::memcpy(&nrf, &nr, 4);
   c->ns_region_max = std::max(c->ns_region_max, (double)nrf);
-  if (flags & kErrDivergence)
-    return set_err(c, NSRGS_ERR_DIVERGENCE, "Newton-Schulz retraction diverged (||S||_F > 10 sqrt(d) or non-finite)");
+  NSRGS_TRY(check_run_flags(c, flags));
   if (trace)
     for (int t = 0; t < T; ++t)
       if (!std::isfinite(trace[t])) return set_err(c, NSRGS_ERR_NONFINITE, "objective non-finite at t = %d", t);
@@ -656,12 +663,68 @@ static int run_impl(nsrgs_ctx *c, int T, double eta, int K, double *trace) {
 
 int nsrgs_step(nsrgs_ctx *c, double eta, int K, double *objective_before) {
   NSRGS_TRY(enter(c));
-  return run_impl(c, 1, eta, K, objective_before);
+  return run_impl(c, kModeRgs, 1, eta, K, objective_before);
 }
 
 int nsrgs_run(nsrgs_ctx *c, int T, double eta, int K, double *objective_trace) {
   NSRGS_TRY(enter(c));
-  return run_impl(c, T, eta, K, objective_trace);
+  return run_impl(c, kModeRgs, T, eta, K, objective_trace);
+}
+
+int nsrgs_gpm_run(nsrgs_ctx *c, int T, double *objective_trace) {
+  NSRGS_TRY(enter(c));
+  return run_impl(c, kModeGpm, T, 0.0, 0, objective_trace);
+}
+
+int nsrgs_solve(nsrgs_ctx *c, int algorithm, int max_iter, double eta, int K, double stop_tol, int *iters_used,
+                double *trace) {
+  NSRGS_TRY(enter(c));
+  NSRGS_TRY(require_ready(c, true));
+  const int mode = algorithm == NSRGS_ALG_GPM ? kModeGpm : kModeRgs;
+  if ((algorithm != NSRGS_ALG_NSRGS && algorithm != NSRGS_ALG_GPM) || max_iter < 1 || K < 0 || !(stop_tol >= 0.0) ||
+      (mode == kModeRgs && !(eta > 0.0)))
+    return set_err(c, NSRGS_ERR_INVALID_ARG, "solve: bad algorithm / max_iter / eta / K / stop_tol");
+  NSRGS_TRY(ensure_res(c, max_iter + 1));
+  NSRGS_TRY(ensure_small(c, kSmallOut + max_iter + 8));
+  const int np = c->shape.npart;
+  std::vector<double> F(max_iter + 1, 0.0);
+  int it = 0, stopped = 0;
+  for (; it < max_iter; ++it) {
+    // X^it -> X^{it+1}; the same pass yields the partials of F(X^it)
+    NSRGS_TRY(launch_panel(c, mode, c->X[c->cur], c->X[1 - c->cur], c->res + (size_t)it * np, eta, K));
+    NSRGS_TRY(allgather_X(c, c->X[1 - c->cur]));
+    c->cur = 1 - c->cur;
+    NSRGS_TRY(allreduce_sum(c, c->res + (size_t)it * np, np));
+    CUDA_TRY(c, launch_objective_final(c->d, 1, c->res + (size_t)it * np, np, c->small + kSmallFro,
+                                       c->small + kSmallOut + it, c->stream));
+    c->kernel_launches++;
+    CUDA_TRY(c, cudaMemcpyAsync(&F[it], c->small + kSmallOut + it, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    int flags = 0;
+    NSRGS_TRY(sync_and_check(c, &flags));
+    NSRGS_TRY(check_run_flags(c, flags));
+    if (!std::isfinite(F[it])) return set_err(c, NSRGS_ERR_NONFINITE, "objective non-finite at t = %d", it);
+    // R^{it-1} = (F(X^{it-1}) - F(X^it)) / F(X^it) < tol: X^it is the answer and
+    // the speculative X^{it+1} is dropped (its pass was needed to evaluate F(X^it) anyway).
+    if (it >= 1 && (F[it - 1] - F[it]) / F[it] < stop_tol) {
+      c->cur = 1 - c->cur;
+      stopped = 1;
+      break;
+    }
+  }
+  if (!stopped) {   // MaxIter reached: X = X^{max_iter}; evaluate F(X^{max_iter}) for the trace
+    NSRGS_TRY(launch_panel(c, kModeObjective, c->X[c->cur], nullptr, c->res + (size_t)max_iter * np, 0.0, 0));
+    NSRGS_TRY(allreduce_sum(c, c->res + (size_t)max_iter * np, np));
+    CUDA_TRY(c, launch_objective_final(c->d, 1, c->res + (size_t)max_iter * np, np, c->small + kSmallFro,
+                                       c->small + kSmallOut + max_iter, c->stream));
+    c->kernel_launches++;
+    CUDA_TRY(c, cudaMemcpyAsync(&F[max_iter], c->small + kSmallOut + max_iter, sizeof(double), cudaMemcpyDeviceToHost,
+                                c->stream));
+    NSRGS_TRY(sync_and_check(c));
+    it = max_iter;
+  }
+  if (iters_used) *iters_used = it;
+  if (trace) std::memcpy(trace, F.data(), sizeof(double) * (it + 1));
+  return NSRGS_OK;
 }
 
 int nsrgs_objective(nsrgs_ctx *c, double *F_out) {

@@ -65,6 +65,9 @@ _SIGS = {
     "nsrgs_step": ([_P, ct.c_double, ct.c_int, ct.POINTER(ct.c_double)], ct.c_int),
     "nsrgs_run": ([_P, ct.c_int, ct.c_double, ct.c_int, ct.POINTER(ct.c_double)], ct.c_int),
     "nsrgs_objective": ([_P, ct.POINTER(ct.c_double)], ct.c_int),
+    "nsrgs_gpm_run": ([_P, ct.c_int, ct.POINTER(ct.c_double)], ct.c_int),
+    "nsrgs_solve": ([_P, ct.c_int, ct.c_int, ct.c_double, ct.c_int, ct.c_double, ct.POINTER(ct.c_int),
+                     ct.POINTER(ct.c_double)], ct.c_int),
     "nsrgs_alignment_error": ([_P, _P, ct.c_int, ct.POINTER(ct.c_double)], ct.c_int),
     "nsrgs_set_X": ([_P, _P, ct.c_int], ct.c_int),
     "nsrgs_get_X": ([_P, _P, ct.c_int], ct.c_int),
@@ -210,6 +213,21 @@ class Solver:
         buf = (ct.c_double * max(T, 1))() if trace else None
         self._check(_lib.nsrgs_run(self._h, T, eta, K, buf))
         return np.array(buf[:T]) if trace else None
+
+    def gpm_run(self, T: int, trace: bool = True):
+        buf = (ct.c_double * max(T, 1))() if trace else None
+        self._check(_lib.nsrgs_gpm_run(self._h, T, buf))
+        return np.array(buf[:T]) if trace else None
+
+    def solve(self, algorithm: str = "ns_rgs", max_iter: int = 100, eta: float | None = None, K: int = 1,
+              stop_tol: float = 1e-8):
+        """Paper protocol.  Returns (iterations, F trace of length it + 1)."""
+        alg = {"ns_rgs": 0, "gpm": 1}[algorithm]
+        it = ct.c_int(0)
+        buf = (ct.c_double * (max_iter + 1))()
+        self._check(_lib.nsrgs_solve(self._h, alg, max_iter, eta if eta is not None else 1.0 / self.n, K, stop_tol,
+                                     ct.byref(it), buf))
+        return it.value, np.array(buf[:it.value + 1])
 
     def objective(self) -> float:
         f = ct.c_double(0.0)

@@ -269,3 +269,68 @@ def test_full_size_run_properties(nsrgs, cfg):
     assert abs(rel - sigma * np.sqrt((d - 1) / n)) <= 0.1 * rel
     assert abs(mse - dF ** 2 / n) <= 1e-9 * mse
     s.close()
+
+
+# ---------------------------------------------------------------------------- GPM + paper protocol (§8f)
+@pytest.mark.parametrize("n,d,sigma,dtype", [(100, 3, 0.5, "f32"), (100, 3, 0.5, "f64"), (43, 5, 1.0, "f32"),
+                                             (60, 10, 0.8, "f32"), (37, 7, 0.6, "f32"), (33, 6, 0.9, "f64")])
+def test_gpm_step_from_shared_iterate(nsrgs, n, d, sigma, dtype):
+    code, npdt = _dt(nsrgs, dtype)
+    s = nsrgs.Solver(n, d, code)
+    s.generate(5, sigma, want_Z=False)
+    Z = inst.ground_truth(5, n, d)
+    A = inst.measurement_matrix(5, Z, sigma, dtype=npdt)
+    X = oracle_iterate_near(Z, 0.2, 1).astype(npdt)
+    s.set_X(X)
+    tr = s.gpm_run(1)
+    Xo = ons.gpm_step(A, X.astype(np.float64))
+    assert rel_fro(s.get_X(), Xo) <= (1e-6 if dtype == "f32" else 1e-12)
+    fo = ons.objective(A, X.astype(np.float64))
+    assert abs(tr[0] - fo) <= (2e-6 if dtype == "f32" else 1e-10) * fo
+    s.close()
+
+
+def test_gpm_T_steps_and_agreement_with_nsrgs(nsrgs):
+    n, d, sigma, T = 100, 3, 0.5, 20
+    s = nsrgs.Solver(n, d)
+    Zg = s.generate(0, sigma)
+    Z = inst.ground_truth(0, n, d)
+    A = inst.measurement_matrix(0, Z, sigma)
+    X0, _, _ = ons.spectral_init(A, d)
+    s.set_X(X0.astype(np.float32))
+    s.gpm_run(T, trace=False)
+    Xo = X0.astype(np.float32).astype(np.float64)
+    for _ in range(T):
+        Xo = ons.gpm_step(A, Xo)
+    assert rel_fro(s.get_X(), Xo) <= 1e-5
+    r_gpm = s.alignment_error(Zg)[0]
+    s.set_X(X0.astype(np.float32))
+    s.run(T, 1.0 / n, 3, trace=False)
+    r_rgs = s.alignment_error(Zg)[0]
+    assert abs(r_gpm - r_rgs) <= 1e-4            # identical Rel.Err. rows in Table 1
+    s.close()
+
+
+@pytest.mark.parametrize("alg", ["ns_rgs", "gpm"])
+def test_solve_protocol(nsrgs, alg):
+    n, d, sigma = 300, 3, 1.0
+    s = nsrgs.Solver(n, d, nsrgs.F64)
+    s.generate(2, sigma, want_Z=False)
+    Z = inst.ground_truth(2, n, d)
+    A = inst.measurement_matrix(2, Z, sigma, dtype=np.float64)
+    X0, _, _ = ons.spectral_init(A, d)
+    s.set_X(X0)
+    it, tr = s.solve(alg, max_iter=100, K=1, stop_tol=1e-8)
+    Xo, it_o, tr_o = ons.solve_protocol(A, X0, 1.0 / n, 1, alg, max_iter=100, tol=1e-8)
+    assert abs(it - it_o) <= 1 and len(tr) == it + 1
+    # internal consistency of the stopping rule on the device's own trace
+    R = (tr[:-1] - tr[1:]) / tr[1:]
+    assert (it == 100) or (R[-1] < 1e-8 and np.all(R[:-1] >= 1e-8))
+    X_it = ons.run(A, X0, it, 1.0 / n, 1) if alg == "ns_rgs" else None
+    if alg == "gpm":
+        X_it = X0.copy()
+        for _ in range(it):
+            X_it = ons.gpm_step(A, X_it)
+    assert rel_fro(s.get_X(), X_it) <= 1e-10
+    assert np.max(np.abs(tr - np.array(tr_o[:len(tr)]) if len(tr_o) >= len(tr) else 0) / tr[0]) <= 1e-10
+    s.close()
