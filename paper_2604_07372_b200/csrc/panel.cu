@@ -20,6 +20,7 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "epilogue.cuh"
 
 namespace nsrgs {
 
@@ -55,7 +56,6 @@ struct PanelCfg {
   static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + BAR_BYTES + SCR_BYTES;
 };
 
-template <typename T> __device__ __forceinline__ T tfma(T a, T b, T c) { return fma(a, b, c); }
 
 __device__ __forceinline__ uint64_t pack2(float lo, float hi) {
   uint64_t r;
@@ -156,7 +156,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   double s_own = 0.0, xb = 0.0;     // sum_i ||X_i^T X_i||^2, <X, B>
   float ns_region = 0.f;
   int err = 0;
-  const T coef = (T)p.coef, eta = (T)p.eta;
 
   // Objective / Gram partials.  A panel whose tiles all lie in this CTA's stream-K range is
   // finished here by construction (static) and accumulates into the per-CTA running sums; a
@@ -346,268 +345,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (((r * D + k) & 31) == lane) sG[r * D + k] = acc[r][k];
     }
 
-    // ---- per-node epilogue, entry-parallel in warp-private smem.
-    // Entry e = (q, a, b): node q of the warp, row a, column b; flat index e = (q*D + a)*D + b,
-    // which equals the accumulator index r*D + k with r = q*D + a (row of the panel), k = b.
+    // ---- per-node epilogue (epilogue.cuh), entry-parallel in warp-private smem.
     const int64_t node_base = (int64_t)panel * C::NODES + warp * C::NPW;   // local node of q = 0
     const int64_t rem = p.n_local - node_base;
     const int nvalid = rem <= 0 ? 0 : (rem < C::NPW ? (int)rem : C::NPW);
-#pragma unroll
-    for (int m = 0; m < C::EPL; ++m) {
-      const int e = lane + 32 * m;
-      if (e < C::E) {
-        const int q = e / C::DD, a = (e / D) % D, b = e % D;
-        T x = T(0);
-        if (q < nvalid) {
-          const int64_t c = (p.node0 + node_base + q) * D + a;
-          x = Xg[tile_index(c, b, D, p.rows_local, p.tiles_per_rank)];
-        }
-        sX[e] = x;
-      }
-    }
+    double g1s[C::DDL], g2s[C::DDL], so = 0.0, xs = 0.0;
+    node_epilogue<T, D, C::NPW, MODE>(p, Xg, lane, node_base, nvalid, sX, sG, sH, sS, sM, g1s, g2s, so, xs,
+                                      ns_region, err);
+    commit(split_panel, panel, g1s, g2s, so, xs);
     __syncwarp();
-
-    if constexpr (MODE == kModeProduct) {
-      // W = A Y rows -> Xout; Gram partials W^T W and Y^T W (Cholesky-QR of the sweep).
-      T *Wout = static_cast<T *>(p.Xout);
-#pragma unroll
-      for (int m = 0; m < C::EPL; ++m) {
-        const int e = lane + 32 * m;
-        if (e < C::E) {
-          const int q = e / C::DD, a = (e / D) % D, b = e % D;
-          if (q < nvalid) {
-            const int64_t c = (p.node0 + node_base + q) * D + a;
-            Wout[tile_index(c, b, D, p.rows_local, p.tiles_per_rank)] = sG[e];
-          }
-        }
-      }
-      double g1s[C::DDL], g2s[C::DDL];
-#pragma unroll
-      for (int m = 0; m < C::DDL; ++m) {
-        const int e2 = lane + 32 * m;
-        double g1 = 0.0, g2 = 0.0;
-        if (e2 < C::DD) {
-          const int a = e2 / D, b = e2 % D;
-          for (int q = 0; q < nvalid; ++q)
-#pragma unroll
-            for (int k = 0; k < D; ++k) {
-              const double w_ka = (double)sG[(q * D + k) * D + a], w_kb = (double)sG[(q * D + k) * D + b];
-              g1 += w_ka * w_kb;
-              g2 += (double)sX[(q * D + k) * D + a] * w_kb;
-            }
-        }
-        g1s[m] = g1;
-        g2s[m] = g2;
-      }
-      commit(split_panel, panel, g1s, g2s, 0.0, 0.0);
-      __syncwarp();
-      continue;
-    } else {
-      // <X, B> and the X Gram terms of the objective expansion.
-      double xs = 0.0, so = 0.0;
-#pragma unroll
-      for (int m = 0; m < C::EPL; ++m) {
-        const int e = lane + 32 * m;
-        if (e < C::E && e / C::DD < nvalid) xs += (double)sX[e] * (double)sG[e];
-      }
-      double g1s[C::DDL], g2s[C::DDL];
-#pragma unroll
-      for (int m = 0; m < C::DDL; ++m) {
-        const int e2 = lane + 32 * m;
-        double g1 = 0.0;
-        if (e2 < C::DD) {
-          const int a = e2 / D, b = e2 % D;
-          for (int q = 0; q < nvalid; ++q) {
-            double v = 0.0;
-#pragma unroll
-            for (int k = 0; k < D; ++k)
-              v += (double)sX[(q * D + k) * D + a] * (double)sX[(q * D + k) * D + b];
-            g1 += v;
-            so += v * v;
-          }
-        }
-        g1s[m] = g1;
-        g2s[m] = 0.0;
-      }
-      commit(split_panel, panel, g1s, g2s, so, xs);
-      if constexpr (MODE == kModeObjective) {
-        __syncwarp();
-        continue;
-      }
-      if constexpr (MODE == kModeGpm) {
-        // GPM (comparison method): X_i <- sgn(B_i), B_i = sum_{j!=i} A_ij X_j, by
-        // Newton-Schulz from S_0 = B_i / ||B_i||_F (singular values in (0, 1]) to convergence.
-        T *inv = sM + C::E - C::NPW;   // scratch: per-node scale (sM is rewritten below)
-        if (lane < C::NPW) {
-          T f2 = T(0);
-          for (int e2 = 0; e2 < C::DD; ++e2) f2 += sG[lane * C::DD + e2] * sG[lane * C::DD + e2];
-          inv[lane] = f2 > T(0) ? T(1) / sqrt(f2) : T(0);
-        }
-        __syncwarp();
-#pragma unroll
-        for (int m = 0; m < C::EPL; ++m) {
-          const int e = lane + 32 * m;
-          if (e < C::E) sS[e] = sG[e] * inv[e / C::DD];
-        }
-        __syncwarp();
-        const T tol = sizeof(T) == 4 ? T(2e-5) : T(1e-13);
-        int polish = 2;
-        bool conv = false;
-        for (int it = 0; it < 60; ++it) {
-#pragma unroll
-          for (int m = 0; m < C::EPL; ++m) {
-            const int e = lane + 32 * m;
-            if (e < C::E) {
-              const int q = e / C::DD, a = (e / D) % D, b = e % D;
-              const T *Sq = sS + q * C::DD;
-              T v = T(0);
-#pragma unroll
-              for (int k = 0; k < D; ++k) v = tfma(Sq[k * D + a], Sq[k * D + b], v);
-              sM[e] = v;
-            }
-          }
-          __syncwarp();
-          bool ok = true;
-          if (lane < nvalid) {
-            T dev = T(0);
-            for (int e2 = 0; e2 < C::DD; ++e2) {
-              const T dv = (e2 / D == e2 % D ? T(1) : T(0)) - sM[lane * C::DD + e2];
-              dev += dv * dv;
-            }
-            ok = sqrt(dev) <= tol;
-          }
-          if (__all_sync(0xffffffffu, ok)) {
-            conv = true;
-            if (polish-- == 0) break;
-          }
-          T snew[C::EPL];
-#pragma unroll
-          for (int m = 0; m < C::EPL; ++m) {
-            const int e = lane + 32 * m;
-            snew[m] = T(0);
-            if (e < C::E) {
-              const int q = e / C::DD, a = (e / D) % D, b = e % D;
-              const T *Sq = sS + q * C::DD, *Mq = sM + q * C::DD;
-              T v = T(0);
-#pragma unroll
-              for (int k = 0; k < D; ++k) v = tfma(Sq[a * D + k], Mq[k * D + b], v);
-              snew[m] = T(1.5) * sS[e] - T(0.5) * v;
-            }
-          }
-          __syncwarp();
-#pragma unroll
-          for (int m = 0; m < C::EPL; ++m) {
-            const int e = lane + 32 * m;
-            if (e < C::E) sS[e] = snew[m];
-          }
-          __syncwarp();
-        }
-        if (!conv && nvalid > 0) err |= kErrSingular;
-      } else {
-      // G = (n-1) X - B   (in place in sG)
-#pragma unroll
-      for (int m = 0; m < C::EPL; ++m) {
-        const int e = lane + 32 * m;
-        if (e < C::E) sG[e] = coef * sX[e] - sG[e];
-      }
-      __syncwarp();
-      // H = G^T X
-#pragma unroll
-      for (int m = 0; m < C::EPL; ++m) {
-        const int e = lane + 32 * m;
-        if (e < C::E) {
-          const int q = e / C::DD, a = (e / D) % D, b = e % D;
-          const T *Gq = sG + q * C::DD, *Xq = sX + q * C::DD;
-          T h = T(0);
-#pragma unroll
-          for (int k = 0; k < D; ++k) h = tfma(Gq[k * D + a], Xq[k * D + b], h);
-          sH[e] = h;
-        }
-      }
-      __syncwarp();
-      // P = (G - X H)/2,  F = X - eta P
-#pragma unroll
-      for (int m = 0; m < C::EPL; ++m) {
-        const int e = lane + 32 * m;
-        if (e < C::E) {
-          const int q = e / C::DD, a = (e / D) % D, b = e % D;
-          const T *Hq = sH + q * C::DD, *Xq = sX + q * C::DD;
-          T xh = T(0);
-#pragma unroll
-          for (int k = 0; k < D; ++k) xh = tfma(Xq[a * D + k], Hq[k * D + b], xh);
-          const T P = T(0.5) * (sG[e] - xh);
-          sS[e] = sX[e] - eta * P;
-        }
-      }
-      __syncwarp();
-      // Algorithm 1: K Newton-Schulz steps S <- 1/2 S (3I - S^T S) = 1.5 S - 0.5 S (S^T S)
-      for (int it = 0; it < p.K; ++it) {
-#pragma unroll
-        for (int m = 0; m < C::EPL; ++m) {
-          const int e = lane + 32 * m;
-          if (e < C::E) {
-            const int q = e / C::DD, a = (e / D) % D, b = e % D;
-            const T *Sq = sS + q * C::DD;
-            T v = T(0);
-#pragma unroll
-            for (int k = 0; k < D; ++k) v = tfma(Sq[k * D + a], Sq[k * D + b], v);
-            sM[e] = v;
-          }
-        }
-        __syncwarp();
-        if (it == 0 && lane < nvalid) {   // ||I - F^T F||_F of node `lane` (PAPER.md:465 eq:conclusion:sigma)
-          const T *Mq = sM + lane * C::DD;
-          float acc2 = 0.f;
-          for (int e2 = 0; e2 < C::DD; ++e2) {
-            const float dv = (float)((e2 / D == e2 % D ? T(1) : T(0)) - Mq[e2]);
-            acc2 += dv * dv;
-          }
-          ns_region = fmaxf(ns_region, sqrtf(acc2));
-        }
-        T snew[C::EPL];
-#pragma unroll
-        for (int m = 0; m < C::EPL; ++m) {
-          const int e = lane + 32 * m;
-          snew[m] = T(0);
-          if (e < C::E) {
-            const int q = e / C::DD, a = (e / D) % D, b = e % D;
-            const T *Sq = sS + q * C::DD, *Mq = sM + q * C::DD;
-            T v = T(0);
-#pragma unroll
-            for (int k = 0; k < D; ++k) v = tfma(Sq[a * D + k], Mq[k * D + b], v);
-            snew[m] = T(1.5) * sS[e] - T(0.5) * v;
-          }
-        }
-        __syncwarp();
-#pragma unroll
-        for (int m = 0; m < C::EPL; ++m) {
-          const int e = lane + 32 * m;
-          if (e < C::E) sS[e] = snew[m];
-        }
-        __syncwarp();
-      }
-      }  // MODE == kModeRgs
-      // divergence guard: non-finite or ||S||_F > 10 sqrt(d)
-      if (lane < nvalid) {
-        const T *Sq = sS + lane * C::DD;
-        double f2 = 0.0;
-        for (int e2 = 0; e2 < C::DD; ++e2) f2 += (double)Sq[e2] * (double)Sq[e2];
-        if (!(f2 <= 100.0 * D)) err |= kErrDivergence;
-      }
-      T *Xo = static_cast<T *>(p.Xout);
-#pragma unroll
-      for (int m = 0; m < C::EPL; ++m) {
-        const int e = lane + 32 * m;
-        if (e < C::E) {
-          const int q = e / C::DD, a = (e / D) % D, b = e % D;
-          if (q < nvalid) {
-            const int64_t c = (p.node0 + node_base + q) * D + a;
-            Xo[tile_index(c, b, D, p.rows_local, p.tiles_per_rank)] = sS[e];
-          }
-        }
-      }
-      __syncwarp();
-    }
   }
 
   // ------------------------------------------------------------------ CTA + grid reduction
