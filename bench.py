@@ -200,6 +200,8 @@ def run_gpu(args, cfg):
     stream = torch.cuda.Stream()
     s = nsrgs.Solver(n, d, nsrgs.F32, rank=rank, world=world, device=local, nccl_id=nid, stream=stream)
     Zh = s.generate(0, cfg["sigma"])                     # A shard generated on the device, resident
+    if args.symmetric:
+        s.set_symmetric(True)
     Zd = torch.from_numpy(Zh).to(f"cuda:{local}")
     Zpin = torch.from_numpy(Zh).pin_memory()
     Xpin = torch.empty((n, d, d), dtype=torch.float32).pin_memory()
@@ -265,11 +267,13 @@ def run_gpu(args, cfg):
     value = T * args.steps / (ms / 1e3)
     e2e_value = T * args.steps / (ms_e2e / 1e3)
     peak, peak_kind = _peaks()
-    bytes_launch = 4 * rows_local * N + 4 * N * d + 4 * rows_local * d
+    # A shard + X^t in + X^{t+1} out; the symmetric pass needs only the upper half
+    a_bytes = 4 * (N * (N + 1) // 2) if args.symmetric else 4 * rows_local * N
+    bytes_launch = a_bytes + 4 * N * d + 4 * rows_local * d
     avg_ms = st["panel_ms_total"] / max(1, st["panel_launches"])
     achieved = bytes_launch / (avg_ms / 1e3) / 1e9
     passes = st["panel_launches"] / args.steps                              # A passes per solve
-    eff_gbs = passes * 4 * rows_local * N * args.steps / (ms / 1e3) / 1e9 * world
+    eff_gbs = passes * a_bytes * args.steps / (ms / 1e3) / 1e9 * world
     if rank != 0:
         s.close()
         return
@@ -285,7 +289,8 @@ def run_gpu(args, cfg):
         "metric": METRIC, "value": value, "unit": "it/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (on-device Philox instance, PAPER.md §4.1 model)",
-        "config": {**_config_dict(args, cfg, world), "init_sweeps": sweeps},
+        "config": {**_config_dict(args, cfg, world), "init_sweeps": sweeps,
+                   "storage": "symmetric half (upper triangle read)" if args.symmetric else "dense row-major shard"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "peak_kind": peak_kind, "kernel": "panel_kernel (fused A.X + epilogue)",
                      "bytes_per_launch": bytes_launch, "avg_launch_ms": avg_ms,
@@ -323,6 +328,7 @@ def main():
     ap.add_argument("--sample-nodes", type=int, default=50)
     ap.add_argument("--cpu-budget", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--symmetric", action="store_true", help="symmetric half-storage pass (d <= 6, 1 GPU)")
     args = ap.parse_args()
     if args.config is None:
         args.config = "c3"

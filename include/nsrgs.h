@@ -174,6 +174,15 @@ int nsrgs_alignment_error(nsrgs_ctx *ctx, const void *Z, int Z_on_device, double
 int nsrgs_set_X(nsrgs_ctx *ctx, const void *X, int on_device);
 int nsrgs_get_X(nsrgs_ctx *ctx, void *X, int on_device);
 
+/* Symmetric half-storage pass (A symmetric by PAPER.md:227): when enabled,
+ * every A pass reads only the upper half of A (row panel p: columns >= its first row, tile
+ * aligned) and forms B = A X from both A_ij X_j and the mirrored A_ij^T X_i — half the HBM
+ * bytes, twice the FMAs per byte.  Requires the stored A to be exactly symmetric (true for
+ * nsrgs_generate; the caller's responsibility for nsrgs_attach_A).  Supported: world == 1,
+ * F32, d in [2, 6]; otherwise NSRGS_ERR_INVALID_ARG.  enable = 0 returns to the dense pass.
+ * Results are deterministic but differ from the dense pass by fp32 summation order. */
+int nsrgs_set_symmetric(nsrgs_ctx *ctx, int enable);
+
 /* Launch configuration + measurement hooks (bench / tests).  */
 typedef struct {
   int32_t grid, threads, stages, rows_per_panel;     /* panel kernel launch shape              */
@@ -184,6 +193,8 @@ typedef struct {
   int64_t kernel_launches;      /* all library kernel launches since reset                     */
   double ns_region_max;         /* max over nodes of ||I - F_i^T F_i||_F seen since reset        */
   double a_fro2;                /* ||A||_F^2 (global)                                           */
+  int32_t symmetric;            /* 1 if the symmetric half-storage pass is active               */
+  int64_t a_bytes_per_pass;     /* A bytes one pass requests from memory (full shard or ~half)  */
 } nsrgs_stats_t;
 int nsrgs_get_stats(nsrgs_ctx *ctx, nsrgs_stats_t *out);
 int nsrgs_reset_stats(nsrgs_ctx *ctx, int enable_panel_timing);

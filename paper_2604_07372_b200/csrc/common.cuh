@@ -35,6 +35,19 @@ struct PanelParams {
   int K;                // Newton-Schulz steps (Algorithm 1)
 };
 
+// Symmetric half-storage pass (sym.cu): blocks of GP panels x kSymTilesPerBlock column tiles.
+constexpr int kSymTilesPerBlock = 4;
+constexpr int kSymPanelsPerBlock = 16;
+struct SymParams {
+  PanelParams e;          // epilogue + partial-reduction fields (X, Xout, n, node0, coef, eta, K, ...)
+  float *rowpart;         // [nJ][N][d]  row-direction partials of (panel, column group J)
+  float *colpart;         // [nI][N][d]  column-direction partials of (row group I, column)
+  const int4 *blocks;     // active upper-triangle blocks (I, J, p_first, p_last), largest first
+  unsigned *sched_cnt;    // block queue head (reset by the final kernel)
+  int nblocks, nt, nJ, gp;
+  int64_t N;
+};
+
 constexpr int kErrDivergence = 1;   // ||S||_F > 10 sqrt(d) or non-finite after NS
 constexpr int kErrSingular = 2;     // init polar did not converge / Cholesky failed
 constexpr int kErrNonfinite = 4;
@@ -104,13 +117,16 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t by
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// try_wait with a suspend-time hint: the waiting thread is parked until the phase completes
+// (or the hint expires) instead of spinning, so an idle producer does not steal issue slots
+// from the consumer warp that shares its scheduler.
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
   uint32_t addr = smem_u32(bar);
   asm volatile(
       "{\n\t.reg .pred P1;\n"
       "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-      "@!P1 bra WAIT_%=;\n\t}" ::"r"(addr), "r"(parity)
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}" ::"r"(addr), "r"(parity), "r"(0x989680u)
       : "memory");
 }
 __device__ __forceinline__ uint64_t policy_evict_first() {

@@ -15,6 +15,12 @@ namespace nsrgs {
 
 template <typename T> __device__ __forceinline__ T tfma(T a, T b, T c) { return fma(a, b, c); }
 
+template <typename T> __device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
 template <typename T, int D, int NPW, int MODE>
 __device__ __forceinline__ void node_epilogue(const PanelParams &p, const T *Xg, int lane, int64_t node_base,
                                               int nvalid, T *sX, T *sG, T *sH, T *sS, T *sM,

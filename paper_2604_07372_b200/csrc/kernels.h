@@ -17,6 +17,13 @@ struct PanelShape {
 cudaError_t panel_dispatch(int dtype, int d, int mode, bool shape_only, PanelShape *shape,
                            const CUtensorMap *tm, const PanelParams *p, int grid, cudaStream_t s);
 
+// sym.cu: symmetric half-storage pass (fp32, world == 1, d in [2, 6]).
+struct SymShape {
+  int rows, nodes, stages, smem, gt, npw, final_nodes_per_cta;
+};
+cudaError_t sym_dispatch(int d, int mode, bool shape_only, SymShape *shape, const CUtensorMap *tm, const SymParams *sp,
+                         int grid, cudaStream_t s);
+
 // aux.cu
 cudaError_t launch_gen_Z(int dtype, int d, int64_t n, uint64_t seed, double *Z64, void *Zt, cudaStream_t s);
 cudaError_t launch_gen_A(int dtype, int d, int64_t n, int64_t node0, int64_t n_local, uint64_t seed,

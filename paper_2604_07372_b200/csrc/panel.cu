@@ -72,11 +72,6 @@ __device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
   return d;
 }
 
-template <typename T> __device__ __forceinline__ T warp_sum(T v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
 
 // Stream-K schedule: the panels x tiles steps are cut into gridDim.x equal contiguous ranges.
 __device__ __forceinline__ int64_t sk_bound(int64_t W, int G, int b) { return W * b / G; }
@@ -95,7 +90,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   using C = PanelCfg<T, D>;
   using V = typename Vec4<T>::type;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // align to 1 KB by offsetting the shared array itself (keeps the shared address space, so
+  // every smem access below compiles to LDS/STS rather than generic LD/ST)
+  uint8_t *smem = smem_raw + (((smem_u32(smem_raw) + 1023u) & ~1023u) - smem_u32(smem_raw));
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + C::STAGES * C::STAGE_BYTES);
   uint64_t *empty = full + 8;
   T *scr_all = reinterpret_cast<T *>(smem + C::STAGES * C::STAGE_BYTES + C::BAR_BYTES);

@@ -120,6 +120,15 @@ struct nsrgs_ctx {
   PanelShape shape{};
   int sm_count = 0, grid = 0, panels = 0, total_tiles = 0;
   float a_keep = 0.f;   // L2 evict_last fraction for A (only when the shard is within ~4x of L2)
+  // symmetric half-storage pass (sym.cu)
+  bool sym = false;
+  SymShape symshape{};
+  float *rowpart = nullptr, *colpart = nullptr;
+  int4 *blocks = nullptr;
+  unsigned *sym_cnt = nullptr;   // [0] block queue head, [1] final-kernel done counter
+  double *sym_part = nullptr;
+  int nblocks = 0, nJ = 0, nI = 0, sym_grid = 0;
+  int64_t a_bytes_pass = 0;
   int64_t steps = 0;
   // scratch
   double *cta_part = nullptr;   // grid * npart
@@ -311,7 +320,25 @@ int launch_panel(nsrgs_ctx *c, int mode, const void *Xin, void *Xout, double *re
     }
     CUDA_TRY(c, cudaEventRecord(c->ev[c->ev_used], c->stream));
   }
-  CUDA_TRY(c, panel_dispatch(c->dtype, c->d, mode, false, nullptr, &c->tmA, &p, c->grid, c->stream));
+  if (c->sym) {
+    SymParams sp{};
+    sp.e = p;
+    sp.e.cta_part = c->sym_part;
+    sp.e.done_cnt = c->sym_cnt + 1;
+    sp.rowpart = c->rowpart;
+    sp.colpart = c->colpart;
+    sp.blocks = c->blocks;
+    sp.sched_cnt = c->sym_cnt;
+    sp.nblocks = c->nblocks;
+    sp.nt = (int)c->plan.tiles_per_rank;
+    sp.nJ = c->nJ;
+    sp.gp = kSymPanelsPerBlock;
+    sp.N = c->N;
+    CUDA_TRY(c, sym_dispatch(c->d, mode, false, nullptr, &c->tmA, &sp, c->sym_grid, c->stream));
+    c->kernel_launches++;
+  } else {
+    CUDA_TRY(c, panel_dispatch(c->dtype, c->d, mode, false, nullptr, &c->tmA, &p, c->grid, c->stream));
+  }
   if (c->timing) {
     CUDA_TRY(c, cudaEventRecord(c->ev[c->ev_used + 1], c->stream));
     c->ev_used += 2;
@@ -399,7 +426,7 @@ int nsrgs_destroy(nsrgs_ctx *c) {
   if (c->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(c->comm);
   for (auto e : c->ev) cudaEventDestroy(e);
   void *bufs[] = {c->X[0], c->X[1], c->stage, c->cta_part, c->counters, c->Bpart, c->res, c->red_part, c->small,
-                  c->err, c->ns_region};
+                  c->err, c->ns_region, c->rowpart, c->colpart, c->blocks, c->sym_cnt, c->sym_part};
   for (void *b : bufs)
     if (b) cudaFree(b);
   if (c->own_A && c->A) cudaFree(c->A);
@@ -763,6 +790,69 @@ int nsrgs_alignment_error(nsrgs_ctx *c, const void *Z, int Z_on_device, double o
   return NSRGS_OK;
 }
 
+int nsrgs_set_symmetric(nsrgs_ctx *c, int enable) {
+  NSRGS_TRY(enter(c));
+  if (!enable) {
+    c->sym = false;
+    return NSRGS_OK;
+  }
+  if (c->world != 1 || c->dtype != NSRGS_F32 || c->d > 6)
+    return set_err(c, NSRGS_ERR_INVALID_ARG, "symmetric storage: world == 1, F32, d in [2, 6] only");
+  if (c->sym) return NSRGS_OK;
+  CUDA_TRY(c, sym_dispatch(c->d, 0, true, &c->symshape, nullptr, nullptr, 0, nullptr));
+  if (c->symshape.rows != c->shape.rows)
+    return set_err(c, NSRGS_ERR_STATE, "symmetric storage: panel height mismatch (internal)");
+  const int64_t R = c->symshape.rows, N = c->N, nt = c->plan.tiles_per_rank;
+  const int GT = c->symshape.gt, GP = kSymPanelsPerBlock;
+  const int np = c->panels;
+  c->nJ = (int)ceil_div(nt, GT);
+  c->nI = (int)ceil_div(np, GP);
+  struct Blk { int I, J, p0, p1; int64_t cost; };
+  std::vector<Blk> blks;
+  int64_t bytes = 0;
+  for (int p = 0; p < np; ++p) {
+    const int64_t rows = std::min<int64_t>(R, N - (int64_t)p * R);
+    const int64_t t0 = (int64_t)p * R / kColTile;
+    bytes += rows * (N - t0 * kColTile) * 4;
+  }
+  for (int I = 0; I < c->nI; ++I) {
+    const int p0 = I * GP, p1 = std::min(np, (I + 1) * GP) - 1;
+    for (int J = 0; J < c->nJ; ++J) {
+      const int64_t tlo = (int64_t)J * GT, thi = std::min<int64_t>(nt, (int64_t)(J + 1) * GT);
+      int plast = -1;
+      int64_t cost = 0;
+      for (int p = p0; p <= p1; ++p) {
+        const int64_t t0 = (int64_t)p * R / kColTile;
+        if (t0 >= thi) break;
+        plast = p;
+        cost += thi - std::max(tlo, t0);
+      }
+      if (plast >= p0) blks.push_back({I, J, p0, plast, cost});
+    }
+  }
+  std::stable_sort(blks.begin(), blks.end(), [](const Blk &a, const Blk &b) { return a.cost > b.cost; });
+  std::vector<int4> hb(blks.size());
+  for (size_t i = 0; i < blks.size(); ++i) hb[i] = make_int4(blks[i].I, blks[i].J, blks[i].p0, blks[i].p1);
+  c->nblocks = (int)hb.size();
+  c->sym_grid = std::min(c->nblocks, c->sm_count);
+  c->a_bytes_pass = bytes;
+  const int fgrid = (int)ceil_div(c->plan.n_local, c->symshape.final_nodes_per_cta);
+  auto alloc0 = [&](void **p, size_t b) -> int {
+    CUDA_TRY(c, cudaMalloc(p, b));
+    CUDA_TRY(c, cudaMemsetAsync(*p, 0, b, c->stream));
+    return NSRGS_OK;
+  };
+  NSRGS_TRY(alloc0((void **)&c->rowpart, sizeof(float) * (size_t)c->nJ * N * c->d));
+  NSRGS_TRY(alloc0((void **)&c->colpart, sizeof(float) * (size_t)c->nI * N * c->d));
+  NSRGS_TRY(alloc0((void **)&c->blocks, sizeof(int4) * hb.size()));
+  NSRGS_TRY(alloc0((void **)&c->sym_cnt, 2 * sizeof(unsigned)));
+  NSRGS_TRY(alloc0((void **)&c->sym_part, sizeof(double) * (size_t)fgrid * c->shape.npart));
+  CUDA_TRY(c, cudaMemcpyAsync(c->blocks, hb.data(), sizeof(int4) * hb.size(), cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  c->sym = true;
+  return NSRGS_OK;
+}
+
 int nsrgs_get_stats(nsrgs_ctx *c, nsrgs_stats_t *o) {
   if (!c || !o) return NSRGS_ERR_INVALID_ARG;
   o->grid = c->grid;
@@ -783,6 +873,8 @@ int nsrgs_get_stats(nsrgs_ctx *c, nsrgs_stats_t *o) {
   o->kernel_launches = c->kernel_launches;
   o->ns_region_max = c->ns_region_max;
   o->a_fro2 = c->a_fro2;
+  o->symmetric = c->sym ? 1 : 0;
+  o->a_bytes_per_pass = c->sym ? c->a_bytes_pass : (int64_t)c->esz * c->plan.rows_local * c->N;
   return NSRGS_OK;
 }
 

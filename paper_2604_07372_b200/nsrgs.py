@@ -45,7 +45,8 @@ class Stats(ct.Structure):
     _fields_ = [("grid", ct.c_int32), ("threads", ct.c_int32), ("stages", ct.c_int32),
                 ("rows_per_panel", ct.c_int32), ("cut_panels", ct.c_int32), ("panels", ct.c_int64),
                 ("smem_bytes", ct.c_int64), ("panel_ms_total", ct.c_double), ("panel_launches", ct.c_int64),
-                ("kernel_launches", ct.c_int64), ("ns_region_max", ct.c_double), ("a_fro2", ct.c_double)]
+                ("kernel_launches", ct.c_int64), ("ns_region_max", ct.c_double), ("a_fro2", ct.c_double),
+                ("symmetric", ct.c_int32), ("a_bytes_per_pass", ct.c_int64)]
 
 
 _P = ct.c_void_p
@@ -72,6 +73,7 @@ _SIGS = {
     "nsrgs_set_X": ([_P, _P, ct.c_int], ct.c_int),
     "nsrgs_get_X": ([_P, _P, ct.c_int], ct.c_int),
     "nsrgs_get_stats": ([_P, ct.POINTER(Stats)], ct.c_int),
+    "nsrgs_set_symmetric": ([_P, ct.c_int], ct.c_int),
     "nsrgs_reset_stats": ([_P, ct.c_int], ct.c_int),
 }
 for _name, (_args, _res) in _SIGS.items():
@@ -254,6 +256,9 @@ class Solver:
         ptr, dev = self._ptr(out)
         self._check(_lib.nsrgs_get_X(self._h, ptr, dev))
         return out
+
+    def set_symmetric(self, enable: bool = True):
+        self._check(_lib.nsrgs_set_symmetric(self._h, int(enable)))
 
     def stats(self) -> dict:
         st = Stats()

@@ -334,3 +334,90 @@ def test_solve_protocol(nsrgs, alg):
     assert rel_fro(s.get_X(), X_it) <= 1e-10
     assert np.max(np.abs(tr - np.array(tr_o[:len(tr)]) if len(tr_o) >= len(tr) else 0) / tr[0]) <= 1e-10
     s.close()
+
+
+# ---------------------------------------------------------------------------- symmetric half storage (§8f row 1)
+SYM_CASES = [(2, 2, 0.3, 3), (7, 3, 0.5, 5), (100, 3, 0.5, 3), (43, 5, 1.0, 5), (50, 4, 1.5, 2), (33, 6, 0.9, 5),
+             (500, 3, 2.0, 5), (300, 5, 1.0, 5), (1000, 2, 0.5, 4)]
+
+
+@pytest.mark.parametrize("n,d,sigma,K", SYM_CASES)
+def test_symmetric_step_from_shared_iterate(nsrgs, n, d, sigma, K):
+    s = nsrgs.Solver(n, d)
+    s.generate(5, sigma, want_Z=False)
+    s.set_symmetric(True)
+    assert s.stats()["symmetric"] == 1
+    Z = inst.ground_truth(5, n, d)
+    A = inst.measurement_matrix(5, Z, sigma)
+    X = oracle_iterate_near(Z, 0.2, 1).astype(np.float32)
+    s.set_X(X)
+    f_gpu = s.step(1.0 / n, K)
+    Xo, _, _ = ons.step(A, X.astype(np.float64), 1.0 / n, K)
+    assert rel_fro(s.get_X(), Xo) <= 1e-6
+    fo = ons.objective(A, X.astype(np.float64))
+    assert abs(f_gpu - fo) <= 2e-6 * fo
+    s.close()
+
+
+def test_symmetric_modes_and_rejects(nsrgs):
+    n, d, sigma = 200, 3, 1.0
+    s = nsrgs.Solver(n, d)
+    Zg = s.generate(0, sigma)
+    s.set_symmetric(True)
+    Z = inst.ground_truth(0, n, d)
+    A = inst.measurement_matrix(0, Z, sigma)
+    s.init_spectral(0, 200, 1e-6, allow_unconverged=True)        # PRODUCT mode through sym_final
+    X0, _, _ = ons.spectral_init(A, d)
+    assert rel_mod_rotation(s.get_X(), X0) <= 1e-4
+    X = oracle_iterate_near(Z, 0.1, 3).astype(np.float32)
+    s.set_X(X)
+    s.gpm_run(1)                                                # GPM mode
+    assert rel_fro(s.get_X(), ons.gpm_step(A, X.astype(np.float64))) <= 1e-6
+    s.set_X(X)
+    assert s.objective() == pytest.approx(ons.objective(A, X.astype(np.float64)), rel=2e-6)
+    s.close()
+    with pytest.raises(nsrgs.NSRGSError):
+        t = nsrgs.Solver(30, 7)
+        t.generate(0, 0.5, want_Z=False)
+        t.set_symmetric(True)
+    with pytest.raises(nsrgs.NSRGSError):
+        t = nsrgs.Solver(30, 3, nsrgs.F64)
+        t.set_symmetric(True)
+
+
+@pytest.mark.parametrize("cfg", ["mid", "c3"])
+def test_symmetric_full_size_sampled_and_run(nsrgs, cfg):
+    n, d, sigma, K = FULL[cfg]
+    s = nsrgs.Solver(n, d)
+    Zg = s.generate(0, sigma)
+    s.set_symmetric(True)
+    Z = inst.ground_truth(0, n, d)
+    X = oracle_iterate_near(Z, 0.05, 3).astype(np.float32)
+    s.set_X(X)
+    s.step(1.0 / n, K)
+    Xg = s.get_X()
+    nodes = np.unique(np.r_[0, n - 1, np.random.default_rng(1).integers(0, n, 14)])
+    R = inst.measurement_rows(0, Z, sigma, nodes)
+    Xo = oracle_node_step(R, X.astype(np.float64), nodes, 1.0 / n, K)
+    assert rel_fro(Xg[nodes], Xo) <= 1e-5
+    s.init_spectral(0, 100, 1e-5, allow_unconverged=True)
+    tr = s.run(30, 1.0 / n, K)
+    assert np.all(np.diff(tr) <= 1e-6 * tr[0])
+    rel = s.alignment_error(Zg)[0]
+    assert abs(rel - sigma * np.sqrt((d - 1) / n)) <= 0.1 * rel
+    s.close()
+
+
+def test_symmetric_deterministic_and_matches_dense(nsrgs):
+    n, d = 900, 5
+    out = []
+    for sym in (True, True, False):
+        s = nsrgs.Solver(n, d)
+        s.generate(8, 1.0, want_Z=False)
+        s.set_symmetric(sym)
+        s.init_spectral(8, 50, 1e-5, allow_unconverged=True)
+        tr = s.run(10, 1.0 / n, 5)
+        out.append((s.get_X(), tr))
+        s.close()
+    assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1])
+    assert rel_mod_rotation(out[0][0], out[2][0]) <= 1e-5
