@@ -274,6 +274,25 @@ def run_gpu(args, cfg):
     achieved = bytes_launch / (avg_ms / 1e3) / 1e9
     passes = st["panel_launches"] / args.steps                              # A passes per solve
     eff_gbs = passes * a_bytes * args.steps / (ms / 1e3) / 1e9 * world
+    # §8(f) row 1 alongside the headline: the symmetric half-storage pass on the same instance
+    sym_variant = None
+    if world == 1 and d <= 6 and not args.symmetric and not args.no_sym_variant:
+        s.set_symmetric(True)
+        for _ in range(max(1, args.warmup - 1)):
+            solve()
+        s.reset_stats(timing=True)
+        with Clocks(local) as clk2:
+            ms_sym, (_, _, met_sym) = timed(args.steps, e2e=False)
+        st2 = s.stats()
+        s.set_symmetric(False)
+        avg2 = st2["panel_ms_total"] / max(1, st2["panel_launches"])
+        a_sym = 4 * (N * (N + 1) // 2)
+        sym_variant = {"value": T * args.steps / (ms_sym / 1e3), "unit": "it/s", "ms_per_step": ms_sym / args.steps,
+                       "avg_pass_ms": avg2, "a_bytes_per_pass_algorithmic": a_sym,
+                       "a_bytes_per_pass_read": st2["a_bytes_per_pass"],
+                       "achieved_gbs": (a_sym + 4 * N * d + 4 * rows_local * d) / (avg2 / 1e3) / 1e9,
+                       "rel_err": met_sym[0], "clocks": clk2.summary(),
+                       "note": "upper-triangle stream, 2 FMA directions per element (FFMA2/issue-bound, not HBM-bound)"}
     if rank != 0:
         s.close()
         return
@@ -312,6 +331,8 @@ def run_gpu(args, cfg):
     }
     if cpu:
         line["cpu_baseline"] = cpu
+    if sym_variant:
+        line["symmetric_variant"] = sym_variant
     print(json.dumps(line), flush=True)
     s.close()
     if world > 1:
@@ -329,6 +350,7 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--symmetric", action="store_true", help="symmetric half-storage pass (d <= 6, 1 GPU)")
+    ap.add_argument("--no-sym-variant", action="store_true", help="skip the extra symmetric-variant measurement")
     args = ap.parse_args()
     if args.config is None:
         args.config = "c3"

@@ -12,7 +12,7 @@ d x d with sign fix" for Z_i.  We fix:
 
 * Philox4x32-10 (Salmon, Moraes, Dror, Shaw, SC'11 "Parallel random numbers:
   as easy as 1, 2, 3"), key = (seed & 0xffffffff, seed >> 32), counter
-  (c0, c1, c2, c3) = (i, j, q, tag); tag 1 = Z, 2 = W, 3 = Y0.
+  (c0, c1, c2, c3) = (i, j, q, tag); tag 1 = Z, 2 = W, 3 = Y0, 4 = mask.
 * One Philox call -> two fp64 uniforms u = (m + 1) * 2^-53 in (0, 1], with
   m = (x0 >> 5) * 2^26 + (x1 >> 6) (resp. x2, x3) -> two Box-Muller normals
   r cos(2 pi u2), r sin(2 pi u2) with r = sqrt(-2 ln u1).  Call q yields the
@@ -24,7 +24,9 @@ d x d with sign fix" for Z_i.  We fix:
   A_ii = 0.  ``dtype=np.float64`` keeps the fp64 values (config c1 "fp64").
 
 The CUDA generator implements the same definition independently
-(paper_2604_07372_b200/csrc/generate.cu); the two share no code.
+(paper_2604_07372_b200/csrc/aux.cu, common.cuh); the two share no code.
+* p < 1: pair {i < j} observed iff u < p, u the first uniform of
+  counter (i, j, 0, 4); unobserved A_ij = A_ji = 0.
 """
 from __future__ import annotations
 
@@ -33,6 +35,7 @@ import numpy as np
 TAG_Z = 1
 TAG_W = 2
 TAG_Y0 = 3
+TAG_MASK = 4
 
 # Philox4x32 constants (Salmon et al., SC'11, §"Philox").
 _M0 = np.uint64(0xD2511F53)
@@ -91,6 +94,17 @@ def block_normals(seed: int, c0, c1, tag: int, count: int) -> np.ndarray:
     return z[:, :count]
 
 
+def observed(seed: int, i, j, p: float) -> np.ndarray:
+    """Observation mask of PAPER.md:300-310 (§4.1): the unordered pair {i, j} (i < j) is in the
+    edge set with probability p (reading R18: unordered pairs, symmetric mask).  Drawn as
+    u < p with u the first uniform of Philox counter (i, j, 0, TAG_MASK)."""
+    i = np.atleast_1d(np.asarray(i, dtype=np.uint64))
+    j = np.atleast_1d(np.asarray(j, dtype=np.uint64))
+    i, j = np.broadcast_arrays(i, j)
+    x0, x1, _, _ = philox4x32_10(i, j, np.uint64(0), np.uint64(TAG_MASK), seed & 0xFFFFFFFF, (seed >> 32) & 0xFFFFFFFF)
+    return _uniform53(x0, x1) < p
+
+
 def ground_truth(seed: int, n: int, d: int) -> np.ndarray:
     """Z in O(d)^{(x)n}, shape (n, d, d): Q of QR(G_i) with diag(R) > 0 (BASELINE configs)."""
     G = block_normals(seed, np.arange(n), 0, TAG_Z, d * d).reshape(n, d, d)
@@ -107,9 +121,10 @@ def noise_block(seed: int, i: int, j: int, d: int) -> np.ndarray:
     return block_normals(seed, i, j, TAG_W, d * d).reshape(d, d)
 
 
-def measurement_rows(seed: int, Z: np.ndarray, sigma: float, nodes, dtype=np.float32) -> np.ndarray:
+def measurement_rows(seed: int, Z: np.ndarray, sigma: float, nodes, dtype=np.float32, p: float = 1.0) -> np.ndarray:
     """Block rows of A for the given node indices: shape (len(nodes)*d, n*d), float64 array
-    holding `dtype`-rounded values.  Independent regeneration used for sampled parity."""
+    holding `dtype`-rounded values.  Independent regeneration used for sampled parity.
+    p < 1: unobserved blocks are 0."""
     n, d, _ = Z.shape
     nodes = np.asarray(nodes, dtype=np.int64)
     out = np.zeros((len(nodes) * d, n * d), dtype=np.float64)
@@ -122,17 +137,20 @@ def measurement_rows(seed: int, Z: np.ndarray, sigma: float, nodes, dtype=np.flo
         Wt = np.where((js > i)[:, None, None], W, np.transpose(W, (0, 2, 1)))
         blocks = np.einsum("ak,jbk->jab", Z[i], Z) + sigma * Wt  # (n, d, d): Z_i Z_j^T + sigma W_ij
         blocks = blocks.astype(dtype).astype(np.float64)
+        if p < 1.0:
+            blocks[~observed(seed, lo, hi, p)] = 0.0
         blocks[i] = 0.0  # A_ii = 0 ("W_ii = 0", self-loops excluded)
         out[k * d:(k + 1) * d, :] = blocks.transpose(1, 0, 2).reshape(d, n * d)
     return out
 
 
-def measurement_matrix(seed: int, Z: np.ndarray, sigma: float, dtype=np.float32) -> np.ndarray:
+def measurement_matrix(seed: int, Z: np.ndarray, sigma: float, dtype=np.float32, p: float = 1.0) -> np.ndarray:
     """Dense A (nd x nd), values rounded to `dtype`, returned as float64.
 
     Built from the upper blocks i < j; the lower blocks are the transposes of the
     SAME rounded values, so A is bitwise symmetric ("symmetric").
-    """
+    p < 1: each unordered pair is observed with probability p, else A_ij = A_ji = 0
+    (§4.1)."""
     n, d, _ = Z.shape
     A = np.zeros((n * d, n * d), dtype=np.float64)
     for i in range(n - 1):
@@ -140,6 +158,8 @@ def measurement_matrix(seed: int, Z: np.ndarray, sigma: float, dtype=np.float32)
         W = block_normals(seed, i, js, TAG_W, d * d).reshape(len(js), d, d)
         blocks = np.einsum("ak,jbk->jab", Z[i], Z[js]) + sigma * W
         blocks = blocks.astype(dtype).astype(np.float64)
+        if p < 1.0:
+            blocks[~observed(seed, i, js, p)] = 0.0
         row = blocks.transpose(1, 0, 2).reshape(d, len(js) * d)
         A[i * d:(i + 1) * d, (i + 1) * d:] = row
         A[(i + 1) * d:, i * d:(i + 1) * d] = row.T
