@@ -123,6 +123,12 @@ int nsrgs_attach_A(nsrgs_ctx *ctx, const void *A_shard_dev, int64_t lda);
  * nullable — receives the ground truth.  sigma >= 0. */
 int nsrgs_generate(nsrgs_ctx *ctx, uint64_t seed, double sigma, void *Z_out_host);
 
+/* As nsrgs_generate with incomplete observations (§4.1):
+ * the unordered pair {i < j} is observed iff u < p, u = first uniform of Philox counter
+ * (i, j, 0, 4); unobserved blocks A_ij = A_ji = 0 (stored densely — the bytes per pass do not
+ * shrink).  Use eta = 1/(n p) in nsrgs_run.  p in (0, 1]. */
+int nsrgs_generate_observed(nsrgs_ctx *ctx, uint64_t seed, double sigma, double p, void *Z_out_host);
+
 /* Copy rows [row0, row0+nrows) of THIS rank's A shard (local row index) to host `out`
  * (nrows x n d, dense).  Diagnostic / sampled-parity helper. */
 int nsrgs_copy_A_rows(nsrgs_ctx *ctx, int64_t row0, int64_t nrows, void *out_host);

@@ -72,7 +72,7 @@ __global__ void cast_kernel(const double *src, T *dst, int64_t count) {
 // A_ij = round(Z_i Z_j^T + sigma W_ij), W_ij from counter (min, max) transposed for i > j,
 // A_ii = 0.  ||A_shard||_F^2 partial per block (of the rounded values).
 template <typename T, int D>
-__global__ void gen_A_kernel(int64_t n, int64_t node0, int64_t n_local, uint64_t seed, double sigma,
+__global__ void gen_A_kernel(int64_t n, int64_t node0, int64_t n_local, uint64_t seed, double sigma, double p_obs,
                              const double *Z64, T *A, int64_t lda, double *part) {
   __shared__ double Zi[D * D];
   __shared__ double sh[32];
@@ -95,6 +95,16 @@ __global__ void gen_A_kernel(int64_t n, int64_t node0, int64_t n_local, uint64_t
     const double *Zj = Z64 + j * D * D;
     const uint32_t lo = (uint32_t)min(i, j), hi = (uint32_t)max(i, j);
     const bool tr = i > j;
+    if (p_obs < 1.0) {   // incomplete observations: pair {lo, hi} in the edge set?
+      const U4 v = philox4x32_10(lo, hi, 0u, 4u, (uint32_t)(seed & 0xffffffffu), (uint32_t)(seed >> 32));
+      if (!(uniform53(v.x, v.y) < p_obs)) {
+#pragma unroll
+        for (int a = 0; a < D; ++a)
+#pragma unroll
+          for (int b = 0; b < D; ++b) Ab[a * lda + b] = T(0);
+        continue;
+      }
+    }
 #pragma unroll
     for (int q = 0; q < (D * D + 1) / 2; ++q) {
       double w[2];
@@ -455,13 +465,14 @@ cudaError_t launch_gen_Z(int dtype, int d, int64_t n, uint64_t seed, double *Z64
 }
 
 cudaError_t launch_gen_A(int dtype, int d, int64_t n, int64_t node0, int64_t n_local, uint64_t seed, double sigma,
-                         const double *Z64, void *A, int64_t lda, double *part, int *nblocks, cudaStream_t s) {
+                         double p_obs, const double *Z64, void *A, int64_t lda, double *part, int *nblocks,
+                         cudaStream_t s) {
   dim3 grid(nblk(n, 128), (unsigned)(n_local < 32768 ? n_local : 32768));
   *nblocks = (int)(grid.x * grid.y);
   if (dtype == 0) {
-    NSRGS_D_SWITCH(d, (gen_A_kernel<float, D><<<grid, 128, 0, s>>>(n, node0, n_local, seed, sigma, Z64, (float *)A, lda, part)));
+    NSRGS_D_SWITCH(d, (gen_A_kernel<float, D><<<grid, 128, 0, s>>>(n, node0, n_local, seed, sigma, p_obs, Z64, (float *)A, lda, part)));
   } else {
-    NSRGS_D_SWITCH(d, (gen_A_kernel<double, D><<<grid, 128, 0, s>>>(n, node0, n_local, seed, sigma, Z64, (double *)A, lda, part)));
+    NSRGS_D_SWITCH(d, (gen_A_kernel<double, D><<<grid, 128, 0, s>>>(n, node0, n_local, seed, sigma, p_obs, Z64, (double *)A, lda, part)));
   }
   return cudaGetLastError();
 }

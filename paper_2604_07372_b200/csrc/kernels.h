@@ -27,7 +27,7 @@ cudaError_t sym_dispatch(int d, int mode, bool shape_only, SymShape *shape, cons
 // aux.cu
 cudaError_t launch_gen_Z(int dtype, int d, int64_t n, uint64_t seed, double *Z64, void *Zt, cudaStream_t s);
 cudaError_t launch_gen_A(int dtype, int d, int64_t n, int64_t node0, int64_t n_local, uint64_t seed,
-                         double sigma, const double *Z64, void *A, int64_t lda, double *part,
+                         double sigma, double p_obs, const double *Z64, void *A, int64_t lda, double *part,
                          int *nblocks, cudaStream_t s);
 cudaError_t launch_gen_Y0(int dtype, int d, int64_t n, uint64_t seed, void *Y, int64_t rows_local,
                           int64_t tiles_per_rank, cudaStream_t s);

@@ -528,8 +528,13 @@ int nsrgs_attach_A(nsrgs_ctx *c, const void *A_shard_dev, int64_t lda) {
 }
 
 int nsrgs_generate(nsrgs_ctx *c, uint64_t seed, double sigma, void *Z_out_host) {
+  return nsrgs_generate_observed(c, seed, sigma, 1.0, Z_out_host);
+}
+
+int nsrgs_generate_observed(nsrgs_ctx *c, uint64_t seed, double sigma, double p_obs, void *Z_out_host) {
   NSRGS_TRY(enter(c));
   if (!(sigma >= 0.0) || !std::isfinite(sigma)) return set_err(c, NSRGS_ERR_INVALID_ARG, "sigma must be finite, >= 0");
+  if (!(p_obs > 0.0 && p_obs <= 1.0)) return set_err(c, NSRGS_ERR_INVALID_ARG, "p must be in (0, 1]");
   const int64_t align = 16 / (int64_t)c->esz;
   const int64_t lda = ceil_div(c->N, align) * align;
   if (!(c->own_A && c->A && c->lda == lda)) {
@@ -549,8 +554,8 @@ int nsrgs_generate(nsrgs_ctx *c, uint64_t seed, double sigma, void *Z_out_host) 
   const int64_t nbx = ceil_div(c->n, 128), nby = std::min<int64_t>(c->plan.n_local, 32768);
   NSRGS_TRY(ensure_red(c, nbx * nby));
   int nb = 0;
-  CUDA_TRY(c, launch_gen_A(c->dtype, c->d, c->n, c->plan.node0, c->plan.n_local, seed, sigma, Z64, c->A, c->lda,
-                           c->red_part, &nb, c->stream));
+  CUDA_TRY(c, launch_gen_A(c->dtype, c->d, c->n, c->plan.node0, c->plan.n_local, seed, sigma, p_obs, Z64, c->A,
+                           c->lda, c->red_part, &nb, c->stream));
   c->kernel_launches++;
   if (Z_out_host)
     CUDA_TRY(c, cudaMemcpyAsync(Z_out_host, c->stage, c->esz * (size_t)(c->n * c->d * c->d), cudaMemcpyDeviceToHost,

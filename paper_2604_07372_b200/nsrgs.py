@@ -61,6 +61,7 @@ _SIGS = {
     "nsrgs_last_error": ([_P], ct.c_char_p),
     "nsrgs_attach_A": ([_P, _P, ct.c_int64], ct.c_int),
     "nsrgs_generate": ([_P, ct.c_uint64, ct.c_double, _P], ct.c_int),
+    "nsrgs_generate_observed": ([_P, ct.c_uint64, ct.c_double, ct.c_double, _P], ct.c_int),
     "nsrgs_copy_A_rows": ([_P, ct.c_int64, ct.c_int64, _P], ct.c_int),
     "nsrgs_init_spectral": ([_P, ct.c_uint64, ct.c_int, ct.c_double, ct.POINTER(ct.c_int)], ct.c_int),
     "nsrgs_step": ([_P, ct.c_double, ct.c_int, ct.POINTER(ct.c_double)], ct.c_int),
@@ -182,9 +183,13 @@ class Solver:
         return x.data_ptr(), int(x.is_cuda)
 
     # ------------------------------------------------------------------ C-ABI calls
-    def generate(self, seed: int, sigma: float, want_Z: bool = True):
+    def generate(self, seed: int, sigma: float, want_Z: bool = True, p: float = 1.0):
         Z = np.empty((self.n, self.d, self.d), dtype=self.np_dtype) if want_Z else None
-        self._check(_lib.nsrgs_generate(self._h, seed, sigma, Z.ctypes.data if want_Z else None))
+        zp = Z.ctypes.data if want_Z else None
+        if p == 1.0:
+            self._check(_lib.nsrgs_generate(self._h, seed, sigma, zp))
+        else:
+            self._check(_lib.nsrgs_generate_observed(self._h, seed, sigma, p, zp))
         return Z
 
     def attach_A(self, A_shard, lda: int | None = None):

@@ -421,3 +421,47 @@ def test_symmetric_deterministic_and_matches_dense(nsrgs):
         s.close()
     assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1])
     assert rel_mod_rotation(out[0][0], out[2][0]) <= 1e-5
+
+
+# ---------------------------------------------------------------------------- incomplete observations (§8f row 2)
+@pytest.mark.parametrize("n,d,sigma,p,dtype", [(100, 3, 0.5, 0.5, "f32"), (60, 5, 0.3, 0.8, "f64"), (40, 10, 0.2, 0.3, "f32")])
+def test_masked_generator_and_step(nsrgs, n, d, sigma, p, dtype):
+    code, npdt = _dt(nsrgs, dtype)
+    s = nsrgs.Solver(n, d, code)
+    s.generate(7, sigma, want_Z=False, p=p)
+    Z = inst.ground_truth(7, n, d)
+    A = inst.measurement_matrix(7, Z, sigma, dtype=npdt, p=p)
+    Ag = s.copy_A_rows(0, n * d).astype(np.float64)
+    assert np.array_equal(Ag == 0.0, A == 0.0)                         # same edge set (exact decision)
+    if dtype == "f32":
+        ulp = np.spacing(np.abs(A).astype(npdt)).astype(np.float64)
+        assert np.all(np.abs(Ag - A) <= ulp)
+    else:
+        assert np.max(np.abs(Ag - A)) <= 1e-13 * max(1.0, np.abs(A).max())
+    X = oracle_iterate_near(Z, 0.2, 1).astype(npdt)
+    s.set_X(X)
+    eta = 1.0 / (n * p)                                                # mu = 1/(np)
+    s.step(eta, 3)
+    Xo, _, _ = ons.step(A, X.astype(np.float64), eta, 3)
+    assert rel_fro(s.get_X(), Xo) <= (1e-6 if dtype == "f32" else 1e-12)
+    s.close()
+
+
+def test_masked_end_to_end_and_symmetric(nsrgs):
+    n, d, sigma, p, K, T = 400, 3, 0.3, 0.5, 3, 40
+    out = []
+    Z = inst.ground_truth(2, n, d)
+    A = inst.measurement_matrix(2, Z, sigma, p=p)
+    X0, _, _ = ons.spectral_init(A, d)
+    Xo = ons.run(A, X0, T, 1.0 / (n * p), K)
+    for sym in (False, True):
+        s = nsrgs.Solver(n, d)
+        Zg = s.generate(2, sigma, p=p)
+        s.set_symmetric(sym)
+        s.init_spectral(2, 300, 1e-6, allow_unconverged=True)
+        s.run(T, 1.0 / (n * p), K, trace=False)
+        assert rel_mod_rotation(s.get_X(), Xo) <= 1e-4
+        rel = s.alignment_error(Zg)[0]
+        assert abs(rel - mt.rel_err(Xo, Z)) <= 1e-3 * rel
+        assert abs(rel - sigma * np.sqrt((d - 1) / (n * p))) <= 0.15 * rel
+        s.close()
