@@ -33,6 +33,10 @@ struct PanelParams {
   double coef;          // n - 1   (identity term of G_i)
   double eta;           // step size mu
   int K;                // Newton-Schulz steps (Algorithm 1)
+  // multi-iteration persistent launch (world == 1, cooperative): iteration t reads X (t even) or
+  // Xout (t odd), writes the other; result slot t = result + t * npart; iter_cnt = grid barrier
+  int iters;
+  unsigned *iter_cnt;
 };
 
 // Symmetric half-storage pass (sym.cu): blocks of GP panels x kSymTilesPerBlock column tiles.
@@ -51,6 +55,7 @@ struct SymParams {
 constexpr int kErrDivergence = 1;   // ||S||_F > 10 sqrt(d) or non-finite after NS
 constexpr int kErrSingular = 2;     // init polar did not converge / Cholesky failed
 constexpr int kErrNonfinite = 4;
+constexpr int kErrTimeout = 8;      // multi-iteration grid barrier timed out (should never happen)
 
 // Tile layout of X: the N stack rows of one rank's slice are cut into column
 // tiles of 128; tile (g, j) holds dp = d rounded up to even components as dp/2 pair-blocks of
@@ -164,6 +169,15 @@ __device__ __forceinline__ void bulk_load(void *smem_dst, const void *gsrc, uint
 }
 __device__ __forceinline__ void prefetch_tmap(const void *tmap) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tmap)) : "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned *p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// generic-proxy writes (other CTAs' X^{t+1} stores, acquired above) before async-proxy reads
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");

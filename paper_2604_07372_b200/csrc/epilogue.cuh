@@ -39,7 +39,7 @@ __device__ __forceinline__ void node_epilogue(const PanelParams &p, const T *Xg,
       T x = T(0);
       if (q < nvalid) {
         const int64_t c = (p.node0 + node_base + q) * D + a;
-        x = Xg[tile_index(c, b, D, p.rows_local, p.tiles_per_rank)];
+        x = __ldcg(Xg + tile_index(c, b, D, p.rows_local, p.tiles_per_rank));   // L2: written by other CTAs
       }
       sX[e] = x;
     }

@@ -111,8 +111,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   __syncthreads();
 
-  const T *Xg = static_cast<const T *>(p.X);
-
   // ------------------------------------------------------------------ producer warp
   if (warp == kWarps) {
     if (lane == 0) {
@@ -122,16 +120,31 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       const int64_t s_end = sk_bound(p.steps, gridDim.x, blockIdx.x + 1);
-      for (int64_t st = sk_bound(p.steps, gridDim.x, blockIdx.x); st < s_end; ++st) {
-        const int panel = (int)(st / p.total_tiles), t = (int)(st - (int64_t)panel * p.total_tiles);
-        const int tt = tile_of_step(t, p);
-        const int g = tt / (int)p.tiles_per_rank, jt = tt - g * (int)p.tiles_per_rank;
-        mbar_wait(&empty[stage], phase ^ 1u);
-        uint8_t *sb = smem + stage * C::STAGE_BYTES;
-        mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
-        tma_load_3d(sb, &tmA, &full[stage], jt * kColTile, g, panel * C::ROWS, pol_a);
-        bulk_load(sb + C::A_BYTES, Xg + (int64_t)tt * C::DP * kColTile, C::X_BYTES, &full[stage], pol_x);
-        if (++stage == C::STAGES) { stage = 0; phase ^= 1u; }
+      for (int it = 0; it < p.iters; ++it) {
+        const T *Xin = static_cast<const T *>((it & 1) ? p.Xout : p.X);
+        bool ready = it == 0;
+        for (int64_t st = sk_bound(p.steps, gridDim.x, blockIdx.x); st < s_end; ++st) {
+          const int panel = (int)(st / p.total_tiles), t = (int)(st - (int64_t)panel * p.total_tiles);
+          const int tt = tile_of_step(t, p);
+          const int g = tt / (int)p.tiles_per_rank, jt = tt - g * (int)p.tiles_per_rank;
+          mbar_wait(&empty[stage], phase ^ 1u);
+          uint8_t *sb = smem + stage * C::STAGE_BYTES;
+          mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
+          tma_load_3d(sb, &tmA, &full[stage], jt * kColTile, g, panel * C::ROWS, pol_a);
+          if (!ready) {
+            // A of iteration `it` is already in flight; X^it needs every CTA's epilogues of it-1
+            const unsigned target = (unsigned)it * gridDim.x;
+            unsigned spins = 0;
+            while (ld_acquire_gpu(p.iter_cnt) < target) {
+              __nanosleep(64);
+              if (++spins > (1u << 26)) { atomicOr(p.err, kErrTimeout); break; }
+            }
+            fence_proxy_async_global();
+            ready = true;
+          }
+          bulk_load(sb + C::A_BYTES, Xin + (int64_t)tt * C::DP * kColTile, C::X_BYTES, &full[stage], pol_x);
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1u; }
+        }
       }
     }
     return;
@@ -195,6 +208,21 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   int stage = 0;
   uint32_t phase = 0;
+  for (int it = 0; it < p.iters; ++it) {
+  PanelParams pt = p;                 // per-iteration view: X^it in, X^{it+1} out, result slot it
+  pt.X = (it & 1) ? p.Xout : p.X;
+  pt.Xout = (it & 1) ? const_cast<void *>(p.X) : p.Xout;
+  pt.result = p.result + (int64_t)it * C::NPART;
+  const T *Xg = static_cast<const T *>(pt.X);
+  if (it > 0) {
+#pragma unroll
+    for (int m = 0; m < C::DDL; ++m) {
+      const int e = lane + 32 * m;
+      if (e < C::DD) { gram1[e] = 0.0; gram2[e] = 0.0; }
+    }
+    s_own = 0.0;
+    xb = 0.0;
+  }
   const int64_t my_s0 = sk_bound(p.steps, gridDim.x, blockIdx.x);
   const int64_t my_s1 = sk_bound(p.steps, gridDim.x, blockIdx.x + 1);
   const int first_panel = (int)(my_s0 / p.total_tiles);
@@ -347,7 +375,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int64_t rem = p.n_local - node_base;
     const int nvalid = rem <= 0 ? 0 : (rem < C::NPW ? (int)rem : C::NPW);
     double g1s[C::DDL], g2s[C::DDL], so = 0.0, xs = 0.0;
-    node_epilogue<T, D, C::NPW, MODE>(p, Xg, lane, node_base, nvalid, sX, sG, sH, sS, sM, g1s, g2s, so, xs,
+    node_epilogue<T, D, C::NPW, MODE>(pt, Xg, lane, node_base, nvalid, sX, sG, sH, sS, sM, g1s, g2s, so, xs,
                                       ns_region, err);
     commit(split_panel, panel, g1s, g2s, so, xs);
     __syncwarp();
@@ -389,10 +417,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       double v = 0.0;
       for (int b = lane; b < nslots; b += 32) v += __ldcg(p.cta_part + (int64_t)b * C::NPART + i);
       v = warp_sum(v);
-      if (lane == 0) p.result[i] = v;
+      if (lane == 0) pt.result[i] = v;
     }
     if (threadIdx.x == 0) *p.done_cnt = 0u;
   }
+  if (p.iters > 1) {   // grid barrier: this CTA's share of X^{it+1} (and partial slots) is done
+    named_bar_sync(1, kWarps * 32);
+    if (threadIdx.x == 0) {
+      __threadfence();
+      atomicAdd(p.iter_cnt, 1u);
+    }
+  }
+  }  // iterations
 }
 
 // ------------------------------------------------------------------ host-side launchers
@@ -405,6 +441,13 @@ static cudaError_t launch_impl(const CUtensorMap *tm, const PanelParams &p, int 
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return e;
     attr_set = true;
+  }
+  if (p.iters > 1) {   // all CTAs must be co-resident for the in-kernel grid barrier
+    CUtensorMap tmc = *tm;
+    PanelParams pc = p;
+    void *args[] = {&tmc, &pc};
+    return cudaLaunchCooperativeKernel(reinterpret_cast<const void *>(kern), dim3(grid), dim3(kThreads), args,
+                                       (size_t)C::SMEM, s);
   }
   kern<<<grid, kThreads, C::SMEM, s>>>(*tm, p);
   return cudaGetLastError();

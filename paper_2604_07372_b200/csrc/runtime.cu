@@ -14,6 +14,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -132,7 +133,8 @@ struct nsrgs_ctx {
   int64_t steps = 0;
   // scratch
   double *cta_part = nullptr;   // grid * npart
-  unsigned *counters = nullptr; // [0] done_cnt, [1..panels] panel counters
+  unsigned *counters = nullptr; // [0] done_cnt, [1..panels] panel counters, [panels+1] iteration barrier
+  bool coop = false;            // cooperative multi-iteration launches available (world == 1)
   void *Bpart = nullptr;
   double *res = nullptr;        // res_cap * npart
   int res_cap = 0;
@@ -287,8 +289,12 @@ int build_tmap(nsrgs_ctx *c) {
 }
 
 // One panel-kernel launch: X[src] -> out (mode), partials into res slot.
-int launch_panel(nsrgs_ctx *c, int mode, const void *Xin, void *Xout, double *result, double eta, int K) {
+int launch_panel(nsrgs_ctx *c, int mode, const void *Xin, void *Xout, double *result, double eta, int K,
+                 int iters = 1) {
   PanelParams p{};
+  p.iters = iters;
+  p.iter_cnt = c->counters + c->panels + 1;
+  if (iters > 1) CUDA_TRY(c, cudaMemsetAsync(p.iter_cnt, 0, sizeof(unsigned), c->stream));
   p.X = Xin;
   p.Xout = Xout;
   p.Bpart = c->Bpart;
@@ -343,7 +349,7 @@ int launch_panel(nsrgs_ctx *c, int mode, const void *Xin, void *Xout, double *re
     CUDA_TRY(c, cudaEventRecord(c->ev[c->ev_used + 1], c->stream));
     c->ev_used += 2;
   }
-  c->panel_launches++;
+  c->panel_launches += iters;   // per-pass statistics: one launch may run several iterations
   c->kernel_launches++;
   return NSRGS_OK;
 }
@@ -493,7 +499,7 @@ int nsrgs_create(const nsrgs_desc *desc, nsrgs_ctx **out) {
   const size_t xb = c->esz * (size_t)c->plan.x_elems;
   bool ok = alloc(&c->X[0], xb) && alloc(&c->X[1], xb) && alloc(&c->stage, c->esz * (size_t)(c->n * c->d * c->d)) &&
             alloc((void **)&c->cta_part, sizeof(double) * (size_t)c->grid * 2 * c->shape.npart) &&
-            alloc((void **)&c->counters, sizeof(unsigned) * (c->panels + 1)) &&
+            alloc((void **)&c->counters, sizeof(unsigned) * (c->panels + 2)) &&
             alloc((void **)&c->err, sizeof(int)) && alloc((void **)&c->ns_region, sizeof(unsigned));
   if (ok) ok = alloc(&c->Bpart, c->esz * (size_t)c->grid * 2 * c->shape.rows * c->d);
   if (!ok) return bail(NSRGS_ERR_OOM, "device allocation failed");
@@ -503,6 +509,12 @@ int nsrgs_create(const nsrgs_desc *desc, nsrgs_ctx **out) {
     ncclUniqueId id;
     std::memcpy(&id, desc->nccl_unique_id, sizeof id);
     if (g_nccl.CommInitRank(&c->comm, c->world, id, c->rank) != ncclSuccess) return bail(NSRGS_ERR_NCCL, "ncclCommInitRank failed");
+  }
+  {
+    int coop = 0;
+    cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, c->device);
+    const char *env = getenv("NSRGS_NO_COOP");
+    c->coop = coop && c->world == 1 && !(env && env[0] == '1');
   }
   if (cudaStreamSynchronize(c->stream) != cudaSuccess) return bail(NSRGS_ERR_CUDA);
   *out = c;
@@ -657,6 +669,7 @@ int nsrgs_init_spectral(nsrgs_ctx *c, uint64_t seed, int max_sweeps, double tol,
 }
 
 static int check_run_flags(nsrgs_ctx *c, int flags) {
+  if (flags & kErrTimeout) return set_err(c, NSRGS_ERR_CUDA, "multi-iteration grid barrier timed out");
   if (flags & kErrDivergence)
     return set_err(c, NSRGS_ERR_DIVERGENCE, "Newton-Schulz retraction diverged (||S||_F > 10 sqrt(d) or non-finite)");
   if (flags & kErrSingular)
@@ -670,10 +683,17 @@ static int run_impl(nsrgs_ctx *c, int mode, int T, double eta, int K, double *tr
     return set_err(c, NSRGS_ERR_INVALID_ARG, "run: need T >= 0, K >= 0, eta > 0");
   if (T == 0) return NSRGS_OK;
   NSRGS_TRY(ensure_res(c, T));
-  for (int t = 0; t < T; ++t) {
-    NSRGS_TRY(launch_panel(c, mode, c->X[c->cur], c->X[1 - c->cur], c->res + (size_t)t * c->shape.npart, eta, K));
-    NSRGS_TRY(allgather_X(c, c->X[1 - c->cur]));
-    c->cur = 1 - c->cur;
+  if (c->coop && !c->sym && T > 1) {
+    // one persistent cooperative launch for all T iterations (grid barrier between them, A
+    // prefetched across the boundary) — removes launch gaps and pipeline drains
+    NSRGS_TRY(launch_panel(c, mode, c->X[c->cur], c->X[1 - c->cur], c->res, eta, K, T));
+    if (T & 1) c->cur = 1 - c->cur;
+  } else {
+    for (int t = 0; t < T; ++t) {
+      NSRGS_TRY(launch_panel(c, mode, c->X[c->cur], c->X[1 - c->cur], c->res + (size_t)t * c->shape.npart, eta, K));
+      NSRGS_TRY(allgather_X(c, c->X[1 - c->cur]));
+      c->cur = 1 - c->cur;
+    }
   }
   if (trace) {
     NSRGS_TRY(allreduce_sum(c, c->res, (size_t)T * c->shape.npart));
