@@ -61,7 +61,7 @@ typedef enum { NSRGS_F32 = 0, NSRGS_F64 = 1 } nsrgs_dtype;
 /* Context description. */
 typedef struct {
   int64_t n;                    /* number of nodes (group elements), n >= 2                     */
-  int32_t d;                    /* block size; supported: 2..10 (F32), 2..6 (F64)               */
+  int32_t d;                    /* block size; supported: 2..10 and 12,16,20,24,25,32 (F32), 2..6 (F64) */
   int32_t dtype;                /* nsrgs_dtype: storage + arithmetic type of A, X (fp64 partials) */
   int32_t rank, world;          /* world >= 1, 0 <= rank < world, n % world == 0; for world > 1
                                    also (n/world)*d*sizeof(dtype) % 16 == 0 (TMA row-segment

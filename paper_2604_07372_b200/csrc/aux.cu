@@ -437,6 +437,262 @@ __global__ void metrics_final_kernel(int64_t n, const double *g, double *out) {
 }
 
 // ----------------------------------------------------------------------------------------
+// Runtime-d variants for wide blocks (d in (10, 32], wide.cu): same definitions as the
+// templated kernels above, loops not unrolled, small arrays in local memory (one-time work).
+__global__ void gen_Z_rt(int64_t n, int d, uint64_t seed, double *Z64) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double G[kMaxD * kMaxD];
+  for (int q = 0; q < (d * d + 1) / 2; ++q) {
+    double z0, z1;
+    normal_pair(seed, (uint32_t)i, 0u, (uint32_t)q, 1u, z0, z1);
+    G[2 * q] = z0;
+    if (2 * q + 1 < d * d) G[2 * q + 1] = z1;
+  }
+  for (int j = 0; j < d; ++j) {           // modified Gram-Schmidt on the columns (sign fix: R_jj > 0)
+    for (int k = 0; k < j; ++k) {
+      double r = 0.0;
+      for (int a = 0; a < d; ++a) r += G[a * d + k] * G[a * d + j];
+      for (int a = 0; a < d; ++a) G[a * d + j] -= r * G[a * d + k];
+    }
+    double nr = 0.0;
+    for (int a = 0; a < d; ++a) nr += G[a * d + j] * G[a * d + j];
+    nr = 1.0 / sqrt(nr);
+    for (int a = 0; a < d; ++a) G[a * d + j] *= nr;
+  }
+  for (int e = 0; e < d * d; ++e) Z64[i * d * d + e] = G[e];
+}
+
+template <typename T>
+__global__ void gen_A_rt(int64_t n, int d, int64_t node0, int64_t n_local, uint64_t seed, double sigma, double p_obs,
+                         const double *Z64, T *A, int64_t lda, double *part) {
+  __shared__ double sh[32];
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double ss = 0.0;
+  for (int64_t il = blockIdx.y; il < n_local; il += gridDim.y) {
+    const int64_t i = node0 + il;
+    if (j >= n) continue;
+    T *Ab = A + (il * d) * lda + j * d;
+    bool zero = (j == i);
+    const uint32_t lo = (uint32_t)min(i, j), hi = (uint32_t)max(i, j);
+    if (!zero && p_obs < 1.0) {
+      const U4 v = philox4x32_10(lo, hi, 0u, 4u, (uint32_t)(seed & 0xffffffffu), (uint32_t)(seed >> 32));
+      zero = !(uniform53(v.x, v.y) < p_obs);
+    }
+    if (zero) {
+      for (int a = 0; a < d; ++a)
+        for (int b = 0; b < d; ++b) Ab[a * lda + b] = T(0);
+      continue;
+    }
+    const double *Zi = Z64 + i * d * d, *Zj = Z64 + j * d * d;
+    const bool tr = i > j;
+    for (int q = 0; q < (d * d + 1) / 2; ++q) {
+      double w[2];
+      normal_pair(seed, lo, hi, (uint32_t)q, 2u, w[0], w[1]);
+      for (int h = 0; h < 2; ++h) {
+        const int e = 2 * q + h;
+        if (e < d * d) {
+          const int a = tr ? e % d : e / d, b = tr ? e / d : e % d;
+          double v = 0.0;
+          for (int k = 0; k < d; ++k) v += Zi[a * d + k] * Zj[b * d + k];
+          v += sigma * w[h];
+          const T tv = (T)v;
+          Ab[a * lda + b] = tv;
+          ss += (double)tv * (double)tv;
+        }
+      }
+    }
+  }
+  const double t = block_sum<T>(ss, sh);
+  if (threadIdx.x == 0) part[(int64_t)blockIdx.y * gridDim.x + blockIdx.x] = t;
+}
+
+template <typename T>
+__global__ void gen_Y0_rt(int64_t N, int d, uint64_t seed, T *Y, int64_t rows_local, int64_t tpr) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= N) return;
+  for (int q = 0; q < (d + 1) / 2; ++q) {
+    double z0, z1;
+    normal_pair(seed, (uint32_t)r, 0u, (uint32_t)q, 3u, z0, z1);
+    Y[tile_index(r, 2 * q, d, rows_local, tpr)] = (T)z0;
+    if (2 * q + 1 < d) Y[tile_index(r, 2 * q + 1, d, rows_local, tpr)] = (T)z1;
+  }
+}
+
+__global__ void chol_rt(int d, const double *res, double *MC, int *err) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double L[kMaxD * kMaxD], Li[kMaxD * kMaxD];
+  for (int e = 0; e < d * d; ++e) L[e] = Li[e] = 0.0;
+  bool ok = true;
+  for (int j = 0; j < d; ++j) {
+    double s = res[j * d + j];
+    for (int k = 0; k < j; ++k) s -= L[j * d + k] * L[j * d + k];
+    if (!(s > 0.0)) { ok = false; s = 1.0; }
+    L[j * d + j] = sqrt(s);
+    for (int i = j + 1; i < d; ++i) {
+      double t = res[i * d + j];
+      for (int k = 0; k < j; ++k) t -= L[i * d + k] * L[j * d + k];
+      L[i * d + j] = t / L[j * d + j];
+    }
+  }
+  for (int c = 0; c < d; ++c) {
+    Li[c * d + c] = 1.0 / L[c * d + c];
+    for (int i = c + 1; i < d; ++i) {
+      double t = 0.0;
+      for (int k = c; k < i; ++k) t += L[i * d + k] * Li[k * d + c];
+      Li[i * d + c] = -t / L[i * d + i];
+    }
+  }
+  for (int a = 0; a < d; ++a)
+    for (int b = 0; b < d; ++b) MC[a * d + b] = Li[b * d + a];
+  const double *Cm = res + d * d;
+  for (int a = 0; a < d; ++a)
+    for (int b = 0; b < d; ++b) {
+      double t = 0.0;
+      for (int k = 0; k < d; ++k) t += Cm[a * d + k] * Li[b * d + k];
+      MC[d * d + a * d + b] = t;
+    }
+  if (!ok) atomicOr(err, kErrSingular);
+}
+
+template <typename T>
+__global__ void scale_rt(int d, int64_t row0, int64_t rows, const double *MC, T *W, const T *Yold, int64_t rows_local,
+                         int64_t tpr, double *part) {
+  __shared__ double sh[32];
+  const int64_t rl = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double ss = 0.0;
+  if (rl < rows) {
+    const int64_t r = row0 + rl;
+    double w[kMaxD], y[kMaxD];
+    for (int k = 0; k < d; ++k) {
+      w[k] = (double)W[tile_index(r, k, d, rows_local, tpr)];
+      y[k] = (double)Yold[tile_index(r, k, d, rows_local, tpr)];
+    }
+    for (int b = 0; b < d; ++b) {
+      double v = 0.0, pr = 0.0;
+      for (int k = 0; k < d; ++k) {
+        v += w[k] * MC[k * d + b];
+        pr += y[k] * MC[d * d + k * d + b];
+      }
+      const T tv = (T)v;
+      W[tile_index(r, b, d, rows_local, tpr)] = tv;
+      const double dl = (double)tv - pr;
+      ss += dl * dl;
+    }
+  }
+  const double t = block_sum<T>(ss, sh);
+  if (threadIdx.x == 0) part[blockIdx.x] = t;
+}
+
+template <typename T>
+__global__ void polar_rt(int64_t n, int d, const T *Y, T *X, int64_t rows_local, int64_t tpr, int *err) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  T S[kMaxD * kMaxD], M[kMaxD * kMaxD], Sn[kMaxD * kMaxD];
+  T f2 = T(0);
+  for (int a = 0; a < d; ++a)
+    for (int b = 0; b < d; ++b) {
+      S[a * d + b] = Y[tile_index(i * d + a, b, d, rows_local, tpr)];
+      f2 += S[a * d + b] * S[a * d + b];
+    }
+  const T tol = sizeof(T) == 4 ? T(2e-5) * (T)d / T(3) : T(1e-13);
+  bool conv = false;
+  if (f2 > T(0) && isfinite((double)f2)) {
+    const T sc = T(1) / sqrt(f2);
+    for (int e = 0; e < d * d; ++e) S[e] *= sc;
+    int extra = 2;
+    for (int it = 0; it < 100; ++it) {
+      T dev = T(0);
+      for (int a = 0; a < d; ++a)
+        for (int b = 0; b < d; ++b) {
+          T v = T(0);
+          for (int k = 0; k < d; ++k) v += S[k * d + a] * S[k * d + b];
+          M[a * d + b] = v;
+          const T dv = (a == b ? T(1) : T(0)) - v;
+          dev += dv * dv;
+        }
+      if (sqrt(dev) <= tol) {
+        conv = true;
+        if (extra-- == 0) break;
+      }
+      for (int a = 0; a < d; ++a)
+        for (int b = 0; b < d; ++b) {
+          T v = T(0);
+          for (int k = 0; k < d; ++k) v += S[a * d + k] * M[k * d + b];
+          Sn[a * d + b] = T(1.5) * S[a * d + b] - T(0.5) * v;
+        }
+      for (int e = 0; e < d * d; ++e) S[e] = Sn[e];
+    }
+  }
+  if (!conv) atomicOr(err, kErrSingular);
+  for (int a = 0; a < d; ++a)
+    for (int b = 0; b < d; ++b) X[tile_index(i * d + a, b, d, rows_local, tpr)] = S[a * d + b];
+}
+
+template <typename T>
+__global__ void metrics_rt(int64_t n, int d, const T *X, const T *Z, int64_t rows_local, int64_t tpr, int64_t chunk,
+                           double *part) {
+  const int64_t i0 = (int64_t)blockIdx.x * chunk, i1 = min(n, i0 + chunk);
+  for (int e = threadIdx.x; e < 3 * d * d; e += blockDim.x) {
+    const int which = e / (d * d), a = (e / d) % d, b = e % d;
+    double s = 0.0;
+    for (int64_t i = i0; i < i1; ++i)
+      for (int k = 0; k < d; ++k) {
+        const double z_ka = (double)Z[(i * d + k) * d + a], z_kb = (double)Z[(i * d + k) * d + b];
+        const double x_ka = (double)X[tile_index(i * d + k, a, d, rows_local, tpr)];
+        const double x_kb = (double)X[tile_index(i * d + k, b, d, rows_local, tpr)];
+        s += which == 0 ? z_ka * z_kb : which == 1 ? x_ka * x_kb : z_ka * x_kb;
+      }
+    part[(int64_t)blockIdx.x * 3 * d * d + e] = s;
+  }
+}
+
+__global__ void metrics_final_rt(int64_t n, int d, const double *g, double *out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const double *ZZ = g, *XX = g + d * d, *ZX = g + 2 * d * d;
+  double zz = 0, xx = 0, zx = 0, trz = 0, trx = 0;
+  for (int e = 0; e < d * d; ++e) { zz += ZZ[e] * ZZ[e]; xx += XX[e] * XX[e]; zx += ZX[e] * ZX[e]; }
+  for (int a = 0; a < d; ++a) { trz += ZZ[a * d + a]; trx += XX[a * d + a]; }
+  double S[kMaxD * kMaxD];
+  for (int a = 0; a < d; ++a)
+    for (int b = 0; b < d; ++b) {
+      double v = 0.0;
+      for (int k = 0; k < d; ++k) v += ZX[k * d + a] * ZX[k * d + b];
+      S[a * d + b] = v;
+    }
+  for (int sweep = 0; sweep < 100; ++sweep) {   // cyclic Jacobi eigenvalues of (Z^T X)^T (Z^T X)
+    double off = 0.0;
+    for (int p = 0; p < d; ++p)
+      for (int q = p + 1; q < d; ++q) off += S[p * d + q] * S[p * d + q];
+    if (off < 1e-30) break;
+    for (int p = 0; p < d; ++p)
+      for (int q = p + 1; q < d; ++q) {
+        if (S[p * d + q] == 0.0) continue;
+        const double th = (S[q * d + q] - S[p * d + p]) / (2.0 * S[p * d + q]);
+        const double t = (th >= 0 ? 1.0 : -1.0) / (fabs(th) + sqrt(th * th + 1.0));
+        const double c = 1.0 / sqrt(t * t + 1.0), s = t * c;
+        for (int k = 0; k < d; ++k) {
+          const double skp = S[k * d + p], skq = S[k * d + q];
+          S[k * d + p] = c * skp - s * skq;
+          S[k * d + q] = s * skp + c * skq;
+        }
+        for (int k = 0; k < d; ++k) {
+          const double spk = S[p * d + k], sqk = S[q * d + k];
+          S[p * d + k] = c * spk - s * sqk;
+          S[q * d + k] = s * spk + c * sqk;
+        }
+      }
+  }
+  double nuc = 0.0;
+  for (int a = 0; a < d; ++a) nuc += sqrt(fmax(S[a * d + a], 0.0));
+  const double rel = sqrt(fmax(zz + xx - 2.0 * zx, 0.0)) / sqrt(zz);
+  const double df2 = fmax(trx + trz - 2.0 * nuc, 0.0);
+  out[0] = rel;
+  out[1] = sqrt(df2);
+  out[2] = df2 / (double)n;
+}
+
+// ----------------------------------------------------------------------------------------
 // dispatchers
 #define NSRGS_D_SWITCH(d, CALL)                   \
   switch (d) {                                   \
@@ -455,7 +711,11 @@ __global__ void metrics_final_kernel(int64_t n, const double *g, double *out) {
 static inline unsigned nblk(int64_t count, int threads) { return (unsigned)((count + threads - 1) / threads); }
 
 cudaError_t launch_gen_Z(int dtype, int d, int64_t n, uint64_t seed, double *Z64, void *Zt, cudaStream_t s) {
-  NSRGS_D_SWITCH(d, (gen_Z_kernel<D><<<nblk(n, 128), 128, 0, s>>>(n, seed, Z64)));
+  if (d > kMaxNarrowD) {
+    gen_Z_rt<<<nblk(n, 64), 64, 0, s>>>(n, d, seed, Z64);
+  } else {
+    NSRGS_D_SWITCH(d, (gen_Z_kernel<D><<<nblk(n, 128), 128, 0, s>>>(n, seed, Z64)));
+  }
   if (Zt) {
     const int64_t cnt = n * d * d;
     if (dtype == 0) cast_kernel<float><<<nblk(cnt, 256), 256, 0, s>>>(Z64, (float *)Zt, cnt);
@@ -469,6 +729,11 @@ cudaError_t launch_gen_A(int dtype, int d, int64_t n, int64_t node0, int64_t n_l
                          cudaStream_t s) {
   dim3 grid(nblk(n, 128), (unsigned)(n_local < 32768 ? n_local : 32768));
   *nblocks = (int)(grid.x * grid.y);
+  if (d > kMaxNarrowD) {
+    if (dtype == 0) gen_A_rt<float><<<grid, 128, 0, s>>>(n, d, node0, n_local, seed, sigma, p_obs, Z64, (float *)A, lda, part);
+    else gen_A_rt<double><<<grid, 128, 0, s>>>(n, d, node0, n_local, seed, sigma, p_obs, Z64, (double *)A, lda, part);
+    return cudaGetLastError();
+  }
   if (dtype == 0) {
     NSRGS_D_SWITCH(d, (gen_A_kernel<float, D><<<grid, 128, 0, s>>>(n, node0, n_local, seed, sigma, p_obs, Z64, (float *)A, lda, part)));
   } else {
@@ -480,6 +745,11 @@ cudaError_t launch_gen_A(int dtype, int d, int64_t n, int64_t node0, int64_t n_l
 cudaError_t launch_gen_Y0(int dtype, int d, int64_t n, uint64_t seed, void *Y, int64_t rows_local, int64_t tpr,
                           cudaStream_t s) {
   const int64_t N = n * d;
+  if (d > kMaxNarrowD) {
+    if (dtype == 0) gen_Y0_rt<float><<<nblk(N, 256), 256, 0, s>>>(N, d, seed, (float *)Y, rows_local, tpr);
+    else gen_Y0_rt<double><<<nblk(N, 256), 256, 0, s>>>(N, d, seed, (double *)Y, rows_local, tpr);
+    return cudaGetLastError();
+  }
   if (dtype == 0) {
     NSRGS_D_SWITCH(d, (gen_Y0_kernel<float, D><<<nblk(N, 256), 256, 0, s>>>(N, seed, (float *)Y, rows_local, tpr)));
   } else {
@@ -513,6 +783,10 @@ cudaError_t launch_pack(int dtype, int d, int64_t n, const void *stack, void *ti
 }
 
 cudaError_t launch_chol(int d, const double *res, double *MC, int *err, cudaStream_t s) {
+  if (d > kMaxNarrowD) {
+    chol_rt<<<1, 32, 0, s>>>(d, res, MC, err);
+    return cudaGetLastError();
+  }
   NSRGS_D_SWITCH(d, (chol_kernel<D><<<1, 32, 0, s>>>(res, MC, err)));
   return cudaGetLastError();
 }
@@ -521,6 +795,13 @@ cudaError_t launch_scale(int dtype, int d, int64_t node0, int64_t n_local, const
                          int64_t rows_local, int64_t tpr, double *part, int *nblocks, cudaStream_t s) {
   const int64_t rows = n_local * d, row0 = node0 * d;
   *nblocks = (int)nblk(rows, 256);
+  if (d > kMaxNarrowD) {
+    if (dtype == 0)
+      scale_rt<float><<<nblk(rows, 256), 256, 0, s>>>(d, row0, rows, MC, (float *)W, (const float *)Yold, rows_local, tpr, part);
+    else
+      scale_rt<double><<<nblk(rows, 256), 256, 0, s>>>(d, row0, rows, MC, (double *)W, (const double *)Yold, rows_local, tpr, part);
+    return cudaGetLastError();
+  }
   if (dtype == 0) {
     NSRGS_D_SWITCH(d, (scale_kernel<float, D><<<nblk(rows, 256), 256, 0, s>>>(row0, rows, MC, (float *)W,
                                                                              (const float *)Yold, rows_local, tpr, part)));
@@ -533,6 +814,11 @@ cudaError_t launch_scale(int dtype, int d, int64_t node0, int64_t n_local, const
 
 cudaError_t launch_polar(int dtype, int d, int64_t n, const void *Y, void *X, int64_t rows_local, int64_t tpr, int *err,
                          cudaStream_t s) {
+  if (d > kMaxNarrowD) {
+    if (dtype == 0) polar_rt<float><<<nblk(n, 32), 32, 0, s>>>(n, d, (const float *)Y, (float *)X, rows_local, tpr, err);
+    else polar_rt<double><<<nblk(n, 32), 32, 0, s>>>(n, d, (const double *)Y, (double *)X, rows_local, tpr, err);
+    return cudaGetLastError();
+  }
   if (dtype == 0) {
     NSRGS_D_SWITCH(d, (polar_kernel<float, D><<<nblk(n, 64), 64, 0, s>>>(n, (const float *)Y, (float *)X, rows_local, tpr, err)));
   } else {
@@ -551,6 +837,13 @@ cudaError_t launch_metrics(int dtype, int d, int64_t n, const void *X, const voi
                            double *part, int *nblocks, cudaStream_t s) {
   const int64_t chunk = 256;
   *nblocks = (int)nblk(n, (int)chunk);
+  if (d > kMaxNarrowD) {
+    if (dtype == 0)
+      metrics_rt<float><<<*nblocks, 256, 0, s>>>(n, d, (const float *)X, (const float *)Z, rows_local, tpr, chunk, part);
+    else
+      metrics_rt<double><<<*nblocks, 256, 0, s>>>(n, d, (const double *)X, (const double *)Z, rows_local, tpr, chunk, part);
+    return cudaGetLastError();
+  }
   const int threads = ((3 * d * d + 31) / 32) * 32;
   if (dtype == 0) {
     NSRGS_D_SWITCH(d, (metrics_kernel<float, D><<<*nblocks, threads, 0, s>>>(n, (const float *)X, (const float *)Z,
@@ -563,6 +856,10 @@ cudaError_t launch_metrics(int dtype, int d, int64_t n, const void *X, const voi
 }
 
 cudaError_t launch_metrics_final(int d, int64_t n, const double *grams, double *out3, cudaStream_t s) {
+  if (d > kMaxNarrowD) {
+    metrics_final_rt<<<1, 32, 0, s>>>(n, d, grams, out3);
+    return cudaGetLastError();
+  }
   NSRGS_D_SWITCH(d, (metrics_final_kernel<D><<<1, 32, 0, s>>>(n, grams, out3)));
   return cudaGetLastError();
 }

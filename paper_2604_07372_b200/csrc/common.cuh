@@ -62,8 +62,19 @@ constexpr int kErrTimeout = 8;      // multi-iteration grid barrier timed out (s
 // 128 x 2 values, component pairs (2kp, 2kp+1) interleaved, so a lane's two adjacent columns
 // of one component pair come in one 128-bit load and feed FFMA2 directly.  Element (row c,
 // component k) of the nd x d stack:
+// Wide blocks (d > kMaxNarrowD, §8(f) row 4: the paper's d = 25) use the "wide" kernel
+// (wide.cu): 32-column tiles and the X tile as a plain row-major 32 x d slab of the stack.
+constexpr int kMaxNarrowD = 10;
+constexpr int kWideColTile = 32;
+constexpr int kMaxD = 32;
+__host__ __device__ constexpr int col_tile(int d) { return d > kMaxNarrowD ? kWideColTile : kColTile; }
+
 __host__ __device__ inline int64_t tile_index(int64_t c, int k, int d, int64_t rows_local,
                                               int64_t tiles_per_rank) {
+  if (d > kMaxNarrowD) {   // wide: per-rank stack padded to whole 32-row tiles
+    const int64_t g = c / rows_local, cl = c - g * rows_local;
+    return ((g * tiles_per_rank * kWideColTile) + cl) * d + k;
+  }
   const int dp = (d + 1) & ~1;
   int64_t g = c / rows_local, cl = c - g * rows_local;
   int64_t j = cl / kColTile, o = cl - j * kColTile;

@@ -17,6 +17,11 @@ struct PanelShape {
 cudaError_t panel_dispatch(int dtype, int d, int mode, bool shape_only, PanelShape *shape,
                            const CUtensorMap *tm, const PanelParams *p, int grid, cudaStream_t s);
 
+// wide.cu: d > 10 (one node per warp, lane = component).
+bool wide_supported(int d);
+cudaError_t wide_dispatch(int d, int mode, bool shape_only, PanelShape *shape, const CUtensorMap *tm,
+                          const PanelParams *p, int grid, cudaStream_t s);
+
 // sym.cu: symmetric half-storage pass (fp32, world == 1, d in [2, 6]).
 struct SymShape {
   int rows, nodes, stages, smem, gt, npw, final_nodes_per_cta;

@@ -72,16 +72,17 @@ int plan_impl(int64_t n, int32_t d, int32_t world, int32_t rank, nsrgs_plan_t *o
   };
   if (!out) return fail("plan: out is NULL");
   if (n < 2) return fail("n must be >= 2");
-  if (d < 2 || d > 10) return fail("d must be in [2, 10] (d = 1: O(1) has a trivial tangent space, SPEC.md:295)");
+  if (d < 2 || d > kMaxD) return fail("d must be in [2, 32] (d = 1: O(1) has a trivial tangent space, SPEC.md:295)");
+  if (d > kMaxNarrowD && !wide_supported(d)) return fail("d in [11, 32]: supported wide sizes are 12, 16, 20, 24, 25, 32");
   if (world < 1 || rank < 0 || rank >= world) return fail("need world >= 1 and 0 <= rank < world");
   if (n % world) return fail("n must be divisible by world (row-block sharding by node)");
   out->n_local = n / world;
   out->node0 = (int64_t)rank * out->n_local;
   out->rows_local = out->n_local * d;
   out->row0 = out->node0 * d;
-  out->col_tile = kColTile;
-  out->tiles_per_rank = ceil_div(out->rows_local, kColTile);
-  out->x_slice_elems = out->tiles_per_rank * padded_d(d) * kColTile;
+  out->col_tile = col_tile(d);
+  out->tiles_per_rank = ceil_div(out->rows_local, out->col_tile);
+  out->x_slice_elems = out->tiles_per_rank * (d > kMaxNarrowD ? d : padded_d(d)) * out->col_tile;
   out->x_elems = (int64_t)world * out->x_slice_elems;
   return NSRGS_OK;
 }
@@ -140,7 +141,7 @@ struct nsrgs_ctx {
   int res_cap = 0;
   double *red_part = nullptr;   // generic reduction partials
   int64_t red_cap = 0;
-  double *small = nullptr;      // [0] a_fro2 | [1] chg2 | [8..8+2DD) MC | [256..) F trace / metrics
+  double *small = nullptr;      // [0] a_fro2 | [1] chg2 | [8..8+2DD) MC | [kSmallOut..) F trace / metrics
   int64_t small_cap = 0;
   int *err = nullptr;
   unsigned *ns_region = nullptr;
@@ -263,7 +264,7 @@ int ensure_small(nsrgs_ctx *c, int64_t count) {
   c->small_cap = count;
   return NSRGS_OK;
 }
-constexpr int kSmallFro = 0, kSmallChg = 1, kSmallMC = 8, kSmallOut = 256;
+constexpr int kSmallFro = 0, kSmallChg = 1, kSmallMC = 8, kSmallOut = 8 + 2 * kMaxD * kMaxD;   // MC holds 2 d^2
 
 int build_tmap(nsrgs_ctx *c) {
   static EncodeTiledFn encode = nullptr;
@@ -279,7 +280,7 @@ int build_tmap(nsrgs_ctx *c) {
   cuuint64_t dims[3] = {c->world == 1 ? (cuuint64_t)c->N : Nr, (cuuint64_t)c->world, (cuuint64_t)c->plan.rows_local};
   cuuint64_t strides[2] = {c->world == 1 ? (cuuint64_t)(c->lda * c->esz) : (cuuint64_t)(Nr * c->esz),
                            (cuuint64_t)(c->lda * c->esz)};
-  cuuint32_t box[3] = {(cuuint32_t)kColTile, 1u, (cuuint32_t)c->shape.rows};
+  cuuint32_t box[3] = {(cuuint32_t)col_tile(c->d), 1u, (cuuint32_t)c->shape.rows};
   cuuint32_t estr[3] = {1u, 1u, 1u};
   CUresult r = encode(&c->tmA, c->dtype == NSRGS_F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64,
                       3, c->A, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -342,6 +343,8 @@ int launch_panel(nsrgs_ctx *c, int mode, const void *Xin, void *Xout, double *re
     sp.N = c->N;
     CUDA_TRY(c, sym_dispatch(c->d, mode, false, nullptr, &c->tmA, &sp, c->sym_grid, c->stream));
     c->kernel_launches++;
+  } else if (c->d > kMaxNarrowD) {
+    CUDA_TRY(c, wide_dispatch(c->d, mode, false, nullptr, &c->tmA, &p, c->grid, c->stream));
   } else {
     CUDA_TRY(c, panel_dispatch(c->dtype, c->d, mode, false, nullptr, &c->tmA, &p, c->grid, c->stream));
   }
@@ -478,12 +481,17 @@ int nsrgs_create(const nsrgs_desc *desc, nsrgs_ctx **out) {
     c->own_stream = true;
   }
   cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, c->device);
-  panel_dispatch(c->dtype, c->d, 0, true, &c->shape, nullptr, nullptr, 0, nullptr);
+  if (c->d > kMaxNarrowD) {
+    if (c->dtype != NSRGS_F32) return bail(NSRGS_ERR_INVALID_ARG, "d > 10 supports F32 only");
+    wide_dispatch(c->d, 0, true, &c->shape, nullptr, nullptr, 0, nullptr);
+  } else {
+    panel_dispatch(c->dtype, c->d, 0, true, &c->shape, nullptr, nullptr, 0, nullptr);
+  }
   // launch shape: stream-K over panels x column tiles, one persistent CTA per SM
   c->panels = (int)ceil_div(c->plan.rows_local, c->shape.rows);
   c->total_tiles = (int)(c->world * c->plan.tiles_per_rank);
   c->steps = (int64_t)c->panels * c->total_tiles;
-  c->grid = (int)std::min<int64_t>(c->steps, c->sm_count);
+  c->grid = c->d > kMaxNarrowD ? c->panels : (int)std::min<int64_t>(c->steps, c->sm_count);   // wide: CTA per panel
   {
     int l2 = 0;
     cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, c->device);
@@ -514,7 +522,7 @@ int nsrgs_create(const nsrgs_desc *desc, nsrgs_ctx **out) {
     int coop = 0;
     cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, c->device);
     const char *env = getenv("NSRGS_NO_COOP");
-    c->coop = coop && c->world == 1 && !(env && env[0] == '1');
+    c->coop = coop && c->world == 1 && c->d <= kMaxNarrowD && !(env && env[0] == '1');
   }
   if (cudaStreamSynchronize(c->stream) != cudaSuccess) return bail(NSRGS_ERR_CUDA);
   *out = c;

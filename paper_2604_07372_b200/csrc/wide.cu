@@ -1,0 +1,217 @@
+// wide.cu — the A.X pass + fused epilogue for wide blocks, d in {12, 16, 20, 24, 25, 32}
+// (the paper's experiments use d = 25).
+//
+// With d > 10 the narrow kernel's register tile (RT rows x d accumulators per lane) no longer
+// fits, so the roles flip: a consumer warp owns ONE node (d rows of A) and lane k owns output
+// component k: acc[r] += A[r][c] X[c][k].  A row pieces are smem broadcasts (128-bit, 4
+// columns), X[c][k] is a per-lane scalar of a row-major 32 x d X slab, and the products run as
+// FFMA2 on column pairs (even / odd column partial sums).  4 consumer warps + 1 TMA producer
+// warp per CTA; one CTA per row panel (4 nodes); the same mbarrier ring, tensor map and
+// per-node epilogue (epilogue.cuh) as the narrow kernel.  Compute-bound (d/2 FMA per byte),
+// sized for the paper's scale (n = 500: a 625 MB A).
+#include <cuda.h>
+
+#include "common.cuh"
+#include "epilogue.cuh"
+#include "kernels.h"
+
+namespace nsrgs {
+
+template <int D>
+struct WideCfg {
+  static constexpr int W = 4;                          // consumer warps = nodes per panel
+  static constexpr int THREADS = 32 * (W + 1);
+  static constexpr int ROWS = W * D;
+  static constexpr int CW = kWideColTile;
+  static constexpr int A_BYTES = ROWS * CW * 4;
+  static constexpr int X_BYTES = CW * D * 4;
+  static constexpr int STAGE_BYTES = A_BYTES + X_BYTES;   // = 128 (ROWS + D): TMA-aligned
+  static constexpr int DD = D * D, E = DD, DDL = (DD + 31) / 32;
+  static constexpr int NPART = 2 * DD + 2;
+  static constexpr int SCR = W * 5 * E * 4;
+  static constexpr int RED = W * NPART * 8;
+  static constexpr int FIXED = 1024 + 128 + SCR + RED + 64;
+  static constexpr int BUDGET = 222 * 1024;
+  static constexpr int STAGES_RAW = (BUDGET - FIXED) / STAGE_BYTES;
+  static constexpr int STAGES = STAGES_RAW > 6 ? 6 : STAGES_RAW;
+  static_assert(STAGES >= 2, "ring");
+  static constexpr int SMEM = FIXED + STAGES * STAGE_BYTES;
+};
+
+__device__ __forceinline__ uint64_t wpack(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ uint64_t wffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+
+template <int D, int MODE>
+__global__ void __launch_bounds__(WideCfg<D>::THREADS, 1)
+    wide_kernel(const __grid_constant__ CUtensorMap tmA, const PanelParams p) {
+  using C = WideCfg<D>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = smem_raw + (((smem_u32(smem_raw) + 1023u) & ~1023u) - smem_u32(smem_raw));
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t *empty = full + 8;
+  float *scr = reinterpret_cast<float *>(smem + C::STAGES * C::STAGE_BYTES + 128);
+  double *red = reinterpret_cast<double *>(reinterpret_cast<uint8_t *>(scr) + C::SCR);
+  int *flag = reinterpret_cast<int *>(red + C::W * C::NPART);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], C::W);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const float *Xg = static_cast<const float *>(p.X);
+  const int panel = blockIdx.x;
+  const int tpr = (int)p.tiles_per_rank;
+
+  if (warp == C::W) {   // ------------------------------------------------ TMA producer
+    if (lane == 0) {
+      prefetch_tmap(&tmA);
+      const uint64_t pol_a = p.a_keep > 0.f ? policy_keep_fraction(p.a_keep) : policy_evict_first();
+      const uint64_t pol_x = policy_evict_last();
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = 0; t < p.total_tiles; ++t) {
+        const int g0 = t / tpr;
+        const int g = (g0 + p.rank) % p.world, jt = t - g0 * tpr;     // own rank slice first
+        const int tt = g * tpr + jt;
+        mbar_wait(&empty[stage], phase ^ 1u);
+        uint8_t *sb = smem + stage * C::STAGE_BYTES;
+        mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
+        tma_load_3d(sb, &tmA, &full[stage], jt * C::CW, g, panel * C::ROWS, pol_a);
+        bulk_load(sb + C::A_BYTES, Xg + (int64_t)tt * C::CW * D, C::X_BYTES, &full[stage], pol_x);
+        if (++stage == C::STAGES) { stage = 0; phase ^= 1u; }
+      }
+    }
+    return;
+  }
+
+  // ------------------------------------------------------------------ consumer warp = one node
+  const int kk = lane < D ? lane : D - 1;
+  uint64_t acc2[D];   // (even-column, odd-column) partial sums of row r, component `lane`
+#pragma unroll
+  for (int r = 0; r < D; ++r) acc2[r] = 0ull;
+  int stage = 0;
+  uint32_t phase = 0;
+  for (int t = 0; t < p.total_tiles; ++t) {
+    mbar_wait(&full[stage], phase);
+    const float *As = reinterpret_cast<const float *>(smem + stage * C::STAGE_BYTES) + warp * D * C::CW;
+    const float *Xs = reinterpret_cast<const float *>(smem + stage * C::STAGE_BYTES + C::A_BYTES) + kk;
+#pragma unroll
+    for (int c4 = 0; c4 < C::CW / 4; ++c4) {
+      const uint64_t xa = wpack(Xs[(4 * c4 + 0) * D], Xs[(4 * c4 + 1) * D]);
+      const uint64_t xb = wpack(Xs[(4 * c4 + 2) * D], Xs[(4 * c4 + 3) * D]);
+#pragma unroll
+      for (int r = 0; r < D; ++r) {
+        const ulonglong2 a = *reinterpret_cast<const ulonglong2 *>(As + r * C::CW + 4 * c4);   // broadcast
+        acc2[r] = wffma2(a.x, xa, acc2[r]);
+        acc2[r] = wffma2(a.y, xb, acc2[r]);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[stage]);
+    if (++stage == C::STAGES) { stage = 0; phase ^= 1u; }
+  }
+
+  float *sX = scr + warp * 5 * C::E, *sG = sX + C::E, *sH = sG + C::E, *sS = sH + C::E, *sM = sS + C::E;
+#pragma unroll
+  for (int r = 0; r < D; ++r) {
+    float lo, hi;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(acc2[r]));
+    if (lane < D) sG[r * D + lane] = lo + hi;   // entry (a = r, b = lane) of B_i
+  }
+  __syncwarp();
+  const int64_t node = (int64_t)panel * C::W + warp;
+  const int nvalid = node < p.n_local ? 1 : 0;
+  double g1s[C::DDL], g2s[C::DDL], so = 0.0, xs = 0.0;
+  float ns_region = 0.f;
+  int err = 0;
+  node_epilogue<float, D, 1, MODE>(p, Xg, lane, node, nvalid, sX, sG, sH, sS, sM, g1s, g2s, so, xs, ns_region, err);
+  if (err) atomicOr(p.err, err);
+  if (lane == 0 && ns_region > 0.f) atomicMax(p.ns_region, __float_as_uint(ns_region));
+
+  // per-CTA partials (fixed warp order) -> slot, last CTA reduces all slots in order
+  so = warp_sum(so);
+  xs = warp_sum(xs);
+  double *rw = red + warp * C::NPART;
+#pragma unroll
+  for (int m = 0; m < C::DDL; ++m) {
+    const int e2 = lane + 32 * m;
+    if (e2 < C::DD) { rw[e2] = g1s[m]; rw[C::DD + e2] = g2s[m]; }
+  }
+  if (lane == 0) { rw[2 * C::DD] = so; rw[2 * C::DD + 1] = xs; }
+  named_bar_sync(1, C::W * 32);
+  for (int i = threadIdx.x; i < C::NPART; i += C::W * 32) {
+    double v = 0.0;
+    for (int w = 0; w < C::W; ++w) v += red[w * C::NPART + i];
+    __stcg(p.cta_part + (int64_t)blockIdx.x * C::NPART + i, v);
+  }
+  __threadfence();
+  named_bar_sync(1, C::W * 32);
+  if (threadIdx.x == 0) *flag = (atomicAdd(p.done_cnt, 1u) == gridDim.x - 1);
+  named_bar_sync(1, C::W * 32);
+  if (*flag) {
+    __threadfence();
+    for (int i = warp; i < C::NPART; i += C::W) {
+      double v = 0.0;
+      for (int b = lane; b < (int)gridDim.x; b += 32) v += __ldcg(p.cta_part + (int64_t)b * C::NPART + i);
+      v = warp_sum(v);
+      if (lane == 0) p.result[i] = v;
+    }
+    if (threadIdx.x == 0) *p.done_cnt = 0u;
+  }
+}
+
+template <int D, int MODE>
+static cudaError_t wide_launch(const CUtensorMap *tm, const PanelParams &p, int grid, cudaStream_t s) {
+  using C = WideCfg<D>;
+  auto kern = wide_kernel<D, MODE>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  kern<<<grid, C::THREADS, C::SMEM, s>>>(*tm, p);
+  return cudaGetLastError();
+}
+
+bool wide_supported(int d) { return d == 12 || d == 16 || d == 20 || d == 24 || d == 25 || d == 32; }
+
+cudaError_t wide_dispatch(int d, int mode, bool shape_only, PanelShape *shape, const CUtensorMap *tm,
+                          const PanelParams *p, int grid, cudaStream_t s) {
+#define NSRGS_WIDE_CASE(DV)                                                                        \
+  case DV: {                                                                                       \
+    using C = WideCfg<DV>;                                                                         \
+    if (shape_only) {                                                                              \
+      *shape = PanelShape{C::ROWS, C::W, C::STAGES, C::SMEM, C::NPART, C::THREADS};                \
+      return cudaSuccess;                                                                          \
+    }                                                                                              \
+    if (mode == kModeRgs) return wide_launch<DV, kModeRgs>(tm, *p, grid, s);                       \
+    if (mode == kModeObjective) return wide_launch<DV, kModeObjective>(tm, *p, grid, s);           \
+    if (mode == kModeGpm) return wide_launch<DV, kModeGpm>(tm, *p, grid, s);                       \
+    return wide_launch<DV, kModeProduct>(tm, *p, grid, s);                                         \
+  }
+  switch (d) {
+    NSRGS_WIDE_CASE(12)
+    NSRGS_WIDE_CASE(16)
+    NSRGS_WIDE_CASE(20)
+    NSRGS_WIDE_CASE(24)
+    NSRGS_WIDE_CASE(25)
+    NSRGS_WIDE_CASE(32)
+    default: return cudaErrorInvalidValue;
+  }
+#undef NSRGS_WIDE_CASE
+}
+
+}  // namespace nsrgs

@@ -465,3 +465,54 @@ def test_masked_end_to_end_and_symmetric(nsrgs):
         assert abs(rel - mt.rel_err(Xo, Z)) <= 1e-3 * rel
         assert abs(rel - sigma * np.sqrt((d - 1) / (n * p))) <= 0.15 * rel
         s.close()
+
+
+# ---------------------------------------------------------------------------- wide blocks, d = 25 (§8f row 4)
+@pytest.mark.parametrize("n,d,sigma,K", [(60, 12, 0.5, 3), (37, 16, 0.3, 4), (50, 25, 0.1, 1), (23, 32, 0.2, 2)])
+def test_wide_generator_step_gpm(nsrgs, n, d, sigma, K):
+    s = nsrgs.Solver(n, d)
+    Zg = s.generate(4, sigma)
+    Z = inst.ground_truth(4, n, d)
+    assert np.max(np.abs(Zg.astype(np.float64) - Z)) <= 2e-7
+    A = inst.measurement_matrix(4, Z, sigma)
+    Ag = s.copy_A_rows(0, n * d).astype(np.float64)
+    assert np.all(np.abs(Ag - A) <= np.spacing(np.abs(A).astype(np.float32)).astype(np.float64))
+    X = oracle_iterate_near(Z, 0.1, 2).astype(np.float32)
+    s.set_X(X)
+    f = s.step(1.0 / n, K)
+    Xo, _, _ = ons.step(A, X.astype(np.float64), 1.0 / n, K)
+    assert rel_fro(s.get_X(), Xo) <= 1e-6
+    assert abs(f - ons.objective(A, X.astype(np.float64))) <= 2e-6 * f
+    s.set_X(X)
+    s.gpm_run(1)
+    assert rel_fro(s.get_X(), ons.gpm_step(A, X.astype(np.float64))) <= 1e-6
+    r = np.array(s.alignment_error(Z))
+    assert np.all(np.abs(r - np.array(mt.alignment_error(s.get_X().astype(np.float64), Z))) <= 1e-6 * np.abs(r) + 1e-12)
+    s.close()
+
+
+def _table1_rows():
+    import os
+    path = os.path.join(os.path.dirname(__file__), "golden", "table1_relerr.txt")
+    return [tuple(float(t) for t in l.split()) for l in open(path) if l.strip() and not l.startswith("#")]
+
+
+def test_table1_on_b200(nsrgs):
+    """PAPER.md Table 1 (all nine cells, :345-359) with the paper's protocol on the GPU:
+    spectral init, T_s = 1, mu = 1/(np), stop at R^t < 1e-8 / MaxIter 100, NS-RGS and GPM."""
+    n, d = 500, 25
+    Z = inst.ground_truth(0, n, d)
+    for (n_, d_, p, sigma, rel_paper) in _table1_rows():
+        s = nsrgs.Solver(n, d)
+        Zg = s.generate(0, sigma, p=p)
+        s.init_spectral(0, 200, 1e-6, allow_unconverged=True)
+        X0 = s.get_X()
+        rels = {}
+        for alg in ("ns_rgs", "gpm"):
+            s.set_X(X0)
+            it, tr = s.solve(alg, max_iter=100, eta=1.0 / (n * p), K=1, stop_tol=1e-8)
+            assert it <= 100 and np.all(np.isfinite(tr))
+            rels[alg] = s.alignment_error(Zg)[0]
+            assert abs(rels[alg] - rel_paper) <= 0.05 * rel_paper, (alg, p, sigma, rels[alg], rel_paper)
+        assert abs(rels["ns_rgs"] - rels["gpm"]) <= 1e-4
+        s.close()
