@@ -289,72 +289,6 @@ __global__ void scale_kernel(int64_t row0, int64_t rows, const double *MC, T *W,
 }
 
 // ----------------------------------------------------------------------------------------
-// a2: X^0_i = sgn(Y_i) by Newton-Schulz with Frobenius pre-scaling S_0 = Y_i/||Y_i||_F (all
-// singular values in (0, 1], inside the (0, sqrt 3) convergence region); iterate until
-// ||I - S^T S||_F <= tol, max 80 steps; non-convergence flags NSRGS_ERR_SINGULAR.
-template <typename T, int D>
-__global__ void polar_kernel(int64_t n, const T *Y, T *X, int64_t rows_local, int64_t tpr, int *err) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  T S[D][D], M[D][D];
-  T f2 = T(0);
-#pragma unroll
-  for (int a = 0; a < D; ++a)
-#pragma unroll
-    for (int b = 0; b < D; ++b) {
-      S[a][b] = Y[tile_index(i * D + a, b, D, rows_local, tpr)];
-      f2 += S[a][b] * S[a][b];
-    }
-  const T tol = sizeof(T) == 4 ? T(2e-5) : T(1e-13);
-  bool conv = false;
-  if (f2 > T(0) && isfinite((double)f2)) {
-    const T sc = T(1) / sqrt(f2);
-#pragma unroll
-    for (int a = 0; a < D; ++a)
-#pragma unroll
-      for (int b = 0; b < D; ++b) S[a][b] *= sc;
-    int extra = 2;   // polish steps after reaching tol
-    for (int it = 0; it < 80; ++it) {
-      T dev = T(0);
-#pragma unroll
-      for (int a = 0; a < D; ++a)
-#pragma unroll
-        for (int b = 0; b < D; ++b) {
-          T v = T(0);
-#pragma unroll
-          for (int k = 0; k < D; ++k) v += S[k][a] * S[k][b];
-          M[a][b] = v;
-          const T dv = (a == b ? T(1) : T(0)) - v;
-          dev += dv * dv;
-        }
-      if (sqrt(dev) <= tol) {
-        conv = true;
-        if (extra-- == 0) break;
-      }
-      T Sn[D][D];
-#pragma unroll
-      for (int a = 0; a < D; ++a)
-#pragma unroll
-        for (int b = 0; b < D; ++b) {
-          T v = T(0);
-#pragma unroll
-          for (int k = 0; k < D; ++k) v += S[a][k] * M[k][b];
-          Sn[a][b] = T(1.5) * S[a][b] - T(0.5) * v;
-        }
-#pragma unroll
-      for (int a = 0; a < D; ++a)
-#pragma unroll
-        for (int b = 0; b < D; ++b) S[a][b] = Sn[a][b];
-    }
-  }
-  if (!conv) atomicOr(err, kErrSingular);
-#pragma unroll
-  for (int a = 0; a < D; ++a)
-#pragma unroll
-    for (int b = 0; b < D; ++b) X[tile_index(i * D + a, b, D, rows_local, tpr)] = S[a][b];
-}
-
-// ----------------------------------------------------------------------------------------
 // a8: F(X^t) = 1/2(||X^T X||^2 - sum_i ||X_i^T X_i||^2) - <X, AX> + 1/2 ||A||^2 for every
 // slot t of res[T][npart] = [X^T X (DD) | unused (DD) | s_own | xb].
 __global__ void objective_final_kernel(int d, int T, const double *res, int npart, const double *a_fro2,
@@ -585,51 +519,6 @@ __global__ void scale_rt(int d, int64_t row0, int64_t rows, const double *MC, T 
 }
 
 template <typename T>
-__global__ void polar_rt(int64_t n, int d, const T *Y, T *X, int64_t rows_local, int64_t tpr, int *err) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  T S[kMaxD * kMaxD], M[kMaxD * kMaxD], Sn[kMaxD * kMaxD];
-  T f2 = T(0);
-  for (int a = 0; a < d; ++a)
-    for (int b = 0; b < d; ++b) {
-      S[a * d + b] = Y[tile_index(i * d + a, b, d, rows_local, tpr)];
-      f2 += S[a * d + b] * S[a * d + b];
-    }
-  const T tol = sizeof(T) == 4 ? T(2e-5) * (T)d / T(3) : T(1e-13);
-  bool conv = false;
-  if (f2 > T(0) && isfinite((double)f2)) {
-    const T sc = T(1) / sqrt(f2);
-    for (int e = 0; e < d * d; ++e) S[e] *= sc;
-    int extra = 2;
-    for (int it = 0; it < 100; ++it) {
-      T dev = T(0);
-      for (int a = 0; a < d; ++a)
-        for (int b = 0; b < d; ++b) {
-          T v = T(0);
-          for (int k = 0; k < d; ++k) v += S[k * d + a] * S[k * d + b];
-          M[a * d + b] = v;
-          const T dv = (a == b ? T(1) : T(0)) - v;
-          dev += dv * dv;
-        }
-      if (sqrt(dev) <= tol) {
-        conv = true;
-        if (extra-- == 0) break;
-      }
-      for (int a = 0; a < d; ++a)
-        for (int b = 0; b < d; ++b) {
-          T v = T(0);
-          for (int k = 0; k < d; ++k) v += S[a * d + k] * M[k * d + b];
-          Sn[a * d + b] = T(1.5) * S[a * d + b] - T(0.5) * v;
-        }
-      for (int e = 0; e < d * d; ++e) S[e] = Sn[e];
-    }
-  }
-  if (!conv) atomicOr(err, kErrSingular);
-  for (int a = 0; a < d; ++a)
-    for (int b = 0; b < d; ++b) X[tile_index(i * d + a, b, d, rows_local, tpr)] = S[a * d + b];
-}
-
-template <typename T>
 __global__ void metrics_rt(int64_t n, int d, const T *X, const T *Z, int64_t rows_local, int64_t tpr, int64_t chunk,
                            double *part) {
   const int64_t i0 = (int64_t)blockIdx.x * chunk, i1 = min(n, i0 + chunk);
@@ -808,21 +697,6 @@ cudaError_t launch_scale(int dtype, int d, int64_t node0, int64_t n_local, const
   } else {
     NSRGS_D_SWITCH(d, (scale_kernel<double, D><<<nblk(rows, 256), 256, 0, s>>>(row0, rows, MC, (double *)W,
                                                                               (const double *)Yold, rows_local, tpr, part)));
-  }
-  return cudaGetLastError();
-}
-
-cudaError_t launch_polar(int dtype, int d, int64_t n, const void *Y, void *X, int64_t rows_local, int64_t tpr, int *err,
-                         cudaStream_t s) {
-  if (d > kMaxNarrowD) {
-    if (dtype == 0) polar_rt<float><<<nblk(n, 32), 32, 0, s>>>(n, d, (const float *)Y, (float *)X, rows_local, tpr, err);
-    else polar_rt<double><<<nblk(n, 32), 32, 0, s>>>(n, d, (const double *)Y, (double *)X, rows_local, tpr, err);
-    return cudaGetLastError();
-  }
-  if (dtype == 0) {
-    NSRGS_D_SWITCH(d, (polar_kernel<float, D><<<nblk(n, 64), 64, 0, s>>>(n, (const float *)Y, (float *)X, rows_local, tpr, err)));
-  } else {
-    NSRGS_D_SWITCH(d, (polar_kernel<double, D><<<nblk(n, 64), 64, 0, s>>>(n, (const double *)Y, (double *)X, rows_local, tpr, err)));
   }
   return cudaGetLastError();
 }

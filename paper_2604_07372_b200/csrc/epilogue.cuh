@@ -128,10 +128,10 @@ __device__ __forceinline__ void node_epilogue(const PanelParams &p, const T *Xg,
         if (e < E) sS[e] = sG[e] * inv[e / DD];
       }
       __syncwarp();
-      const T tol = sizeof(T) == 4 ? T(2e-5) : T(1e-13);
+      const T tol = sizeof(T) == 4 ? T(2e-5) * (D > 3 ? T(D) / T(3) : T(1)) : T(1e-13) * T(D);   // fp32 floor grows ~ d
       int polish = 2;
       bool conv = false;
-      for (int it = 0; it < 60; ++it) {
+      for (int it = 0; it < 100; ++it) {
 #pragma unroll
         for (int m = 0; m < EPL; ++m) {
           const int e = lane + 32 * m;

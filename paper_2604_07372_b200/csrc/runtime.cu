@@ -638,8 +638,9 @@ int nsrgs_init_spectral(nsrgs_ctx *c, uint64_t seed, int max_sweeps, double tol,
   c->kernel_launches++;
   const int64_t nbs = ceil_div(c->plan.rows_local, 256);
   NSRGS_TRY(ensure_red(c, nbs));
-  int sweeps = 0;
+  int sweeps = 0, stalled = 0;
   bool converged = false;
+  double best_chg = 1e300;
   for (sweeps = 1; sweeps <= max_sweeps; ++sweeps) {
     void *Y = c->X[c->cur], *W = c->X[1 - c->cur];
     NSRGS_TRY(launch_panel(c, kModeProduct, Y, W, c->res, 0.0, 0));
@@ -659,7 +660,15 @@ int nsrgs_init_spectral(nsrgs_ctx *c, uint64_t seed, int max_sweeps, double tol,
     NSRGS_TRY(sync_and_check(c, &flags));
     if (flags & kErrSingular) return set_err(c, NSRGS_ERR_SINGULAR, "Cholesky of Y^T Y failed at sweep %d", sweeps);
     if (!std::isfinite(chg2)) return set_err(c, NSRGS_ERR_NONFINITE, "non-finite subspace change at sweep %d", sweeps);
-    if (sweeps >= 2 && std::sqrt(chg2) < tol) { converged = true; break; }
+    const double chg = std::sqrt(chg2);
+    if (sweeps >= 2 && chg < tol) { converged = true; break; }
+    // fp32 noise floor (reading R14): the change stopped shrinking while already tiny
+    if (sweeps >= 4 && chg < 1e-3 && chg > 0.7 * best_chg) {
+      if (++stalled >= 3) { converged = true; break; }
+    } else {
+      stalled = 0;
+    }
+    if (sweeps >= 2) best_chg = std::min(best_chg, chg);
   }
   if (sweeps > max_sweeps) sweeps = max_sweeps;
   CUDA_TRY(c, launch_polar(c->dtype, c->d, c->n, c->X[c->cur], c->X[1 - c->cur], c->plan.rows_local,

@@ -1,0 +1,33 @@
+"""PAPER.md Table 1 (§4.1, :336-363) on one B200: n = 500, d = 25, p in {1, 0.8, 0.5},
+sigma in {0.02, 0.1, 0.2}, spectral init, T_s = 1, mu = 1/(np), stop at R^t < 1e-8 (MaxIter 100),
+NS-RGS and GPM from the same init.  Prints one JSON line per cell (device time per solve)."""
+import json, os, sys
+import numpy as np
+import torch
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2604_07372_b200 import nsrgs
+
+ROWS = [(1.0, 0.02, 4.38e-3, 0.154, 0.282), (1.0, 0.1, 2.19e-2, 0.158, 0.287), (1.0, 0.2, 4.38e-2, 0.161, 0.289),
+        (0.8, 0.02, 4.90e-3, 0.158, 0.292), (0.8, 0.1, 2.45e-2, 0.163, 0.302), (0.8, 0.2, 4.91e-2, 0.234, 0.423),
+        (0.5, 0.02, 6.21e-3, 0.241, 0.420), (0.5, 0.1, 3.11e-2, 0.244, 0.422), (0.5, 0.2, 6.21e-2, 0.240, 0.434)]
+n, d = 500, 25
+st = torch.cuda.current_stream()
+for p, sigma, rel_paper, t_rgs_paper, t_gpm_paper in ROWS:
+    out = {"p": p, "sigma": sigma, "rel_err_paper": rel_paper}
+    s = nsrgs.Solver(n, d)
+    Z = s.generate(0, sigma, p=p)
+    for alg, tp in (("ns_rgs", t_rgs_paper), ("gpm", t_gpm_paper)):
+        best = None
+        for rep in range(3):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            s.init_spectral(0, 200, 1e-6, allow_unconverged=True)
+            it, tr = s.solve(alg, max_iter=100, eta=1.0 / (n * p), K=1, stop_tol=1e-8)
+            e1.record(st)
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1)
+            best = ms if best is None else min(best, ms)
+        out[alg] = {"rel_err": s.alignment_error(Z)[0], "iters": it, "solve_ms_b200": round(best, 3),
+                    "solve_s_paper_cpu": tp}
+    print(json.dumps(out), flush=True)
+    s.close()
