@@ -68,7 +68,9 @@ typedef struct {
                                    alignment of the per-rank column slices)                      */
   int32_t device;               /* CUDA device ordinal the context binds to                      */
   const void *nccl_unique_id;   /* host, 128 bytes from nsrgs_get_nccl_unique_id() on rank 0,
-                                   broadcast by the caller; must be NULL iff world == 1          */
+                                   broadcast by the caller; must be NULL iff world == 1 (test-only
+                                   exception: env NSRGS_EMULATE_RANKS=1 allows world > 1 with NULL;
+                                   collectives become no-ops, for rank-by-rank kernel tests)     */
   void *cuda_stream;            /* cudaStream_t to enqueue on; NULL = library-created stream    */
 } nsrgs_desc;
 

@@ -147,6 +147,7 @@ struct nsrgs_ctx {
   unsigned *ns_region = nullptr;
   // NCCL
   ncclComm_t comm = nullptr;
+  bool emulated = false;   // test-only: world > 1 without a communicator (collectives are no-ops)
   // stats / timing
   bool timing = false;
   std::vector<cudaEvent_t> ev;
@@ -218,13 +219,13 @@ int sync_and_check(nsrgs_ctx *c, int *flags_out = nullptr) {
 }
 
 int allreduce_sum(nsrgs_ctx *c, double *buf, size_t count) {
-  if (c->world == 1 || count == 0) return NSRGS_OK;
+  if (c->world == 1 || count == 0 || c->emulated) return NSRGS_OK;
   NCCL_TRY(c, g_nccl.AllReduce(buf, buf, count, ncclFloat64, ncclSum, c->comm, c->stream));
   return NSRGS_OK;
 }
 
 int allgather_X(nsrgs_ctx *c, void *buf) {
-  if (c->world == 1) return NSRGS_OK;
+  if (c->world == 1 || c->emulated) return NSRGS_OK;
   const size_t cnt = (size_t)c->plan.x_slice_elems;
   char *base = static_cast<char *>(buf);
   NCCL_TRY(c, g_nccl.AllGather(base + (size_t)c->rank * cnt * c->esz, base, cnt, nccl_type(c), c->comm, c->stream));
@@ -461,7 +462,12 @@ int nsrgs_create(const nsrgs_desc *desc, nsrgs_ctx **out) {
   int s = plan_impl(desc->n, desc->d, desc->world, desc->rank, &c->plan, &why);
   if (s) return bail(s);
   if (desc->dtype == NSRGS_F64 && desc->d > 6) return bail(NSRGS_ERR_INVALID_ARG, "F64 supports d in [2, 6]");
-  if ((desc->world > 1) != (desc->nccl_unique_id != nullptr))
+  // Test-only rank emulation (NSRGS_EMULATE_RANKS=1): a context for (rank, world > 1) without a
+  // communicator, so the sharded kernels can be exercised rank by rank on one GPU (no rank ever
+  // waits for another); the caller assembles X across ranks.
+  const char *emu = getenv("NSRGS_EMULATE_RANKS");
+  c->emulated = desc->world > 1 && desc->nccl_unique_id == nullptr && emu && emu[0] == '1';
+  if ((desc->world > 1) != (desc->nccl_unique_id != nullptr) && !c->emulated)
     return bail(NSRGS_ERR_INVALID_ARG, "nccl_unique_id must be given iff world > 1");
   c->n = desc->n;
   c->d = desc->d;
@@ -512,7 +518,7 @@ int nsrgs_create(const nsrgs_desc *desc, nsrgs_ctx **out) {
   if (ok) ok = alloc(&c->Bpart, c->esz * (size_t)c->grid * 2 * c->shape.rows * c->d);
   if (!ok) return bail(NSRGS_ERR_OOM, "device allocation failed");
   if (ensure_res(c, 128) || ensure_small(c, kSmallOut + 256)) return bail(NSRGS_ERR_OOM);
-  if (c->world > 1) {
+  if (c->world > 1 && !c->emulated) {
     if (!load_nccl()) return bail(NSRGS_ERR_NCCL, "libnccl.so.2 not loadable");
     ncclUniqueId id;
     std::memcpy(&id, desc->nccl_unique_id, sizeof id);

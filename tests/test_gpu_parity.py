@@ -516,3 +516,48 @@ def test_table1_on_b200(nsrgs):
             assert abs(rels[alg] - rel_paper) <= 0.05 * rel_paper, (alg, p, sigma, rels[alg], rel_paper)
         assert abs(rels["ns_rgs"] - rels["gpm"]) <= 1e-4
         s.close()
+
+
+# ---------------------------------------------------------------------------- sharded kernels, ranks emulated
+@pytest.mark.parametrize("n,d,world", [(64, 2, 2), (160, 5, 4), (8000, 4, 8), (96, 12, 2), (40, 3, 2)])
+def test_sharded_step_rank_by_rank(nsrgs, monkeypatch, n, d, world):
+    """Each rank's context (row shard generated from the per-(i,j) counters, 3-D tensor map over
+    rank slices, own-slice-first tile order, epilogue into its slice of the tile layout) is run
+    alone on the one GPU (NSRGS_EMULATE_RANKS: no collectives, no rank waits on another); the
+    assembled X^{t+1} must match the single-GPU step and the oracle."""
+    monkeypatch.setenv("NSRGS_EMULATE_RANKS", "1")
+    sigma, K = 0.7, 3
+    Z = inst.ground_truth(6, n, d)
+    X = oracle_iterate_near(Z, 0.1, 5).astype(np.float32)
+    full = nsrgs.Solver(n, d)
+    full.generate(6, sigma, want_Z=False)
+    full.set_X(X)
+    full.step(1.0 / n, K)
+    Xref = full.get_X()
+    full.close()
+    Xsh = np.empty_like(X)
+    nl = n // world
+    for r in range(world):
+        s = nsrgs.Solver(n, d, rank=r, world=world)
+        s.generate(6, sigma, want_Z=False)
+        if r == 0 or n <= 200:        # shard rows are rows of the global instance
+            rows = s.copy_A_rows(0, min(nl * d, 3 * d)).astype(np.float64)
+            R = inst.measurement_rows(6, Z, sigma, np.arange(r * nl, r * nl + min(nl, 3)))
+            assert np.all(np.abs(rows - R) <= np.spacing(np.abs(R).astype(np.float32)))
+        s.set_X(X)
+        s.step(1.0 / n, K)
+        Xsh[r * nl:(r + 1) * nl] = s.get_X()[r * nl:(r + 1) * nl]
+        s.close()
+    assert rel_fro(Xsh, Xref) <= 1e-6
+    if n <= 200:
+        A = inst.measurement_matrix(6, Z, sigma)
+        Xo, _, _ = ons.step(A, X.astype(np.float64), 1.0 / n, K)
+        assert rel_fro(Xsh, Xo) <= 1e-6
+
+
+def test_sharded_alignment_rule(nsrgs, monkeypatch):
+    # (n/world)*d*4 bytes must be a multiple of 16 (TMA row segments of each rank slice)
+    monkeypatch.setenv("NSRGS_EMULATE_RANKS", "1")
+    with pytest.raises(nsrgs.NSRGSError) as e:
+        nsrgs.Solver(120, 5, rank=0, world=4)
+    assert e.value.name == "INVALID_ARG"
