@@ -82,17 +82,19 @@ typedef struct {
   int64_t row0;         /* first owned A row = node0 * d                                      */
   int64_t col_tile;     /* X/A column tile width (elements) of the device layout = 128        */
   int64_t tiles_per_rank; /* ceil(rows_local / col_tile)                                       */
-  int64_t x_elems;      /* elements of one device X buffer = world*tiles_per_rank*dp*col_tile */
+  int64_t x_elems;      /* elements of one device X buffer = world*tiles_per_rank*d*col_tile  */
   int64_t x_slice_elems;/* elements of one rank's contiguous X slice (NCCL all-gather count)  */
 } nsrgs_plan_t;
 
 int nsrgs_version(void);
 
 /* Pure host: the sharding plan of (n, d, world, rank).  Returns INVALID_ARG if the
- * combination is not supported.  Device X layout ("tile layout"): with
- * dp = d rounded up to even, element (row c of the nd x d stack, component k) lives at
- *   ((g * tiles_per_rank + j) * dp + (k & ~1)) * col_tile + 2 * o + (k & 1),
- *   g = c / rows_local, j = (c % rows_local) / col_tile, o = (c % rows_local) % col_tile;
+ * combination is not supported.  Device X layout ("tile layout"), with
+ * g = c / rows_local the owning rank, cl = c % rows_local, T = col_tile:
+ *   d <= 10: tile base b = (g*tiles_per_rank + cl/T) * d * T, o = cl % T; element (row c,
+ *            component k) at b + (k & ~1)*T + 2*o + (k & 1), except for odd d and k = d-1:
+ *            b + (d-1)*T + o;
+ *   d > 10 : (g*tiles_per_rank*T + cl) * d + k   (row-major stack, rank slice padded to T rows);
  * padding entries are zero.  */
 int nsrgs_plan(int64_t n, int32_t d, int32_t world, int32_t rank, nsrgs_plan_t *out);
 

@@ -58,10 +58,10 @@ constexpr int kErrNonfinite = 4;
 constexpr int kErrTimeout = 8;      // multi-iteration grid barrier timed out (should never happen)
 
 // Tile layout of X: the N stack rows of one rank's slice are cut into column
-// tiles of 128; tile (g, j) holds dp = d rounded up to even components as dp/2 pair-blocks of
-// 128 x 2 values, component pairs (2kp, 2kp+1) interleaved, so a lane's two adjacent columns
-// of one component pair come in one 128-bit load and feed FFMA2 directly.  Element (row c,
-// component k) of the nd x d stack:
+// tiles of 128; tile (g, j) holds d x 128 values: component pairs (2kp, 2kp+1) as pair-blocks
+// of 128 x 2 (interleaved, so a lane's two adjacent columns of one pair come in one 128-bit
+// load and feed FFMA2 with a broadcast A operand), and for odd d the last component as a plain
+// 128-vector (its column pairs feed FFMA2 against A column pairs).  No padding component.
 // Wide blocks (d > kMaxNarrowD, §8(f) row 4: the paper's d = 25) use the "wide" kernel
 // (wide.cu): 32-column tiles and the X tile as a plain row-major 32 x d slab of the stack.
 constexpr int kMaxNarrowD = 10;
@@ -75,12 +75,12 @@ __host__ __device__ inline int64_t tile_index(int64_t c, int k, int d, int64_t r
     const int64_t g = c / rows_local, cl = c - g * rows_local;
     return ((g * tiles_per_rank * kWideColTile) + cl) * d + k;
   }
-  const int dp = (d + 1) & ~1;
   int64_t g = c / rows_local, cl = c - g * rows_local;
   int64_t j = cl / kColTile, o = cl - j * kColTile;
-  return ((g * tiles_per_rank + j) * dp + (k & ~1)) * kColTile + 2 * o + (k & 1);
+  const int64_t base = (g * tiles_per_rank + j) * d * kColTile;
+  if ((d & 1) && k == d - 1) return base + (int64_t)(d - 1) * kColTile + o;   // odd d: last component contiguous
+  return base + (int64_t)(k & ~1) * kColTile + 2 * o + (k & 1);
 }
-__host__ __device__ constexpr int padded_d(int d) { return (d + 1) & ~1; }
 
 // ------------------------------------------------------------------------------------------
 // Philox4x32-10 (Salmon et al., SC'11).  Same definition as oracle/instance.py, written

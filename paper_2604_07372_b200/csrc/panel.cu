@@ -35,9 +35,9 @@ struct PanelCfg {
   static constexpr int ROWS = RT * kWarps;
   static constexpr int NODES = ROWS / D;
   static constexpr int A_BYTES = ROWS * kColTile * (int)sizeof(T);
-  static constexpr int DP = padded_d(D);           // components incl. the zero pad (even)
-  static constexpr int KP = DP / 2;                // component pairs
-  static constexpr int X_BYTES = DP * kColTile * (int)sizeof(T);
+  static constexpr int KP = D / 2;                 // component pairs (2kp, 2kp+1)
+  static constexpr bool ODD = (D & 1) != 0;        // last component handled with column pairs
+  static constexpr int X_BYTES = D * kColTile * (int)sizeof(T);
   static constexpr int STAGE_BYTES = A_BYTES + X_BYTES;
   static constexpr int E = NPW * D * D;          // epilogue entries per warp
   static constexpr int EPL = (E + 31) / 32;      // entries per lane
@@ -142,7 +142,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             fence_proxy_async_global();
             ready = true;
           }
-          bulk_load(sb + C::A_BYTES, Xin + (int64_t)tt * C::DP * kColTile, C::X_BYTES, &full[stage], pol_x);
+          bulk_load(sb + C::A_BYTES, Xin + (int64_t)tt * D * kColTile, C::X_BYTES, &full[stage], pol_x);
           if (++stage == C::STAGES) { stage = 0; phase ^= 1u; }
         }
       }
@@ -238,29 +238,39 @@ __global__ void __launch_bounds__(kThreads, 1)
     // conflict-free 64-bit smem loads, X component pairs conflict-free 128-bit loads.
     T acc[C::RT][D];
     if constexpr (sizeof(T) == 4) {
-      // fp32: packed FFMA2 on component pairs (acc[r][2kp], acc[r][2kp+1]) += (x_2kp, x_2kp+1) * a
-      uint64_t acc2[C::RT][C::KP];
+      // fp32: packed FFMA2 on component pairs (acc[r][2kp], acc[r][2kp+1]) += (x_2kp, x_2kp+1) * a,
+      // and for odd d the last component on column pairs (even, odd column sums) += (a_c, a_c+1) * (x_c, x_c+1)
+      constexpr int KL = C::ODD ? 1 : 0;
+      uint64_t acc2[C::RT][C::KP + KL];
 #pragma unroll
       for (int r = 0; r < C::RT; ++r)
 #pragma unroll
-        for (int kp = 0; kp < C::KP; ++kp) acc2[r][kp] = 0ull;
+        for (int kp = 0; kp < C::KP + KL; ++kp) acc2[r][kp] = 0ull;
       for (int t = t0; t < t1; ++t) {
         mbar_wait(&full[stage], phase);
         const float *As = reinterpret_cast<const float *>(smem + stage * C::STAGE_BYTES) + (warp * C::RT) * kColTile + 2 * lane;
-        const float *Xs = reinterpret_cast<const float *>(smem + stage * C::STAGE_BYTES + C::A_BYTES) + 4 * lane;
-        uint64_t xp[C::KP][4];   // pairs for the lane's 4 columns
+        const float *Xt = reinterpret_cast<const float *>(smem + stage * C::STAGE_BYTES + C::A_BYTES);
+        const float *Xs = Xt + 4 * lane;
+        uint64_t xp[C::KP + KL][4];   // pairs for the lane's 4 columns (+ last-component column pairs)
 #pragma unroll
         for (int kp = 0; kp < C::KP; ++kp) {
           const ulonglong2 lo = *reinterpret_cast<const ulonglong2 *>(Xs + kp * 2 * kColTile);
           const ulonglong2 hi = *reinterpret_cast<const ulonglong2 *>(Xs + kp * 2 * kColTile + kColTile);
           xp[kp][0] = lo.x; xp[kp][1] = lo.y; xp[kp][2] = hi.x; xp[kp][3] = hi.y;
         }
+        if constexpr (C::ODD) {
+          xp[C::KP][0] = *reinterpret_cast<const uint64_t *>(Xt + (D - 1) * kColTile + 2 * lane);
+          xp[C::KP][1] = *reinterpret_cast<const uint64_t *>(Xt + (D - 1) * kColTile + 64 + 2 * lane);
+        }
 #pragma unroll
         for (int r = 0; r < C::RT; ++r) {
-          const float2 a0 = *reinterpret_cast<const float2 *>(As + r * kColTile);
-          const float2 a1 = *reinterpret_cast<const float2 *>(As + r * kColTile + 64);
-          const uint64_t b0 = pack2(a0.x, a0.x), b1 = pack2(a0.y, a0.y);
-          const uint64_t b2 = pack2(a1.x, a1.x), b3 = pack2(a1.y, a1.y);
+          const uint64_t a0 = *reinterpret_cast<const uint64_t *>(As + r * kColTile);        // (A[r][2l], A[r][2l+1])
+          const uint64_t a1 = *reinterpret_cast<const uint64_t *>(As + r * kColTile + 64);   // (.., 64+2l, 65+2l)
+          float f0, f1, f2, f3;
+          unpack2(a0, f0, f1);
+          unpack2(a1, f2, f3);
+          const uint64_t b0 = pack2(f0, f0), b1 = pack2(f1, f1);
+          const uint64_t b2 = pack2(f2, f2), b3 = pack2(f3, f3);
 #pragma unroll
           for (int kp = 0; kp < C::KP; ++kp) {
             uint64_t v = acc2[r][kp];
@@ -270,20 +280,32 @@ __global__ void __launch_bounds__(kThreads, 1)
             v = ffma2(xp[kp][3], b3, v);
             acc2[r][kp] = v;
           }
+          if constexpr (C::ODD) {
+            uint64_t v = acc2[r][C::KP];
+            v = ffma2(a0, xp[C::KP][0], v);
+            v = ffma2(a1, xp[C::KP][1], v);
+            acc2[r][C::KP] = v;
+          }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[stage]);
         if (++stage == C::STAGES) { stage = 0; phase ^= 1u; }
       }
 #pragma unroll
-      for (int r = 0; r < C::RT; ++r)
+      for (int r = 0; r < C::RT; ++r) {
 #pragma unroll
         for (int kp = 0; kp < C::KP; ++kp) {
           float lo, hi;
           unpack2(acc2[r][kp], lo, hi);
           acc[r][2 * kp] = (T)lo;
-          if (2 * kp + 1 < D) acc[r][2 * kp + 1] = (T)hi;
+          acc[r][2 * kp + 1] = (T)hi;
         }
+        if constexpr (C::ODD) {
+          float lo, hi;
+          unpack2(acc2[r][C::KP], lo, hi);
+          acc[r][D - 1] = (T)(lo + hi);
+        }
+      }
     } else {
 #pragma unroll
       for (int r = 0; r < C::RT; ++r)
@@ -293,13 +315,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&full[stage], phase);
         const T *As = reinterpret_cast<const T *>(smem + stage * C::STAGE_BYTES) + (warp * C::RT) * kColTile + 2 * lane;
         const T *Xs = reinterpret_cast<const T *>(smem + stage * C::STAGE_BYTES + C::A_BYTES) + 4 * lane;
-        T xv[C::DP][4];
+        T xv[D][4];
 #pragma unroll
         for (int kp = 0; kp < C::KP; ++kp) {
           const V lo = *reinterpret_cast<const V *>(Xs + kp * 2 * kColTile);
           const V hi = *reinterpret_cast<const V *>(Xs + kp * 2 * kColTile + kColTile);
           xv[2 * kp][0] = lo.x; xv[2 * kp + 1][0] = lo.y; xv[2 * kp][1] = lo.z; xv[2 * kp + 1][1] = lo.w;
           xv[2 * kp][2] = hi.x; xv[2 * kp + 1][2] = hi.y; xv[2 * kp][3] = hi.z; xv[2 * kp + 1][3] = hi.w;
+        }
+        if constexpr (C::ODD) {
+          const T *Xl = reinterpret_cast<const T *>(smem + stage * C::STAGE_BYTES + C::A_BYTES) + (D - 1) * kColTile;
+          xv[D - 1][0] = Xl[2 * lane]; xv[D - 1][1] = Xl[2 * lane + 1];
+          xv[D - 1][2] = Xl[64 + 2 * lane]; xv[D - 1][3] = Xl[65 + 2 * lane];
         }
 #pragma unroll
         for (int r = 0; r < C::RT; ++r) {

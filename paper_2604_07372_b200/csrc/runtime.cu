@@ -82,7 +82,7 @@ int plan_impl(int64_t n, int32_t d, int32_t world, int32_t rank, nsrgs_plan_t *o
   out->row0 = out->node0 * d;
   out->col_tile = col_tile(d);
   out->tiles_per_rank = ceil_div(out->rows_local, out->col_tile);
-  out->x_slice_elems = out->tiles_per_rank * (d > kMaxNarrowD ? d : padded_d(d)) * out->col_tile;
+  out->x_slice_elems = out->tiles_per_rank * d * out->col_tile;
   out->x_elems = (int64_t)world * out->x_slice_elems;
   return NSRGS_OK;
 }

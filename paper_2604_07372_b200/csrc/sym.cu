@@ -36,12 +36,13 @@ struct SymCfg {
   static constexpr int NPW = RT / D;
   static constexpr int ROWS = RT * kWarps;
   static constexpr int NODES = ROWS / D;
-  static constexpr int DP = padded_d(D), KP = DP / 2;
+  static constexpr int KP = D / 2;                    // component pairs (2kp, 2kp+1)
+  static constexpr bool ODD = (D & 1) != 0;          // last component on column pairs
   static constexpr int GT = kSymTilesPerBlock;          // column tiles per block (512 columns)
   static constexpr int A_BYTES = ROWS * kColTile * 4;
-  static constexpr int X_BYTES = DP * kColTile * 4;
+  static constexpr int X_BYTES = D * kColTile * 4;
   static constexpr int STAGE_BYTES = A_BYTES + X_BYTES;
-  static constexpr int SLICE_FLOATS = GT * KP * kColTile * 2;     // [g][kp][col][2] per warp
+  static constexpr int SLICE_FLOATS = GT * D * kColTile;          // per warp: GT tiles in the X tile layout
   static constexpr int SLICE_BYTES = kWarps * SLICE_FLOATS * 4;
   static constexpr int META_BYTES = 8 * 32;
   static constexpr int BUDGET = 222 * 1024;
@@ -138,7 +139,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint8_t *sb = smem + stage * C::STAGE_BYTES;
             mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
             tma_load_3d(sb, &tmA, &full[stage], t * kColTile, 0, pp * C::ROWS, pol_a);
-            bulk_load(sb + C::A_BYTES, Xg + (int64_t)t * C::DP * kColTile, C::X_BYTES, &full[stage], pol_x);
+            bulk_load(sb + C::A_BYTES, Xg + (int64_t)t * D * kColTile, C::X_BYTES, &full[stage], pol_x);
             if (++stage == C::STAGES) { stage = 0; phase ^= 1u; }
           }
         }
@@ -148,18 +149,29 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 
   // ------------------------------------------------------------------ consumer warps
+  // Slice = GT column tiles in the X tile layout (pairs interleaved, odd d's last component
+  // contiguous); this warp only touches its own slice until the end-of-block reduction.
   float *myslice = slices + warp * C::SLICE_FLOATS;
   auto zero_slice = [&]() {
 #pragma unroll
-    for (int g = 0; g < C::GT * C::KP; ++g) {
-      *reinterpret_cast<float4 *>(myslice + (g * kColTile + 2 * lane) * 2) = make_float4(0.f, 0.f, 0.f, 0.f);
-      *reinterpret_cast<float4 *>(myslice + (g * kColTile + 64 + 2 * lane) * 2) = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int g = 0; g < C::GT; ++g) {
+#pragma unroll
+      for (int kp = 0; kp < C::KP; ++kp) {
+        float *b = myslice + (g * D + 2 * kp) * kColTile;
+        *reinterpret_cast<float4 *>(b + 4 * lane) = make_float4(0.f, 0.f, 0.f, 0.f);
+        *reinterpret_cast<float4 *>(b + kColTile + 4 * lane) = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      if constexpr (C::ODD) *reinterpret_cast<float4 *>(myslice + (g * D + D - 1) * kColTile + 4 * lane) =
+          make_float4(0.f, 0.f, 0.f, 0.f);
     }
+    __syncwarp();   // the last component's entries are zeroed by other lanes than their owners
   };
   zero_slice();
 
-  uint64_t acc2[C::RT][C::KP];   // row direction: rows of this warp x component pairs
-  uint64_t xr[C::RT][C::KP];     // X of this warp's rows (column-direction operand)
+  constexpr int KL = C::ODD ? 1 : 0;
+  uint64_t acc2[C::RT][C::KP + KL];   // row direction: pairs (+ last component's column pair)
+  uint64_t xr[C::RT][C::KP];          // X of this warp's rows, component pairs (column direction)
+  float xl[C::RT];                    // ... and the last component for odd d
   int stage = 0;
   uint32_t phase = 0;
   for (;;) {
@@ -170,28 +182,35 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int64_t wrow0 = row_lo + warp * C::RT;          // this warp's first row
     if (m.flags & kFirstP) {
 #pragma unroll
-      for (int r = 0; r < C::RT; ++r)
+      for (int r = 0; r < C::RT; ++r) {
+        const int64_t row = wrow0 + r;
+        const float *xb = Xg + (row >> 7) * D * kColTile;   // world == 1: tile of row
+        const int o = (int)(row & 127);
 #pragma unroll
-        for (int kp = 0; kp < C::KP; ++kp) {
-          acc2[r][kp] = 0ull;
-          const int64_t row = wrow0 + r;
-          // world == 1: tile_index(row, 2kp) = ((row / 128) * DP + 2kp) * 128 + 2 (row % 128)
-          xr[r][kp] = row < N ? __ldg(reinterpret_cast<const unsigned long long *>(
-                                    Xg + (((row >> 7) * C::DP + 2 * kp) << 7) + 2 * (row & 127)))
-                              : 0ull;
-        }
+        for (int kp = 0; kp < C::KP + KL; ++kp) acc2[r][kp] = 0ull;
+#pragma unroll
+        for (int kp = 0; kp < C::KP; ++kp)
+          xr[r][kp] = row < N ? __ldg(reinterpret_cast<const unsigned long long *>(xb + 2 * kp * kColTile + 2 * o)) : 0ull;
+        if constexpr (C::ODD) xl[r] = row < N ? __ldg(xb + (D - 1) * kColTile + o) : 0.f;
+      }
     }
     const int64_t col0 = (int64_t)m.t * kColTile;
     const float *As = reinterpret_cast<const float *>(smem + stage * C::STAGE_BYTES) + (warp * C::RT) * kColTile + 2 * lane;
-    const float *Xs = reinterpret_cast<const float *>(smem + stage * C::STAGE_BYTES + C::A_BYTES) + 4 * lane;
-    uint64_t xp[C::KP][4];
+    const float *Xt = reinterpret_cast<const float *>(smem + stage * C::STAGE_BYTES + C::A_BYTES);
+    const float *Xs = Xt + 4 * lane;
+    uint64_t xp[C::KP + KL][4];
 #pragma unroll
     for (int kp = 0; kp < C::KP; ++kp) {
       const ulonglong2 lo = *reinterpret_cast<const ulonglong2 *>(Xs + kp * 2 * kColTile);
       const ulonglong2 hi = *reinterpret_cast<const ulonglong2 *>(Xs + kp * 2 * kColTile + kColTile);
       xp[kp][0] = lo.x; xp[kp][1] = lo.y; xp[kp][2] = hi.x; xp[kp][3] = hi.y;
     }
+    if constexpr (C::ODD) {
+      xp[C::KP][0] = *reinterpret_cast<const uint64_t *>(Xt + (D - 1) * kColTile + 2 * lane);
+      xp[C::KP][1] = *reinterpret_cast<const uint64_t *>(Xt + (D - 1) * kColTile + 64 + 2 * lane);
+    }
     uint64_t colc[4][C::KP];
+    uint64_t colL[2] = {0ull, 0ull};   // odd d: last component, column pairs (2l, 2l+1), (64+2l, 65+2l)
 #pragma unroll
     for (int j = 0; j < 4; ++j)
 #pragma unroll
@@ -228,6 +247,17 @@ __global__ void __launch_bounds__(kThreads, 1)
             colc[j][kp] = ffma2s(xr[r][kp], bcast2(ac[j]), colc[j][kp]);
           }
         }
+        if constexpr (C::ODD) {
+          uint64_t ra0, ra1, ca0, ca1;
+          asm("mov.b64 %0, {%1, %2};" : "=l"(ra0) : "f"(ar[0]), "f"(ar[1]));
+          asm("mov.b64 %0, {%1, %2};" : "=l"(ra1) : "f"(ar[2]), "f"(ar[3]));
+          asm("mov.b64 %0, {%1, %2};" : "=l"(ca0) : "f"(ac[0]), "f"(ac[1]));
+          asm("mov.b64 %0, {%1, %2};" : "=l"(ca1) : "f"(ac[2]), "f"(ac[3]));
+          acc2[r][C::KP] = ffma2s(ra0, xp[C::KP][0], acc2[r][C::KP]);
+          acc2[r][C::KP] = ffma2s(ra1, xp[C::KP][1], acc2[r][C::KP]);
+          colL[0] = ffma2s(ca0, bcast2(xl[r]), colL[0]);
+          colL[1] = ffma2s(ca1, bcast2(xl[r]), colL[1]);
+        }
       }
     };
     if (col0 >= row_lo + C::ROWS) tile_pass(std::integral_constant<bool, false>{});
@@ -239,10 +269,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     // column direction -> this warp's slice (thread-exclusive entries, no atomics)
     {
       const int g = m.t - m.J * C::GT;
-      const uint32_t sbase = smem_u32(myslice) + (uint32_t)(((g * C::KP) * kColTile + 2 * lane) * 2 * 4);
+      const uint32_t tb = smem_u32(myslice) + (uint32_t)(g * D * kColTile * 4);
 #pragma unroll
       for (int kp = 0; kp < C::KP; ++kp) {
-        const uint32_t a0 = sbase + kp * kColTile * 2 * 4, a1 = a0 + 64 * 2 * 4;
+        const uint32_t a0 = tb + (uint32_t)((2 * kp * kColTile + 4 * lane) * 4), a1 = a0 + kColTile * 4;
         uint64_t v0, v1, v2, v3;
         asm volatile("ld.shared.v2.b64 {%0, %1}, [%2];" : "=l"(v0), "=l"(v1) : "r"(a0) : "memory");
         asm volatile("ld.shared.v2.b64 {%0, %1}, [%2];" : "=l"(v2), "=l"(v3) : "r"(a1) : "memory");
@@ -253,18 +283,34 @@ __global__ void __launch_bounds__(kThreads, 1)
         asm volatile("st.shared.v2.b64 [%0], {%1, %2};" ::"r"(a0), "l"(v0), "l"(v1) : "memory");
         asm volatile("st.shared.v2.b64 [%0], {%1, %2};" ::"r"(a1), "l"(v2), "l"(v3) : "memory");
       }
+      if constexpr (C::ODD) {
+        const uint32_t l0 = tb + (uint32_t)(((D - 1) * kColTile + 2 * lane) * 4), l1 = l0 + 64 * 4;
+        uint64_t v0, v1;
+        asm volatile("ld.shared.b64 %0, [%1];" : "=l"(v0) : "r"(l0) : "memory");
+        asm volatile("ld.shared.b64 %0, [%1];" : "=l"(v1) : "r"(l1) : "memory");
+        v0 = add2s(v0, colL[0]);
+        v1 = add2s(v1, colL[1]);
+        asm volatile("st.shared.b64 [%0], %1;" ::"r"(l0), "l"(v0) : "memory");
+        asm volatile("st.shared.b64 [%0], %1;" ::"r"(l1), "l"(v1) : "memory");
+      }
     }
 
     if (m.flags & kLastP) {   // row partials of (panel, J) -> rowpart[J][row][k]
-      // reduce-scatter butterfly over the warp: value i = r*DP + k; after 5 rounds lane l holds
-      // the full sums of values [l*VP/32, (l+1)*VP/32) (VP = RT*DP padded to a power of two).
-      constexpr int V = C::RT * C::DP;
+      // reduce-scatter butterfly over the warp: value i = r*D + k; after 5 rounds lane l holds
+      // the full sums of values [l*VP/32, (l+1)*VP/32) (VP = RT*D padded to a power of two).
+      constexpr int V = C::RT * D;
       constexpr int VP = V <= 32 ? 32 : V <= 64 ? 64 : V <= 128 ? 128 : 256;
       float v[VP];
 #pragma unroll
-      for (int r = 0; r < C::RT; ++r)
+      for (int r = 0; r < C::RT; ++r) {
 #pragma unroll
-        for (int kp = 0; kp < C::KP; ++kp) split2(acc2[r][kp], v[r * C::DP + 2 * kp], v[r * C::DP + 2 * kp + 1]);
+        for (int kp = 0; kp < C::KP; ++kp) split2(acc2[r][kp], v[r * D + 2 * kp], v[r * D + 2 * kp + 1]);
+        if constexpr (C::ODD) {
+          float lo, hi;
+          split2(acc2[r][C::KP], lo, hi);
+          v[r * D + D - 1] = lo + hi;
+        }
+      }
 #pragma unroll
       for (int i = V; i < VP; ++i) v[i] = 0.f;
 #pragma unroll
@@ -283,9 +329,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
       for (int j = 0; j < VP / 32; ++j) {
         const int i = lane * (VP / 32) + j;
-        const int r = i / C::DP, k = i % C::DP;
+        const int r = i / D, k = i % D;
         const int64_t row = wrow0 + r;
-        if (i < V && k < D && row < N) rp[row * D + k] = v[j];
+        if (i < V && row < N) rp[row * D + k] = v[j];
       }
     }
     if (m.flags & kLastBlock) {   // sum the 7 slices (fixed warp order) -> colpart[I][col][k]
@@ -293,12 +339,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       float *cp = sp.colpart + ((int64_t)m.I * N) * D;
       const int64_t cbase = (int64_t)m.J * C::GT * kColTile;
       for (int idx = threadIdx.x; idx < C::SLICE_FLOATS; idx += kWarps * 32) {
-        // idx = ((g*KP + kp)*128 + col)*2 + h
-        const int h = idx & 1, col = (idx >> 1) % kColTile, gk = (idx >> 1) / kColTile;
-        const int kp = gk % C::KP, gg = gk / C::KP;
-        const int k = 2 * kp + h;
+        const int gg = idx / (D * kColTile), rem = idx - gg * D * kColTile;
+        int k, col;
+        if (C::ODD && rem >= (D - 1) * kColTile) {
+          k = D - 1;
+          col = rem - (D - 1) * kColTile;
+        } else {
+          const int kp = rem / (2 * kColTile), w2 = rem - kp * 2 * kColTile;
+          col = w2 >> 1;
+          k = 2 * kp + (w2 & 1);
+        }
         const int64_t c = cbase + (int64_t)gg * kColTile + col;
-        if (k < D && c < N) {
+        if (c < N) {
           float v = 0.f;
           for (int w = 0; w < kWarps; ++w) v += slices[w * C::SLICE_FLOATS + idx];
           cp[c * D + k] = v;

@@ -40,38 +40,43 @@ def test_exports_every_declared_symbol(nsrgs):
     assert nsrgs.version() == 1
 
 
-def _tile_index(c, k, d, rows_local, tpr, CT=128):
+def _tile_index(c, k, d, rows_local, tpr):
     # the layout formula as written in include/nsrgs.h (nsrgs_plan comment)
-    dp = d + (d % 2)
     g, cl = divmod(c, rows_local)
-    j, o = divmod(cl, CT)
-    return ((g * tpr + j) * dp + (k - k % 2)) * CT + 2 * o + k % 2
+    if d > 10:
+        return (g * tpr * 32 + cl) * d + k
+    j, o = divmod(cl, 128)
+    b = (g * tpr + j) * d * 128
+    if d % 2 == 1 and k == d - 1:
+        return b + (d - 1) * 128 + o
+    return b + (k - k % 2) * 128 + 2 * o + k % 2
 
 
 @pytest.mark.parametrize("n,d,world", [(2, 2, 1), (100, 3, 1), (100, 3, 4), (43, 5, 1), (20000, 5, 8),
-                                       (12000, 10, 8), (40000, 5, 4), (7, 9, 7)])
+                                       (12000, 10, 8), (40000, 5, 4), (7, 9, 7), (500, 25, 4)])
 def test_plan_partitions_rows(nsrgs, n, d, world):
     rows = []
     for r in range(world):
         p = nsrgs.plan(n, d, world, r)
         assert p["n_local"] * world == n and p["node0"] == r * p["n_local"]
         assert p["rows_local"] == p["n_local"] * d and p["row0"] == p["node0"] * d
-        assert p["tiles_per_rank"] == -(-p["rows_local"] // 128)
+        ct = 32 if d > 10 else 128
+        assert p["col_tile"] == ct and p["tiles_per_rank"] == -(-p["rows_local"] // ct)
         assert p["x_slice_elems"] * world == p["x_elems"]
-        assert p["x_slice_elems"] == p["tiles_per_rank"] * (d + d % 2) * 128
+        assert p["x_slice_elems"] == p["tiles_per_rank"] * d * ct
         rows.append((p["row0"], p["row0"] + p["rows_local"]))
     assert rows[0][0] == 0 and rows[-1][1] == n * d
     assert all(a[1] == b[0] for a, b in zip(rows, rows[1:]))
 
 
-@pytest.mark.parametrize("kw", [dict(n=1, d=3), dict(n=10, d=1), dict(n=10, d=11), dict(n=10, d=3, world=3),
+@pytest.mark.parametrize("kw", [dict(n=1, d=3), dict(n=10, d=1), dict(n=10, d=11), dict(n=10, d=33), dict(n=10, d=3, world=3),
                                 dict(n=10, d=3, world=2, rank=2)])
 def test_plan_rejects(nsrgs, kw):
     with pytest.raises(nsrgs.NSRGSError):
         nsrgs.plan(kw["n"], kw["d"], kw.get("world", 1), kw.get("rank", 0))
 
 
-@pytest.mark.parametrize("n,d,world", [(10, 3, 2), (43, 5, 1), (300, 7, 3), (64, 2, 4)])
+@pytest.mark.parametrize("n,d,world", [(10, 3, 2), (43, 5, 1), (300, 7, 3), (64, 2, 4), (40, 25, 2), (30, 12, 1)])
 @pytest.mark.parametrize("dt", [np.float32, np.float64])
 def test_pack_layout(nsrgs, n, d, world, dt):
     N = n * d
