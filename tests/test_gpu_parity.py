@@ -561,3 +561,48 @@ def test_sharded_alignment_rule(nsrgs, monkeypatch):
     with pytest.raises(nsrgs.NSRGSError) as e:
         nsrgs.Solver(120, 5, rank=0, world=4)
     assert e.value.name == "INVALID_ARG"
+
+
+# ---------------------------------------------------------------------------- API surface
+def test_device_pointers_and_padded_attach(nsrgs):
+    """set_X / get_X / alignment_error with device tensors; attach_A with lda > n d (padded rows)."""
+    import torch
+
+    n, d, sigma = 50, 3, 0.6
+    Z = inst.ground_truth(9, n, d)
+    A = inst.measurement_matrix(9, Z, sigma).astype(np.float32)
+    N = n * d
+    lda = N + 14                                     # 16-byte aligned padded row stride
+    Ap = torch.zeros((N, lda), dtype=torch.float32)
+    Ap[:, :N] = torch.from_numpy(A)
+    Ad = Ap.cuda()
+    s = nsrgs.Solver(n, d)
+    s.attach_A(Ad, lda)
+    X = oracle_iterate_near(Z, 0.1, 4).astype(np.float32)
+    Xd = torch.from_numpy(X).cuda()
+    s.set_X(Xd)
+    s.run(3, 1.0 / n, 3, trace=False)
+    out = torch.empty((n, d, d), dtype=torch.float32, device="cuda")
+    s.get_X(out)
+    Xo = ons.run(A.astype(np.float64), X.astype(np.float64), 3, 1.0 / n, 3)
+    assert rel_fro(out.cpu().numpy(), Xo) <= 1e-6
+    r_dev = np.array(s.alignment_error(torch.from_numpy(Z.astype(np.float32)).cuda()))
+    r_host = np.array(s.alignment_error(Z.astype(np.float32)))
+    assert np.array_equal(r_dev, r_host)
+    with pytest.raises(nsrgs.NSRGSError):
+        s.attach_A(Ad, N - 1)                        # lda < n d
+    s.close()
+
+
+def test_stats_and_launch_accounting(nsrgs):
+    n, d = 300, 5
+    s = nsrgs.Solver(n, d)
+    s.generate(1, 1.0, want_Z=False)
+    s.init_spectral(1, 50, 1e-5, allow_unconverged=True)
+    s.reset_stats(timing=True)
+    s.run(7, 1.0 / n, 5)
+    st = s.stats()
+    assert st["panel_launches"] == 7 and st["panel_ms_total"] > 0
+    assert st["kernel_launches"] >= 1 and st["a_bytes_per_pass"] == 4 * (n * d) ** 2
+    assert 0 < st["ns_region_max"] < 1.0
+    s.close()
