@@ -232,10 +232,11 @@ FULL = {  # BASELINE.json configs[2], configs[3] in the launch configuration ben
     "c3": (20000, 5, 0.3 * np.sqrt(20000) / 5, 5),
     "c4": (12000, 10, 0.2 * np.sqrt(12000) / 10, 6),
     "mid": (6000, 3, 1.0, 5),       # panels >= #SMs: no split-K
+    "c5": (40000, 5, 0.3 * np.sqrt(40000) / 5, 5),   # 160 GB A: fits one 183 GB B200
 }
 
 
-@pytest.mark.parametrize("cfg", ["mid", "c3", "c4"])
+@pytest.mark.parametrize("cfg", ["mid", "c3", "c4", "c5"])
 def test_full_size_sampled_step(nsrgs, cfg):
     n, d, sigma, K = FULL[cfg]
     s = nsrgs.Solver(n, d)
@@ -385,7 +386,7 @@ def test_symmetric_modes_and_rejects(nsrgs):
         t.set_symmetric(True)
 
 
-@pytest.mark.parametrize("cfg", ["mid", "c3"])
+@pytest.mark.parametrize("cfg", ["mid", "c3", "c5"])
 def test_symmetric_full_size_sampled_and_run(nsrgs, cfg):
     n, d, sigma, K = FULL[cfg]
     s = nsrgs.Solver(n, d)

@@ -7,9 +7,9 @@ from paper_2604_07372_b200 import nsrgs
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "c3"
 sym = "--sym" in sys.argv
-n, d, c = {"c2": (2000, 3, None), "c3": (20000, 5, 0.3), "c4": (12000, 10, 0.2), "c5h": (20000, 5, 0.3)}[cfg]
+n, d, c = {"c2": (2000, 3, None), "c3": (20000, 5, 0.3), "c4": (12000, 10, 0.2), "c5": (40000, 5, 0.3)}[cfg]
 sigma = 0.5 if c is None else c * np.sqrt(n) / d
-K = {"c2": 5, "c3": 5, "c4": 6, "c5h": 5}[cfg]
+K = {"c2": 5, "c3": 5, "c4": 6, "c5": 5}[cfg]
 s = nsrgs.Solver(n, d)
 t = time.time(); Z = s.generate(0, sigma); torch.cuda.synchronize(); print("generate s", time.time() - t, flush=True)
 if sym:
