@@ -258,6 +258,20 @@ def run_gpu(args, cfg):
         barrier()
         return e0.elapsed_time(e1) / iters
 
+    # phase split of one solve (device time): spectral init | T iterations | metrics
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    barrier()
+    ev[0].record(stream)
+    s.init_spectral(0, INIT_MAX_SWEEPS, INIT_TOL, allow_unconverged=True)
+    ev[1].record(stream)
+    s.run(T, eta, K, trace=True)
+    ev[2].record(stream)
+    s.alignment_error(Zd)
+    ev[3].record(stream)
+    barrier()
+    phases = {"init_ms": ev[0].elapsed_time(ev[1]), "iterations_ms": ev[1].elapsed_time(ev[2]),
+              "metrics_ms": ev[2].elapsed_time(ev[3])}
+    phases["iterations_per_sec_run_only"] = T / (phases["iterations_ms"] / 1e3)
     s.init_spectral(0, INIT_MAX_SWEEPS, INIT_TOL, allow_unconverged=True)
     rgs_ms = per_iter_ms(lambda k: s.run(k, eta, K, trace=False))
     gpm_ms = per_iter_ms(lambda k: s.gpm_run(k, trace=False))
@@ -314,7 +328,7 @@ def run_gpu(args, cfg):
                      "traffic": traffic, "peak_kind": peak_kind, "kernel": "panel_kernel (fused A.X + epilogue)",
                      "bytes_per_launch": bytes_launch, "avg_launch_ms": avg_ms,
                      "frac_of_nominal_8TBs": achieved / 8000.0},
-        "effective_gbs": eff_gbs, "a_passes_per_step": passes,
+        "effective_gbs": eff_gbs, "a_passes_per_step": passes, "phases": phases,
         "e2e": {"value": e2e_value, "unit": "it/s", "h2d_bytes_per_step": 4 * n * d * d,
                 "d2h_bytes_per_step": 4 * n * d * d + 8 * T + 24},
         "gpu_launches": st["kernel_launches"],
