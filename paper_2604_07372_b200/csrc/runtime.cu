@@ -148,6 +148,7 @@ struct nsrgs_ctx {
   // NCCL
   ncclComm_t comm = nullptr;
   bool emulated = false;   // test-only: world > 1 without a communicator (collectives are no-ops)
+  bool forced_nccl = false; // test-only: world == 1 with a 1-rank NCCL communicator
   // stats / timing
   bool timing = false;
   std::vector<cudaEvent_t> ev;
@@ -219,13 +220,13 @@ int sync_and_check(nsrgs_ctx *c, int *flags_out = nullptr) {
 }
 
 int allreduce_sum(nsrgs_ctx *c, double *buf, size_t count) {
-  if (c->world == 1 || count == 0 || c->emulated) return NSRGS_OK;
+  if ((c->world == 1 && !c->forced_nccl) || count == 0 || c->emulated) return NSRGS_OK;
   NCCL_TRY(c, g_nccl.AllReduce(buf, buf, count, ncclFloat64, ncclSum, c->comm, c->stream));
   return NSRGS_OK;
 }
 
 int allgather_X(nsrgs_ctx *c, void *buf) {
-  if (c->world == 1 || c->emulated) return NSRGS_OK;
+  if ((c->world == 1 && !c->forced_nccl) || c->emulated) return NSRGS_OK;
   const size_t cnt = (size_t)c->plan.x_slice_elems;
   char *base = static_cast<char *>(buf);
   NCCL_TRY(c, g_nccl.AllGather(base + (size_t)c->rank * cnt * c->esz, base, cnt, nccl_type(c), c->comm, c->stream));
@@ -518,17 +519,25 @@ int nsrgs_create(const nsrgs_desc *desc, nsrgs_ctx **out) {
   if (ok) ok = alloc(&c->Bpart, c->esz * (size_t)c->grid * 2 * c->shape.rows * c->d);
   if (!ok) return bail(NSRGS_ERR_OOM, "device allocation failed");
   if (ensure_res(c, 128) || ensure_small(c, kSmallOut + 256)) return bail(NSRGS_ERR_OOM);
-  if (c->world > 1 && !c->emulated) {
+  // Test-only (NSRGS_FORCE_NCCL=1, world == 1): run every collective through a real 1-rank
+  // NCCL communicator so the NCCL plumbing is exercised on a single GPU.
+  const char *force = getenv("NSRGS_FORCE_NCCL");
+  c->forced_nccl = c->world == 1 && force && force[0] == '1';
+  if ((c->world > 1 && !c->emulated) || c->forced_nccl) {
     if (!load_nccl()) return bail(NSRGS_ERR_NCCL, "libnccl.so.2 not loadable");
     ncclUniqueId id;
-    std::memcpy(&id, desc->nccl_unique_id, sizeof id);
+    if (c->forced_nccl) {
+      if (g_nccl.GetUniqueId(&id) != ncclSuccess) return bail(NSRGS_ERR_NCCL, "ncclGetUniqueId failed");
+    } else {
+      std::memcpy(&id, desc->nccl_unique_id, sizeof id);
+    }
     if (g_nccl.CommInitRank(&c->comm, c->world, id, c->rank) != ncclSuccess) return bail(NSRGS_ERR_NCCL, "ncclCommInitRank failed");
   }
   {
     int coop = 0;
     cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, c->device);
     const char *env = getenv("NSRGS_NO_COOP");
-    c->coop = coop && c->world == 1 && c->d <= kMaxNarrowD && !(env && env[0] == '1');
+    c->coop = coop && c->world == 1 && !c->forced_nccl && c->d <= kMaxNarrowD && !(env && env[0] == '1');
   }
   if (cudaStreamSynchronize(c->stream) != cudaSuccess) return bail(NSRGS_ERR_CUDA);
   *out = c;
