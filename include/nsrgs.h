@@ -209,6 +209,14 @@ typedef struct {
 int nsrgs_get_stats(nsrgs_ctx *ctx, nsrgs_stats_t *out);
 int nsrgs_reset_stats(nsrgs_ctx *ctx, int enable_panel_timing);
 
+/* Debug: per-CTA phase timestamps (%globaltimer, ns) of the dense panel kernel.  max_iters > 0
+ * arms a [max_iters][grid][16] buffer for the following launches (slots: 0 producer start,
+ * 1 X ready after the iteration barrier, 2 first stage consumed, 3 work + epilogues done,
+ * 4 iteration reduction done, 5 last segment streamed, 6 its B rows complete, 7..10 cut-panel
+ * hand-off sub-steps; unused slots 0); max_iters == 0 copies it to out_host (host, may be NULL) and
+ * disarms. */
+int nsrgs_debug_timestamps(nsrgs_ctx *ctx, int max_iters, unsigned long long *out_host);
+
 #ifdef __cplusplus
 }
 #endif

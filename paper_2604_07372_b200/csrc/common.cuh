@@ -8,6 +8,7 @@
 namespace nsrgs {
 
 constexpr int kColTile = 128;      // X/A column tile (elements); one float4/double4 per lane
+constexpr int kTsSlots = 16;   // debug timestamp slots per CTA per iteration
 constexpr int kWarps = 7;          // consumer warps per panel CTA (7 + producer = 8 warps: 2 per SMSP, 255 regs)
 constexpr int kThreads = 32 * (kWarps + 1);   // + 1 TMA producer warp
 
@@ -37,6 +38,12 @@ struct PanelParams {
   // Xout (t odd), writes the other; result slot t = result + t * npart; iter_cnt = grid barrier
   int iters;
   unsigned *iter_cnt;
+  // deferred objective partials (iters > 1): iteration t's 2G partial slots go to
+  // part_iters + t * 2G * npart (zeroed once; the same slots are written every launch), and the
+  // slot reduction for all t runs once after the last iteration, off the per-iteration
+  // critical path.  nullptr: per-iteration last-CTA reduction through cta_part.
+  double *part_iters;
+  unsigned long long *ts;   // optional phase timestamps [iters][grid][8] (%globaltimer ns), debug
 };
 
 // Symmetric half-storage pass (sym.cu): blocks of GP panels x kSymTilesPerBlock column tiles.
@@ -181,6 +188,15 @@ __device__ __forceinline__ void bulk_load(void *smem_dst, const void *gsrc, uint
 __device__ __forceinline__ void prefetch_tmap(const void *tmap) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tmap)) : "memory");
 }
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+// Release/acquire ordering for the last-arriver patterns (data stores -> fence -> relaxed
+// atomic; atomic observed -> fence -> data loads).  fence.acq_rel is sufficient under the PTX
+// memory model and far cheaper than __threadfence()'s fence.sc (MEMBAR.SC.GPU).
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 __device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned *p) {
   unsigned v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");

@@ -46,7 +46,9 @@ struct PanelCfg {
   static constexpr int NPART = 2 * DD + 2;
   // shared memory after the stages
   static constexpr int BAR_BYTES = 2 * 8 * 8;                         // up to 8 stages
-  static constexpr int SCR_T = 5 * E;                                 // sX sG sH sS sM
+  static constexpr int VW = 16 / (int)sizeof(T);                      // elements per 16 B
+  static constexpr int EP = (E + VW - 1) / VW * VW;                  // E padded to 16 B
+  static constexpr int SCR_T = 5 * EP;                                // sX sG sH sS sM
   static constexpr int SCR_T_BYTES = (kWarps * SCR_T * (int)sizeof(T) + 15) / 16 * 16;   // keep doubles aligned
   static constexpr int SCR_BYTES = SCR_T_BYTES + kWarps * 2 * DD * 8 + kWarps * 2 * 8 + kWarps * NPART * 8 + 64;
   static constexpr int BUDGET = 220 * 1024;
@@ -56,6 +58,52 @@ struct PanelCfg {
   static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + BAR_BYTES + SCR_BYTES;
 };
 
+
+// After warp_sum every lane holds all RT x D sums of the warp; lane 0 writes them (zero-padded
+// to 16 B) with vector stores to a 16-byte aligned destination.  (Picking value r*D+k in lane
+// (r*D+k)%32 compiles to a divergent switch over the lane id: ~2 us per panel hand-off.)
+template <typename T, int RT, int D, bool GLOBAL>
+__device__ __forceinline__ void lane0_store_rows(T *dst, const T (&acc)[RT][D], int lane) {
+  if (lane != 0) return;
+  constexpr int N = RT * D, VW = 16 / (int)sizeof(T);
+#pragma unroll
+  for (int e = 0; e < N; e += VW) {
+    T v[VW];
+#pragma unroll
+    for (int j = 0; j < VW; ++j) v[j] = (e + j < N) ? acc[(e + j) / D][(e + j) % D] : T(0);
+    if constexpr (sizeof(T) == 4) {
+      const float4 f = make_float4(v[0], v[1], v[2], v[3]);
+      if constexpr (GLOBAL) __stcg(reinterpret_cast<float4 *>(dst + e), f);
+      else *reinterpret_cast<float4 *>(dst + e) = f;
+    } else {
+      const double2 f = make_double2(v[0], v[1]);
+      if constexpr (GLOBAL) __stcg(reinterpret_cast<double2 *>(dst + e), f);
+      else *reinterpret_cast<double2 *>(dst + e) = f;
+    }
+  }
+}
+
+// Sum nslots partial slots [nslots][NPART] into out[NPART] (consumer warps).  Warp w takes
+// entries w, w + kWarps, ...; lane j sums slots j, j + 32, ... in order (loads issued 8 at a
+// time: independent L2 round trips), then a fixed butterfly — deterministic.
+template <int NPART>
+__device__ __forceinline__ void reduce_slots(const double *slots, int nslots, double *out, int warp, int lane) {
+  for (int i = warp; i < NPART; i += kWarps) {
+    double v = 0.0;
+    for (int b0 = lane; b0 < nslots; b0 += 32 * 8) {
+      double q[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int b = b0 + 32 * j;
+        q[j] = b < nslots ? __ldcg(slots + (int64_t)b * NPART + i) : 0.0;
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v += q[j];
+    }
+    v = warp_sum(v);
+    if (lane == 0) out[i] = v;
+  }
+}
 
 __device__ __forceinline__ uint64_t pack2(float lo, float hi) {
   uint64_t r;
@@ -123,6 +171,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int it = 0; it < p.iters; ++it) {
         const T *Xin = static_cast<const T *>((it & 1) ? p.Xout : p.X);
         bool ready = it == 0;
+        unsigned long long *ts = p.ts ? p.ts + ((int64_t)it * gridDim.x + blockIdx.x) * kTsSlots : nullptr;
+        if (ts) ts[0] = globaltimer();
         for (int64_t st = sk_bound(p.steps, gridDim.x, blockIdx.x); st < s_end; ++st) {
           const int panel = (int)(st / p.total_tiles), t = (int)(st - (int64_t)panel * p.total_tiles);
           const int tt = tile_of_step(t, p);
@@ -141,6 +191,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             fence_proxy_async_global();
             ready = true;
+            if (ts) ts[1] = globaltimer();
           }
           bulk_load(sb + C::A_BYTES, Xin + (int64_t)tt * D * kColTile, C::X_BYTES, &full[stage], pol_x);
           if (++stage == C::STAGES) { stage = 0; phase ^= 1u; }
@@ -152,10 +203,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   // ------------------------------------------------------------------ consumer warps
   T *sX = scr_all + warp * C::SCR_T;
-  T *sG = sX + C::E;
-  T *sH = sG + C::E;
-  T *sS = sH + C::E;
-  T *sM = sS + C::E;
+  T *sG = sX + C::EP;   // 16-byte aligned: lane 0 fills it with vector stores
+  T *sH = sG + C::EP;
+  T *sS = sH + C::EP;
+  T *sM = sS + C::EP;
   double *gram1 = gram_all + warp * 2 * C::DD;
   double *gram2 = gram1 + C::DD;
 #pragma unroll
@@ -172,6 +223,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // panel cut by a CTA boundary is finished by whichever covering CTA arrives last, so its
   // contribution goes to a per-(panel, warp) slot and is summed later in a fixed order
   // (bitwise-deterministic results).
+  double *part_base = p.cta_part;   // this iteration's partial slots (see part_iters)
   auto commit = [&](bool split_panel, int panel, const double *g1, const double *g2, double so, double xs) {
     if (!split_panel) {
 #pragma unroll
@@ -197,7 +249,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) { xw[2 * C::DD] = so; xw[2 * C::DD + 1] = xs; }
     named_bar_sync(1, kWarps * 32);
     const int slot_cta = sk_owner((int64_t)panel * p.total_tiles, p.steps, gridDim.x) + 1;
-    double *slot = p.cta_part + ((int64_t)gridDim.x + slot_cta) * C::NPART;
+    double *slot = part_base + ((int64_t)gridDim.x + slot_cta) * C::NPART;
     for (int i = threadIdx.x; i < C::NPART; i += kWarps * 32) {
       double v = 0.0;
       for (int w = 0; w < kWarps; ++w) v += xred[w * C::NPART + i];
@@ -213,7 +265,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   pt.X = (it & 1) ? p.Xout : p.X;
   pt.Xout = (it & 1) ? const_cast<void *>(p.X) : p.Xout;
   pt.result = p.result + (int64_t)it * C::NPART;
+  const bool deferred = p.part_iters != nullptr && p.iters > 1;
+  if (deferred) part_base = p.part_iters + (int64_t)it * 2 * gridDim.x * C::NPART;
   const T *Xg = static_cast<const T *>(pt.X);
+  unsigned long long *cts = (p.ts && threadIdx.x == 0) ? p.ts + ((int64_t)it * gridDim.x + blockIdx.x) * kTsSlots : nullptr;
+  bool first_stage = true;
   if (it > 0) {
 #pragma unroll
     for (int m = 0; m < C::DDL; ++m) {
@@ -248,6 +304,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kp = 0; kp < C::KP + KL; ++kp) acc2[r][kp] = 0ull;
       for (int t = t0; t < t1; ++t) {
         mbar_wait(&full[stage], phase);
+        if (cts && first_stage) { cts[2] = globaltimer(); first_stage = false; }
         const float *As = reinterpret_cast<const float *>(smem + stage * C::STAGE_BYTES) + (warp * C::RT) * kColTile + 2 * lane;
         const float *Xt = reinterpret_cast<const float *>(smem + stage * C::STAGE_BYTES + C::A_BYTES);
         const float *Xs = Xt + 4 * lane;
@@ -347,56 +404,76 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
 
+    if (cts) cts[5] = globaltimer();   // streaming of this segment done
     // ---- reduce the lane-partial sums: every lane ends with the full B rows of the warp
 #pragma unroll
     for (int r = 0; r < C::RT; ++r)
 #pragma unroll
       for (int k = 0; k < D; ++k) acc[r][k] = warp_sum(acc[r][k]);
+    if (cts) cts[7] = globaltimer();   // lane partials reduced
 
     if (split_panel) {
       // partial B of this segment -> slot (CTA, first|last segment); the last covering CTA
       // to arrive sums all segments in CTA order and runs the epilogue.
       const int which = (panel == first_panel) ? 0 : 1;
-      T *bp = static_cast<T *>(p.Bpart) + (((int64_t)blockIdx.x * 2 + which) * C::ROWS + warp * C::RT) * D;
-#pragma unroll
-      for (int r = 0; r < C::RT; ++r)
-#pragma unroll
-        for (int k = 0; k < D; ++k)
-          if (((r * D + k) & 31) == lane) __stcg(bp + r * D + k, acc[r][k]);
-      __threadfence();
+      T *bp = static_cast<T *>(p.Bpart) + (((int64_t)blockIdx.x * 2 + which) * kWarps + warp) * C::EP;
+      lane0_store_rows<T, C::RT, D, true>(bp, acc, lane);
       const int c_lo = sk_owner((int64_t)panel * p.total_tiles, p.steps, gridDim.x);
       const int c_hi = sk_owner((int64_t)(panel + 1) * p.total_tiles - 1, p.steps, gridDim.x);
+      // release/acquire through ONE thread: the CTA barrier orders every consumer's stores
+      // before thread 0's (cumulative) fence + arrival; an acquiring fence by thread 0 then the
+      // barrier orders the partial reads after it.  (A fence in every thread serialises: ~4 us.)
       named_bar_sync(1, kWarps * 32);
+      if (cts) cts[8] = globaltimer();   // partial stored
       if (threadIdx.x == 0) {
+        fence_acq_rel_gpu();
         const unsigned prev = atomicAdd(&p.panel_cnt[panel], 1u);
-        *flag = (prev == (unsigned)(c_hi - c_lo));
+        const int is_last = (prev == (unsigned)(c_hi - c_lo));
+        if (is_last) {
+          fence_acq_rel_gpu();
+          p.panel_cnt[panel] = 0u;   // ready for the next launch
+        }
+        *flag = is_last;
       }
       named_bar_sync(1, kWarps * 32);
       const int last = *flag;
+      if (cts) cts[9] = globaltimer();   // arrival counted
       named_bar_sync(1, kWarps * 32);   // everyone read flag before it is rewritten
       if (!last) continue;
-      __threadfence();
-      if (threadIdx.x == 0) p.panel_cnt[panel] = 0u;   // ready for the next launch
+      // Sum the covering CTAs' partials in CTA order.  A covering CTA cb > c_lo starts inside
+      // this panel (slot 0); c_lo used slot 1 iff it started in an earlier panel.  Loads are
+      // issued 4 CTAs x EPL entries at a time (independent L2 round trips), summed in order.
+      const int w2_lo = sk_bound(p.steps, gridDim.x, c_lo) < (int64_t)panel * p.total_tiles ? 1 : 0;
+      const T *bpr = static_cast<const T *>(p.Bpart) + (int64_t)warp * C::EP;
+      T v[C::EPL];
 #pragma unroll
-      for (int m = 0; m < C::EPL; ++m) {
-        const int e = lane + 32 * m;
-        if (e < C::E) {
-          T v = T(0);
-          for (int cb = c_lo; cb <= c_hi; ++cb) {
-            const int w2 = (panel == (int)(sk_bound(p.steps, gridDim.x, cb) / p.total_tiles)) ? 0 : 1;
-            v += __ldcg(static_cast<const T *>(p.Bpart) + (((int64_t)cb * 2 + w2) * C::ROWS + warp * C::RT) * D + e);
+      for (int m = 0; m < C::EPL; ++m) v[m] = T(0);
+      for (int cb0 = c_lo; cb0 <= c_hi; cb0 += 4) {
+        T part[4][C::EPL];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int cb = cb0 + j;
+          const int w2 = cb == c_lo ? w2_lo : 0;
+          const T *src = bpr + ((int64_t)cb * 2 + w2) * kWarps * C::EP;
+#pragma unroll
+          for (int m = 0; m < C::EPL; ++m) {
+            const int e = lane + 32 * m;
+            part[j][m] = (cb <= c_hi && e < C::E) ? __ldcg(src + e) : T(0);
           }
-          sG[e] = v;
         }
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+          for (int m = 0; m < C::EPL; ++m) v[m] += part[j][m];
       }
+#pragma unroll
+      for (int m = 0; m < C::EPL; ++m)
+        if (lane + 32 * m < C::E) sG[lane + 32 * m] = v[m];
     } else {
-#pragma unroll
-      for (int r = 0; r < C::RT; ++r)
-#pragma unroll
-        for (int k = 0; k < D; ++k)
-          if (((r * D + k) & 31) == lane) sG[r * D + k] = acc[r][k];
+      lane0_store_rows<T, C::RT, D, false>(sG, acc, lane);
     }
 
+    if (cts) cts[6] = globaltimer();   // B rows of the panel complete (combine done)
     // ---- per-node epilogue (epilogue.cuh), entry-parallel in warp-private smem.
     const int64_t node_base = (int64_t)panel * C::NODES + warp * C::NPW;   // local node of q = 0
     const int64_t rem = p.n_local - node_base;
@@ -409,6 +486,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 
   // ------------------------------------------------------------------ CTA + grid reduction
+  if (cts) cts[3] = globaltimer();   // all own segments + epilogues done
   if (err) atomicOr(p.err, err);
   if (MODE == kModeRgs || MODE == kModeGpm) {
     float mx = ns_region;
@@ -420,7 +498,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   xb = warp_sum(xb);
   if (lane == 0) { red[warp * 2] = s_own; red[warp * 2 + 1] = xb; }
   named_bar_sync(1, kWarps * 32);
-  double *cp = p.cta_part + (int64_t)blockIdx.x * C::NPART;
+  double *cp = part_base + (int64_t)blockIdx.x * C::NPART;
   for (int i = threadIdx.x; i < C::NPART; i += kWarps * 32) {
     double v = 0.0;
     if (i < 2 * C::DD) {
@@ -430,32 +508,46 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     __stcg(cp + i, v);
   }
-  __threadfence();
-  named_bar_sync(1, kWarps * 32);
-  if (threadIdx.x == 0) *flag = (atomicAdd(p.done_cnt, 1u) == gridDim.x - 1);
-  named_bar_sync(1, kWarps * 32);
-  if (*flag) {
-    __threadfence();
-    // slots [0, G): per-CTA sums; [G, 2G): cut panels (unused slots stay zero).  Warp w sums
-    // columns w, w + kWarps, ...: lane j takes slots j, j + 32, ... in order, then a fixed
-    // butterfly — deterministic.
-    const int nslots = 2 * (int)gridDim.x;
-    for (int i = warp; i < C::NPART; i += kWarps) {
-      double v = 0.0;
-      for (int b = lane; b < nslots; b += 32) v += __ldcg(p.cta_part + (int64_t)b * C::NPART + i);
-      v = warp_sum(v);
-      if (lane == 0) pt.result[i] = v;
+  if (!deferred) {
+    named_bar_sync(1, kWarps * 32);
+    if (threadIdx.x == 0) {
+      fence_acq_rel_gpu();
+      const int is_last = (atomicAdd(p.done_cnt, 1u) == gridDim.x - 1);
+      if (is_last) fence_acq_rel_gpu();
+      *flag = is_last;
     }
-    if (threadIdx.x == 0) *p.done_cnt = 0u;
+    named_bar_sync(1, kWarps * 32);
+    if (*flag) {
+      reduce_slots<C::NPART>(p.cta_part, 2 * (int)gridDim.x, pt.result, warp, lane);
+      if (threadIdx.x == 0) *p.done_cnt = 0u;
+    }
   }
+  if (cts) cts[4] = globaltimer();   // end-of-iteration reduction done
   if (p.iters > 1) {   // grid barrier: this CTA's share of X^{it+1} (and partial slots) is done
     named_bar_sync(1, kWarps * 32);
     if (threadIdx.x == 0) {
-      __threadfence();
+      fence_acq_rel_gpu();
       atomicAdd(p.iter_cnt, 1u);
     }
   }
   }  // iterations
+
+  if (p.part_iters != nullptr && p.iters > 1) {
+    // deferred objective reduction: once every CTA has arrived after the last iteration, CTA b
+    // reduces iterations b, b + G, ... (same fixed slot order as the per-iteration path).
+    if (threadIdx.x == 0) {
+      const unsigned target = (unsigned)p.iters * gridDim.x;
+      unsigned spins = 0;
+      while (ld_acquire_gpu(p.iter_cnt) < target) {
+        __nanosleep(64);
+        if (++spins > (1u << 26)) { atomicOr(p.err, kErrTimeout); break; }
+      }
+    }
+    named_bar_sync(1, kWarps * 32);
+    for (int it = blockIdx.x; it < p.iters; it += gridDim.x)
+      reduce_slots<C::NPART>(p.part_iters + (int64_t)it * 2 * gridDim.x * C::NPART, 2 * (int)gridDim.x,
+                             p.result + (int64_t)it * C::NPART, warp, lane);
+  }
 }
 
 // ------------------------------------------------------------------ host-side launchers

@@ -149,6 +149,9 @@ struct nsrgs_ctx {
   ncclComm_t comm = nullptr;
   bool emulated = false;   // test-only: world > 1 without a communicator (collectives are no-ops)
   bool forced_nccl = false; // test-only: world == 1 with a 1-rank NCCL communicator
+  unsigned long long *ts = nullptr;   // debug phase timestamps (nsrgs_debug_timestamps)
+  double *part_iters = nullptr;       // deferred per-iteration partial slots [iters][2G][npart]
+  int part_iters_cap = 0;
   // stats / timing
   bool timing = false;
   std::vector<cudaEvent_t> ev;
@@ -252,6 +255,20 @@ int ensure_res(nsrgs_ctx *c, int slots) {
   return NSRGS_OK;
 }
 
+// Deferred partial slots for a multi-iteration launch of `iters` iterations (zeroed once:
+// unused cut-panel slots must read zero, and every launch writes the same used slots).
+int ensure_part_iters(nsrgs_ctx *c, int iters) {
+  if (iters <= c->part_iters_cap) return NSRGS_OK;
+  if (c->part_iters) cudaFree(c->part_iters);
+  c->part_iters = nullptr;
+  c->part_iters_cap = 0;
+  const size_t bytes = sizeof(double) * (size_t)iters * 2 * c->grid * c->shape.npart;
+  CUDA_TRY(c, cudaMalloc(&c->part_iters, bytes));
+  CUDA_TRY(c, cudaMemsetAsync(c->part_iters, 0, bytes, c->stream));
+  c->part_iters_cap = iters;
+  return NSRGS_OK;
+}
+
 int ensure_small(nsrgs_ctx *c, int64_t count) {
   if (count <= c->small_cap) return NSRGS_OK;
   double *nb = nullptr;
@@ -293,10 +310,12 @@ int build_tmap(nsrgs_ctx *c) {
 
 // One panel-kernel launch: X[src] -> out (mode), partials into res slot.
 int launch_panel(nsrgs_ctx *c, int mode, const void *Xin, void *Xout, double *result, double eta, int K,
-                 int iters = 1) {
+                 int iters = 1, double *part_iters = nullptr) {
   PanelParams p{};
   p.iters = iters;
+  p.part_iters = iters > 1 ? part_iters : nullptr;
   p.iter_cnt = c->counters + c->panels + 1;
+  p.ts = c->ts;
   if (iters > 1) CUDA_TRY(c, cudaMemsetAsync(p.iter_cnt, 0, sizeof(unsigned), c->stream));
   p.X = Xin;
   p.Xout = Xout;
@@ -436,7 +455,7 @@ int nsrgs_destroy(nsrgs_ctx *c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   if (c->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(c->comm);
   for (auto e : c->ev) cudaEventDestroy(e);
-  void *bufs[] = {c->X[0], c->X[1], c->stage, c->cta_part, c->counters, c->Bpart, c->res, c->red_part, c->small,
+  void *bufs[] = {c->part_iters, c->ts, c->X[0], c->X[1], c->stage, c->cta_part, c->counters, c->Bpart, c->res, c->red_part, c->small,
                   c->err, c->ns_region, c->rowpart, c->colpart, c->blocks, c->sym_cnt, c->sym_part};
   for (void *b : bufs)
     if (b) cudaFree(b);
@@ -516,7 +535,7 @@ int nsrgs_create(const nsrgs_desc *desc, nsrgs_ctx **out) {
             alloc((void **)&c->cta_part, sizeof(double) * (size_t)c->grid * 2 * c->shape.npart) &&
             alloc((void **)&c->counters, sizeof(unsigned) * (c->panels + 2)) &&
             alloc((void **)&c->err, sizeof(int)) && alloc((void **)&c->ns_region, sizeof(unsigned));
-  if (ok) ok = alloc(&c->Bpart, c->esz * (size_t)c->grid * 2 * c->shape.rows * c->d);
+  if (ok) ok = alloc(&c->Bpart, c->esz * (size_t)c->grid * 2 * (c->shape.rows * c->d + 4 * 8));   // per-warp slots padded to 16 B
   if (!ok) return bail(NSRGS_ERR_OOM, "device allocation failed");
   if (ensure_res(c, 128) || ensure_small(c, kSmallOut + 256)) return bail(NSRGS_ERR_OOM);
   // Test-only (NSRGS_FORCE_NCCL=1, world == 1): run every collective through a real 1-rank
@@ -718,8 +737,17 @@ static int run_impl(nsrgs_ctx *c, int mode, int T, double eta, int K, double *tr
   if (c->coop && !c->sym && T > 1) {
     // one persistent cooperative launch for all T iterations (grid barrier between them, A
     // prefetched across the boundary) — removes launch gaps and pipeline drains
-    NSRGS_TRY(launch_panel(c, mode, c->X[c->cur], c->X[1 - c->cur], c->res, eta, K, T));
-    if (T & 1) c->cur = 1 - c->cur;
+    // The objective partials of every iteration are reduced once at the end of the launch
+    // (part_iters); launches are chunked so that buffer stays under ~128 MB.
+    const size_t per_iter = sizeof(double) * 2 * (size_t)c->grid * c->shape.npart;
+    const int chunk = (int)std::max<size_t>(2, std::min<size_t>((size_t)T, ((size_t)128 << 20) / per_iter));
+    NSRGS_TRY(ensure_part_iters(c, chunk));
+    for (int t0 = 0; t0 < T; t0 += chunk) {
+      const int Ti = std::min(chunk, T - t0);
+      NSRGS_TRY(launch_panel(c, mode, c->X[c->cur], c->X[1 - c->cur], c->res + (size_t)t0 * c->shape.npart, eta,
+                             K, Ti, c->part_iters));
+      if (Ti & 1) c->cur = 1 - c->cur;
+    }
   } else {
     for (int t = 0; t < T; ++t) {
       NSRGS_TRY(launch_panel(c, mode, c->X[c->cur], c->X[1 - c->cur], c->res + (size_t)t * c->shape.npart, eta, K));
@@ -907,6 +935,30 @@ int nsrgs_set_symmetric(nsrgs_ctx *c, int enable) {
   CUDA_TRY(c, cudaMemcpyAsync(c->blocks, hb.data(), sizeof(int4) * hb.size(), cudaMemcpyHostToDevice, c->stream));
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   c->sym = true;
+  return NSRGS_OK;
+}
+
+int nsrgs_debug_timestamps(nsrgs_ctx *c, int max_iters, unsigned long long *out_host) {
+  // max_iters > 0: (re)arm a device buffer of [max_iters][grid][8] phase stamps for the next
+  // panel launches; max_iters == 0 with out_host: copy the stamps out and disarm.
+  NSRGS_TRY(enter(c));
+  const size_t per = (size_t)c->grid * nsrgs::kTsSlots;
+  static thread_local int armed_iters = 0;
+  if (max_iters > 0) {
+    if (c->ts) cudaFree(c->ts);
+    c->ts = nullptr;
+    CUDA_TRY(c, cudaMalloc(&c->ts, sizeof(unsigned long long) * per * max_iters));
+    CUDA_TRY(c, cudaMemsetAsync(c->ts, 0, sizeof(unsigned long long) * per * max_iters, c->stream));
+    armed_iters = max_iters;
+    return sync_and_check(c);
+  }
+  if (!c->ts) return set_err(c, NSRGS_ERR_STATE, "timestamps not armed");
+  if (out_host)
+    CUDA_TRY(c, cudaMemcpyAsync(out_host, c->ts, sizeof(unsigned long long) * per * armed_iters, cudaMemcpyDeviceToHost,
+                                c->stream));
+  NSRGS_TRY(sync_and_check(c));
+  cudaFree(c->ts);
+  c->ts = nullptr;
   return NSRGS_OK;
 }
 

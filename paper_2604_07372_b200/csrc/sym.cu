@@ -423,12 +423,15 @@ __global__ void __launch_bounds__(256)
     for (int w = 0; w < W; ++w) v += i < 2 * DD ? gram[w][i] : red[w][i - 2 * DD];
     __stcg(sp.e.cta_part + (int64_t)blockIdx.x * NPART + i, v);
   }
-  __threadfence();
   __syncthreads();
-  if (threadIdx.x == 0) flag = (atomicAdd(sp.e.done_cnt, 1u) == gridDim.x - 1);
+  if (threadIdx.x == 0) {   // one fence per CTA (bar.sync + cumulative fence), see panel.cu
+    fence_acq_rel_gpu();
+    const int is_last = (atomicAdd(sp.e.done_cnt, 1u) == gridDim.x - 1);
+    if (is_last) fence_acq_rel_gpu();
+    flag = is_last;
+  }
   __syncthreads();
   if (flag) {
-    __threadfence();
     for (int i = warp; i < NPART; i += W) {
       double v = 0.0;
       for (int b = lane; b < (int)gridDim.x; b += 32) v += __ldcg(sp.e.cta_part + (int64_t)b * NPART + i);

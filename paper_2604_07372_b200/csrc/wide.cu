@@ -156,12 +156,15 @@ __global__ void __launch_bounds__(WideCfg<D>::THREADS, 1)
     for (int w = 0; w < C::W; ++w) v += red[w * C::NPART + i];
     __stcg(p.cta_part + (int64_t)blockIdx.x * C::NPART + i, v);
   }
-  __threadfence();
   named_bar_sync(1, C::W * 32);
-  if (threadIdx.x == 0) *flag = (atomicAdd(p.done_cnt, 1u) == gridDim.x - 1);
+  if (threadIdx.x == 0) {   // one fence per CTA (bar.sync + cumulative fence), see panel.cu
+    fence_acq_rel_gpu();
+    const int is_last = (atomicAdd(p.done_cnt, 1u) == gridDim.x - 1);
+    if (is_last) fence_acq_rel_gpu();
+    *flag = is_last;
+  }
   named_bar_sync(1, C::W * 32);
   if (*flag) {
-    __threadfence();
     for (int i = warp; i < C::NPART; i += C::W) {
       double v = 0.0;
       for (int b = lane; b < (int)gridDim.x; b += 32) v += __ldcg(p.cta_part + (int64_t)b * C::NPART + i);

@@ -75,6 +75,7 @@ _SIGS = {
     "nsrgs_get_X": ([_P, _P, ct.c_int], ct.c_int),
     "nsrgs_get_stats": ([_P, ct.POINTER(Stats)], ct.c_int),
     "nsrgs_set_symmetric": ([_P, ct.c_int], ct.c_int),
+    "nsrgs_debug_timestamps": ([_P, ct.c_int, _P], ct.c_int),
     "nsrgs_reset_stats": ([_P, ct.c_int], ct.c_int),
 }
 for _name, (_args, _res) in _SIGS.items():
@@ -260,6 +261,16 @@ class Solver:
             out = np.empty((self.n, self.d, self.d), dtype=self.np_dtype)
         ptr, dev = self._ptr(out)
         self._check(_lib.nsrgs_get_X(self._h, ptr, dev))
+        return out
+
+    def debug_timestamps(self, max_iters: int = 0):
+        """Arm (max_iters > 0) or collect (0) per-CTA phase timestamps: array [iters][grid][16] ns."""
+        if max_iters > 0:
+            self._ts_iters = max_iters
+            self._check(_lib.nsrgs_debug_timestamps(self._h, max_iters, None))
+            return None
+        out = np.zeros((self._ts_iters, self.stats()["grid"], 16), dtype=np.uint64)
+        self._check(_lib.nsrgs_debug_timestamps(self._h, 0, out.ctypes.data))
         return out
 
     def set_symmetric(self, enable: bool = True):
