@@ -21,28 +21,48 @@ template <typename T> __device__ __forceinline__ T warp_sum(T v) {
   return v;
 }
 
-template <typename T, int D, int NPW, int MODE>
+// X_i entries of the warp's NPW nodes, entry e = lane + 32 m = (q, a, b) -> X_{node_base+q}[a][b],
+// into registers (zero past nvalid).  Loaded from L2 (written by other CTAs).  The panel kernel
+// issues this when a segment starts so the latency hides under the A stream.
+template <typename T, int D, int NPW>
+__device__ __forceinline__ void epi_load_x(const PanelParams &p, const T *Xg, int lane, int64_t node_base, int nvalid,
+                                           T (&xv)[(NPW * D * D + 31) / 32]) {
+  constexpr int DD = D * D, E = NPW * DD, EPL = (E + 31) / 32;
+#pragma unroll
+  for (int m = 0; m < EPL; ++m) {
+    const int e = lane + 32 * m;
+    const int q = e / DD, a = (e / D) % D, b = e % D;
+    xv[m] = T(0);
+    if (e < E && q < nvalid) {
+      const int64_t c = (p.node0 + node_base + q) * D + a;
+      xv[m] = __ldcg(Xg + tile_index(c, b, D, p.rows_local, p.tiles_per_rank));
+    }
+  }
+}
+
+// XPRE: the caller passes the epi_load_x registers in xpre (else they are loaded here).
+template <typename T, int D, int NPW, int MODE, bool XPRE = false>
 __device__ __forceinline__ void node_epilogue(const PanelParams &p, const T *Xg, int lane, int64_t node_base,
                                               int nvalid, T *sX, T *sG, T *sH, T *sS, T *sM,
                                               double (&g1s)[(D * D + 31) / 32], double (&g2s)[(D * D + 31) / 32],
-                                              double &so, double &xs, float &ns_region, int &err) {
+                                              double &so, double &xs, float &ns_region, int &err,
+                                              const T *xpre = nullptr) {
   constexpr int DD = D * D;
   constexpr int E = NPW * DD;
   constexpr int EPL = (E + 31) / 32;
   constexpr int DDL = (DD + 31) / 32;
   const T coef = (T)p.coef, eta = (T)p.eta;
+  {
+    T xv[EPL];
+    if constexpr (XPRE) {
 #pragma unroll
-  for (int m = 0; m < EPL; ++m) {
-    const int e = lane + 32 * m;
-    if (e < E) {
-      const int q = e / DD, a = (e / D) % D, b = e % D;
-      T x = T(0);
-      if (q < nvalid) {
-        const int64_t c = (p.node0 + node_base + q) * D + a;
-        x = __ldcg(Xg + tile_index(c, b, D, p.rows_local, p.tiles_per_rank));   // L2: written by other CTAs
-      }
-      sX[e] = x;
+      for (int m = 0; m < EPL; ++m) xv[m] = xpre[m];
+    } else {
+      epi_load_x<T, D, NPW>(p, Xg, lane, node_base, nvalid, xv);
     }
+#pragma unroll
+    for (int m = 0; m < EPL; ++m)
+      if (lane + 32 * m < E) sX[lane + 32 * m] = xv[m];
   }
   __syncwarp();
 

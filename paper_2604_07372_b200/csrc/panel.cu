@@ -289,6 +289,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int t1 = t1l < p.total_tiles ? (int)t1l : p.total_tiles;
     st += t1 - t0;
     const bool split_panel = !(t0 == 0 && t1 == p.total_tiles);
+    const int64_t node_base = (int64_t)panel * C::NODES + warp * C::NPW;   // local node of q = 0
+    const int64_t rem = p.n_local - node_base;
+    const int nvalid = rem <= 0 ? 0 : (rem < C::NPW ? (int)rem : C::NPW);
+    // X_i of this warp's nodes for the epilogue, in flight during the stream.  Issued after the
+    // segment's first stage has landed: X^it is only guaranteed complete (all CTAs' epilogues
+    // of it-1) once the producer passed the grid barrier and that stage's barrier completed
+    // (writers' release -> producer acquire -> mbarrier arrive/wait).  The loop's own wait on
+    // this phase then returns at once.
+    mbar_wait(&full[stage], phase);
+    T xpre[C::EPL];
+    epi_load_x<T, D, C::NPW>(pt, Xg, lane, node_base, nvalid, xpre);
 
     // Lane l owns columns {2l, 2l+1, 64+2l, 65+2l} of each 128-column tile: A row pieces are
     // conflict-free 64-bit smem loads, X component pairs conflict-free 128-bit loads.
@@ -475,12 +486,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     if (cts) cts[6] = globaltimer();   // B rows of the panel complete (combine done)
     // ---- per-node epilogue (epilogue.cuh), entry-parallel in warp-private smem.
-    const int64_t node_base = (int64_t)panel * C::NODES + warp * C::NPW;   // local node of q = 0
-    const int64_t rem = p.n_local - node_base;
-    const int nvalid = rem <= 0 ? 0 : (rem < C::NPW ? (int)rem : C::NPW);
     double g1s[C::DDL], g2s[C::DDL], so = 0.0, xs = 0.0;
-    node_epilogue<T, D, C::NPW, MODE>(pt, Xg, lane, node_base, nvalid, sX, sG, sH, sS, sM, g1s, g2s, so, xs,
-                                      ns_region, err);
+    node_epilogue<T, D, C::NPW, MODE, true>(pt, Xg, lane, node_base, nvalid, sX, sG, sH, sS, sM, g1s, g2s, so, xs,
+                                            ns_region, err, xpre);
     commit(split_panel, panel, g1s, g2s, so, xs);
     __syncwarp();
   }

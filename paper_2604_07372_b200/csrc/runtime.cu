@@ -522,8 +522,15 @@ int nsrgs_create(const nsrgs_desc *desc, nsrgs_ctx **out) {
     int l2 = 0;
     cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, c->device);
     const double a_bytes = (double)c->esz * (double)c->plan.rows_local * (double)c->N;
-    const double keep = 0.7 * (double)l2 / std::max(1.0, a_bytes);
-    c->a_keep = a_bytes <= 4.0 * l2 ? (float)std::min(1.0, keep) : 0.f;
+    // Share of A tagged evict_last so that part of it stays L2-resident across passes.
+    // Measured on B200 (tools/keep_sweep.sh, coop per-iteration time): best kept bytes are
+    // ~0.55 L2 for A <= 1.5 L2 (n=2000 d=3, 144 MB: 22.8 us vs 31.3 without, 31.9 keeping
+    // 0.7 L2 — over-keeping thrashes), ~0.4 L2 up to 2.8 L2 (324 MB: 49.7 vs 57.1 us), none
+    // beyond (400 MB: keeping anything is 3 % slower).
+    const double ratio = a_bytes / std::max(1.0, (double)l2);
+    const double kept = ratio <= 1.5 ? 0.55 * l2 : ratio <= 2.8 ? 0.4 * l2 : 0.0;
+    c->a_keep = (float)std::min(1.0, kept / std::max(1.0, a_bytes));
+    if (const char *ek = std::getenv("NSRGS_A_KEEP")) c->a_keep = (float)std::atof(ek);   // tuning experiments
   }
   auto alloc = [&](void **p, size_t bytes) {
     cudaError_t e = cudaMalloc(p, bytes);

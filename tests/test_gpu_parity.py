@@ -630,3 +630,31 @@ def test_nccl_plumbing_one_rank(nsrgs, monkeypatch):
         s.close()
     (sw0, tr0, X0, r0, f0), (sw1, tr1, X1, r1, f1) = outs
     assert sw0 == sw1 and np.array_equal(X0, X1) and np.array_equal(tr0, tr1) and r0 == r1 and f0 == f1
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,d,dtype", [(100, 3, "f32"), (2000, 3, "f32"), (333, 7, "f32"), (300, 10, "f32"),
+                                       (200, 4, "f64"), (150, 5, "f64")])
+def test_multi_iteration_launch_bitwise_equals_per_iteration_launches(nsrgs, monkeypatch, n, d, dtype):
+    """The cooperative multi-iteration launch (grid barrier between iterations, A prefetched
+    across the boundary, X prefetched for the epilogue, deferred objective reduction) must be
+    bitwise identical to one launch per iteration: same X^T, same objective trace (NS-RGS and
+    GPM).  Catches any read of X^t before every CTA has written it."""
+    import torch
+
+    torch.cuda.synchronize()
+    dt = nsrgs.F32 if dtype == "f32" else nsrgs.F64
+    outs = []
+    for no_coop in ("0", "1"):
+        monkeypatch.setenv("NSRGS_NO_COOP", no_coop)
+        s = nsrgs.Solver(n, d, dtype=dt)
+        s.generate(5, 1.0, want_Z=False)
+        s.init_spectral(5, 60, 1e-5, allow_unconverged=True)
+        tr = s.run(25, 1.0 / n, 5)
+        X = s.get_X()
+        trg = s.gpm_run(6)
+        outs.append((tr, X, trg, s.get_X()))
+        s.close()
+    (a, b, c, e), (a1, b1, c1, e1) = outs
+    assert np.array_equal(a, a1) and np.array_equal(b, b1)
+    assert np.array_equal(c, c1) and np.array_equal(e, e1)

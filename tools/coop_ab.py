@@ -6,7 +6,7 @@ if len(sys.argv) > 2 and sys.argv[2] == "child":
     import torch
     from paper_2604_07372_b200 import nsrgs
     cfg = sys.argv[1]
-    n, d, c, K = {"c1": (100, 3, None, 3), "c2": (2000, 3, None, 5), "c3": (20000, 5, 0.3, 5), "c4": (12000, 10, 0.2, 6)}[cfg]
+    n, d, c, K = {"c1": (100, 3, None, 3), "c2": (2000, 3, None, 5), "m1": (1500, 3, None, 5), "m2": (3000, 3, None, 5), "m3": (2000, 5, None, 5), "c3": (20000, 5, 0.3, 5), "c4": (12000, 10, 0.2, 6)}[cfg]
     sigma = 0.5 if c is None else c * np.sqrt(n) / d
     s = nsrgs.Solver(n, d)
     s.generate(0, sigma, want_Z=False)
