@@ -16,12 +16,22 @@ constexpr int kThreads = 32 * (kWarps + 1);   // + 1 TMA producer warp
 // Launch parameters of the panel kernel (panel.cu).  Plain struct, passed by value.
 struct PanelParams {
   const void *X;        // tile layout, input iterate X^t (or Y for the subspace sweep)
-  void *Xout;           // tile layout, output X^{t+1} (RGS) or W = A Y (PRODUCT)
-  void *Bpart;          // stream-K partial B of cut panels [grid][2][rows_per_panel][d]
-  unsigned *panel_cnt;  // arrival counters of cut panels [panels]
-  double *cta_part;     // fp64 partials: [grid][npart] per CTA, then [grid][npart] cut panels (zeroed once)
+  void *Xout;           // tile layout, output X^{t+1} (RGS / GPM) or W = A Y (PRODUCT)
+  // ---- dense panel kernel (panel.cu): dynamic schedule over a fixed unit list
+  const int4 *units;    // [nunits] (panel, t_begin, t_end, slot): column steps [t_begin, t_end) of
+                        // a panel; slot >= 0: the split unit's partial-B slot, -1: whole panel
+  const int2 *pinfo;    // [panels] (units covering the panel, first slot); a split panel's slots
+                        // are contiguous in column order (= the fixed combine order)
+  int nunits;
+  void *Bpart;          // split-unit partial B rows [slots][kWarps][EP] (EP = RT d padded to 16 B)
+  unsigned *ucnt;       // [panels][kWarps] unit arrivals per (split panel, warp); self-resetting
+  unsigned *ctl;        // [0] unit queue head (runs over iters x nunits), [1] (panel, warp)
+                        // epilogues completed (X^{t+1} readiness), [2] CTAs exited; self-resetting
+  unsigned long long *acc;   // [iters][npart][2] exact 128-bit fixed-point sums (lo, hi); self-zeroing
+  // ---- wide / sym kernels: per-CTA fp64 slots + last-CTA reduction
+  double *cta_part;     // [grid][npart]
   unsigned *done_cnt;   // CTA arrival counter for the last-CTA reduction
-  double *result;       // npart doubles: reduced partials of this launch
+  double *result;       // [iters][npart] doubles: reduced partials (objective / Gram terms)
   int *err;             // device error word (bit flags, see kErr*)
   unsigned *ns_region;  // float bits of max ||I - F^T F||_F (atomicMax on non-negative floats)
   int64_t n;            // total nodes
@@ -29,21 +39,14 @@ struct PanelParams {
   int64_t tiles_per_rank;
   int world, rank;
   int panels, total_tiles;   // total_tiles = column tiles per panel (all ranks' slices)
-  int64_t steps;             // stream-K work = panels * total_tiles
   float a_keep;         // fraction of A accesses tagged L2 evict_last (A shard ~ L2 size), else evict_first
   double coef;          // n - 1   (identity term of G_i)
   double eta;           // step size mu
   int K;                // Newton-Schulz steps (Algorithm 1)
-  // multi-iteration persistent launch (world == 1, cooperative): iteration t reads X (t even) or
-  // Xout (t odd), writes the other; result slot t = result + t * npart; iter_cnt = grid barrier
+  // iterations per launch (panel kernel, world == 1): iteration t reads X (t even) or Xout
+  // (t odd) and writes the other; X^t is complete once ctl[1] >= t * panels * kWarps
   int iters;
-  unsigned *iter_cnt;
-  // deferred objective partials (iters > 1): iteration t's 2G partial slots go to
-  // part_iters + t * 2G * npart (zeroed once; the same slots are written every launch), and the
-  // slot reduction for all t runs once after the last iteration, off the per-iteration
-  // critical path.  nullptr: per-iteration last-CTA reduction through cta_part.
-  double *part_iters;
-  unsigned long long *ts;   // optional phase timestamps [iters][grid][8] (%globaltimer ns), debug
+  unsigned long long *ts;   // optional phase timestamps [iters][grid][kTsSlots] (%globaltimer ns), debug
 };
 
 // Symmetric half-storage pass (sym.cu): blocks of GP panels x kSymTilesPerBlock column tiles.

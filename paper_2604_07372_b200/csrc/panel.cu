@@ -5,17 +5,17 @@
 //   P_i = (G_i - X_i G_i^T X_i)/2,  F_i = X_i - eta P_i
 //   X_i^{t+1} = S(F_i): K steps S <- 1/2 S (3I - S^T S)
 //
-// Design: persistent grid, one CTA per SM, 8 consumer warps + 1 TMA
-// producer warp.  Work unit = (row panel of ROWS = 8*RT rows, column split).  The producer
-// streams A tiles (ROWS x 128, 3-D tensor map over (col-in-rank-slice, rank slice, row)) and
-// the matching X tile (d x 128, contiguous in the tile layout) into an mbarrier ring with an
-// L2 evict-first policy on A and evict-last on X.  Each consumer warp owns RT rows (= whole
-// nodes); lane l owns columns 4l..4l+3 of every tile and keeps RT x d fp32 accumulators in
-// registers, so every X value read from smem is reused RT times and A is read from smem once
-// with conflict-free 128-bit loads.  At the end of a panel the warp reduces its accumulators
-// with shuffles and runs the per-node epilogue entry-parallel in warp-private smem; no B is
-// ever written to HBM.  fp64 partials for the objective / Gram matrices are reduced
-// deterministically (fixed order, last-CTA pattern).
+// Design: persistent grid, one CTA per SM, 7 consumer warps + 1 TMA
+// producer warp.  Work units (a row panel of ROWS = 7 RT rows, or a column range of one) come
+// from an atomic queue.  The producer streams A tiles (ROWS x 128, 3-D tensor map over
+// (col-in-rank-slice, rank slice, row)) and the matching X tile (d x 128, contiguous in the
+// tile layout) into an mbarrier ring, A with an L2 evict-first (or fractional evict-last)
+// policy, X evict-last.  Each consumer warp owns RT rows (= whole nodes); lane l owns 4
+// columns of every tile and keeps RT x d fp32 accumulators in registers (FFMA2 on component
+// pairs), so every X value read from smem is reused RT times and A is read from smem once.
+// At the end of a panel the warp reduces its accumulators with shuffles and runs the per-node
+// epilogue entry-parallel in warp-private smem; no B is ever written to HBM.  Objective / Gram
+// partials are summed exactly in 128-bit fixed point (deterministic under any schedule).
 #include <cuda.h>
 
 #include "common.cuh"
@@ -50,7 +50,7 @@ struct PanelCfg {
   static constexpr int EP = (E + VW - 1) / VW * VW;                  // E padded to 16 B
   static constexpr int SCR_T = 5 * EP;                                // sX sG sH sS sM
   static constexpr int SCR_T_BYTES = (kWarps * SCR_T * (int)sizeof(T) + 15) / 16 * 16;   // keep doubles aligned
-  static constexpr int SCR_BYTES = SCR_T_BYTES + kWarps * 2 * DD * 8 + kWarps * 2 * 8 + kWarps * NPART * 8 + 64;
+  static constexpr int SCR_BYTES = SCR_T_BYTES + kWarps * NPART * 16 + 8 * 8 + 64;   // + fixed-point slices, meta, flag
   static constexpr int BUDGET = 220 * 1024;
   static constexpr int STAGES_RAW = (BUDGET - 1024 - BAR_BYTES - SCR_BYTES) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
@@ -83,28 +83,6 @@ __device__ __forceinline__ void lane0_store_rows(T *dst, const T (&acc)[RT][D], 
   }
 }
 
-// Sum nslots partial slots [nslots][NPART] into out[NPART] (consumer warps).  Warp w takes
-// entries w, w + kWarps, ...; lane j sums slots j, j + 32, ... in order (loads issued 8 at a
-// time: independent L2 round trips), then a fixed butterfly — deterministic.
-template <int NPART>
-__device__ __forceinline__ void reduce_slots(const double *slots, int nslots, double *out, int warp, int lane) {
-  for (int i = warp; i < NPART; i += kWarps) {
-    double v = 0.0;
-    for (int b0 = lane; b0 < nslots; b0 += 32 * 8) {
-      double q[8];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const int b = b0 + 32 * j;
-        q[j] = b < nslots ? __ldcg(slots + (int64_t)b * NPART + i) : 0.0;
-      }
-#pragma unroll
-      for (int j = 0; j < 8; ++j) v += q[j];
-    }
-    v = warp_sum(v);
-    if (lane == 0) out[i] = v;
-  }
-}
-
 __device__ __forceinline__ uint64_t pack2(float lo, float hi) {
   uint64_t r;
   asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
@@ -121,10 +99,6 @@ __device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
 }
 
 
-// Stream-K schedule: the panels x tiles steps are cut into gridDim.x equal contiguous ranges.
-__device__ __forceinline__ int64_t sk_bound(int64_t W, int G, int b) { return W * b / G; }
-// CTA whose range contains step s: max b with sk_bound(b) <= s.
-__device__ __forceinline__ int sk_owner(int64_t s, int64_t W, int G) { return (int)(((s + 1) * G + W - 1) / W - 1); }
 // Column-tile order within a panel: this rank's own X slice first (ready earliest under P > 1).
 __device__ __forceinline__ int tile_of_step(int t, const PanelParams &p) {
   const int tpr = (int)p.tiles_per_rank;
@@ -132,6 +106,47 @@ __device__ __forceinline__ int tile_of_step(int t, const PanelParams &p) {
   return ((g + p.rank) % p.world) * tpr + (t - g * tpr);
 }
 
+// ---- exact order-independent fp64 sums: 128-bit fixed point with 40 fraction bits.
+// Objective / Gram partials are converted per (panel, warp) epilogue and added as integers, so
+// the totals do not depend on which CTA ran which unit (bitwise-deterministic results under
+// the dynamic schedule).  |partial| < 2^86; resolution 2^-40 ~ 9e-13 absolute, far below the
+// fp64 rounding of the O(1e4..1e10) terms it sums.
+constexpr double kFixScale = 1099511627776.0;   // 2^40
+constexpr double kTwo64 = 18446744073709551616.0;
+__device__ __forceinline__ void fix_from(double v, unsigned long long &lo, long long &hi, int &err) {
+  if (!(fabs(v) < 1e25)) {   // non-finite or out of range
+    err |= kErrNonfinite;
+    v = 0.0;
+  }
+  const double sc = v * kFixScale;                  // exact (power of two)
+  const double h = floor(sc * (1.0 / kTwo64));      // exact
+  hi = (long long)h;
+  lo = (unsigned long long)(sc - h * kTwo64);       // in [0, 2^64), exact up to sc's own ulp
+}
+__device__ __forceinline__ void fix_add(unsigned long long &lo, long long &hi, unsigned long long alo, long long ahi) {
+  const unsigned long long s = lo + alo;
+  hi += ahi + (s < lo ? 1ll : 0ll);
+  lo = s;
+}
+__device__ __forceinline__ void fix_atomic_add(unsigned long long *g, unsigned long long lo, long long hi) {
+  if (lo == 0ull && hi == 0ll) return;
+  const unsigned long long old = atomicAdd(g, lo);
+  atomicAdd(g + 1, (unsigned long long)hi + (old + lo < old ? 1ull : 0ull));
+}
+__device__ __forceinline__ double fix_to(unsigned long long lo, long long hi) {
+  return (double)hi * (kTwo64 / kFixScale) + (double)lo * (1.0 / kFixScale);
+}
+
+struct UnitMeta {   // published by the producer per stage: global unit index (-1: no more work), tile step
+  int kg, t;
+};
+
+// Dense pass.  Persistent CTAs (one per SM) take work units from an atomic queue that runs over
+// iters x nunits (iteration-major).  A unit is a whole row panel or, for the tail of the list,
+// an equal column range of one; per-SM bandwidth differs by a few % (GPC population), so the
+// dynamic queue, not a static split, balances the pass.  Each consumer warp owns RT rows of the
+// panel; at the end of a split unit it publishes its partial rows and the last of the panel's
+// units to arrive (per warp) sums them in column order and runs the epilogue for its nodes.
 template <typename T, int D, int MODE>
 __global__ void __launch_bounds__(kThreads, 1)
     panel_kernel(const __grid_constant__ CUtensorMap tmA, const PanelParams p) {
@@ -144,10 +159,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + C::STAGES * C::STAGE_BYTES);
   uint64_t *empty = full + 8;
   T *scr_all = reinterpret_cast<T *>(smem + C::STAGES * C::STAGE_BYTES + C::BAR_BYTES);
-  double *gram_all = reinterpret_cast<double *>(reinterpret_cast<uint8_t *>(scr_all) + C::SCR_T_BYTES);
-  double *red = gram_all + kWarps * 2 * C::DD;       // [kWarps][2]
-  double *xred = red + kWarps * 2;                   // [kWarps][NPART] cut-panel pre-reduction
-  int *flag = reinterpret_cast<int *>(xred + kWarps * C::NPART);
+  unsigned long long *fix_all =
+      reinterpret_cast<unsigned long long *>(reinterpret_cast<uint8_t *>(scr_all) + C::SCR_T_BYTES);   // [kWarps][NPART][2]
+  UnitMeta *meta = reinterpret_cast<UnitMeta *>(fix_all + kWarps * C::NPART * 2);                     // [8]
+  int *flag = reinterpret_cast<int *>(meta + 8);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -157,7 +172,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     fence_mbar_init();
   }
+  for (int i = threadIdx.x; i < kWarps * C::NPART * 2; i += kThreads) fix_all[i] = 0ull;
   __syncthreads();
+  const int total_units = p.iters * p.nunits;
+  const unsigned epi_per_iter = (unsigned)p.panels * kWarps;
 
   // ------------------------------------------------------------------ producer warp
   if (warp == kWarps) {
@@ -167,30 +185,40 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t pol_x = policy_evict_last();
       int stage = 0;
       uint32_t phase = 0;
-      const int64_t s_end = sk_bound(p.steps, gridDim.x, blockIdx.x + 1);
-      for (int it = 0; it < p.iters; ++it) {
+      int ready_it = 0;   // X^it known complete for it <= ready_it
+      int ts_it = -1;
+      for (;;) {
+        const int kg = (int)atomicAdd(&p.ctl[0], 1u);
+        if (kg >= total_units) {
+          mbar_wait(&empty[stage], phase ^ 1u);
+          meta[stage].kg = -1;
+          mbar_arrive(&full[stage]);
+          break;
+        }
+        const int it = kg / p.nunits;
+        const int4 u = __ldg(p.units + (kg - it * p.nunits));
         const T *Xin = static_cast<const T *>((it & 1) ? p.Xout : p.X);
-        bool ready = it == 0;
         unsigned long long *ts = p.ts ? p.ts + ((int64_t)it * gridDim.x + blockIdx.x) * kTsSlots : nullptr;
-        if (ts) ts[0] = globaltimer();
-        for (int64_t st = sk_bound(p.steps, gridDim.x, blockIdx.x); st < s_end; ++st) {
-          const int panel = (int)(st / p.total_tiles), t = (int)(st - (int64_t)panel * p.total_tiles);
+        if (ts && it != ts_it) { ts[0] = globaltimer(); ts_it = it; }
+        for (int t = u.y; t < u.z; ++t) {
           const int tt = tile_of_step(t, p);
           const int g = tt / (int)p.tiles_per_rank, jt = tt - g * (int)p.tiles_per_rank;
           mbar_wait(&empty[stage], phase ^ 1u);
+          meta[stage].kg = kg;
+          meta[stage].t = t;
           uint8_t *sb = smem + stage * C::STAGE_BYTES;
           mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
-          tma_load_3d(sb, &tmA, &full[stage], jt * kColTile, g, panel * C::ROWS, pol_a);
-          if (!ready) {
-            // A of iteration `it` is already in flight; X^it needs every CTA's epilogues of it-1
-            const unsigned target = (unsigned)it * gridDim.x;
+          tma_load_3d(sb, &tmA, &full[stage], jt * kColTile, g, u.x * C::ROWS, pol_a);
+          if (it > ready_it) {
+            // A of this unit is in flight; X^it needs every (panel, warp) epilogue of it-1
+            const unsigned target = (unsigned)it * epi_per_iter;
             unsigned spins = 0;
-            while (ld_acquire_gpu(p.iter_cnt) < target) {
+            while (ld_acquire_gpu(&p.ctl[1]) < target) {
               __nanosleep(64);
               if (++spins > (1u << 26)) { atomicOr(p.err, kErrTimeout); break; }
             }
             fence_proxy_async_global();
-            ready = true;
+            ready_it = it;
             if (ts) ts[1] = globaltimer();
           }
           bulk_load(sb + C::A_BYTES, Xin + (int64_t)tt * D * kColTile, C::X_BYTES, &full[stage], pol_x);
@@ -207,97 +235,64 @@ __global__ void __launch_bounds__(kThreads, 1)
   T *sH = sG + C::EP;
   T *sS = sH + C::EP;
   T *sM = sS + C::EP;
-  double *gram1 = gram_all + warp * 2 * C::DD;
-  double *gram2 = gram1 + C::DD;
-#pragma unroll
-  for (int m = 0; m < C::DDL; ++m) {
-    const int e = lane + 32 * m;
-    if (e < C::DD) { gram1[e] = 0.0; gram2[e] = 0.0; }
-  }
-  double s_own = 0.0, xb = 0.0;     // sum_i ||X_i^T X_i||^2, <X, B>
+  unsigned long long *fixw = fix_all + warp * C::NPART * 2;   // this warp's fixed-point sums
   float ns_region = 0.f;
   int err = 0;
 
-  // Objective / Gram partials.  A panel whose tiles all lie in this CTA's stream-K range is
-  // finished here by construction (static) and accumulates into the per-CTA running sums; a
-  // panel cut by a CTA boundary is finished by whichever covering CTA arrives last, so its
-  // contribution goes to a per-(panel, warp) slot and is summed later in a fixed order
-  // (bitwise-deterministic results).
-  double *part_base = p.cta_part;   // this iteration's partial slots (see part_iters)
-  auto commit = [&](bool split_panel, int panel, const double *g1, const double *g2, double so, double xs) {
-    if (!split_panel) {
-#pragma unroll
-      for (int m = 0; m < C::DDL; ++m) {
-        const int e = lane + 32 * m;
-        if (e < C::DD) { gram1[e] += g1[m]; gram2[e] += g2[m]; }
-      }
-      s_own += so;
-      xb += xs;
-      return;
-    }
-    // all consumer warps finish the same cut panel together: pre-reduce across warps in smem
-    // (fixed warp order), one global slot per cut panel, indexed by the first CTA whose range
-    // starts inside it.
-    so = warp_sum(so);
-    xs = warp_sum(xs);
-    double *xw = xred + warp * C::NPART;
-#pragma unroll
-    for (int m = 0; m < C::DDL; ++m) {
-      const int e = lane + 32 * m;
-      if (e < C::DD) { xw[e] = g1[m]; xw[C::DD + e] = g2[m]; }
-    }
-    if (lane == 0) { xw[2 * C::DD] = so; xw[2 * C::DD + 1] = xs; }
+  // CTA-wide: add the warps' fixed-point sums of iteration `it` to the global accumulators.
+  // All consumer warps process the same unit sequence, so they all reach this together.
+  auto flush = [&](int it) {
     named_bar_sync(1, kWarps * 32);
-    const int slot_cta = sk_owner((int64_t)panel * p.total_tiles, p.steps, gridDim.x) + 1;
-    double *slot = part_base + ((int64_t)gridDim.x + slot_cta) * C::NPART;
     for (int i = threadIdx.x; i < C::NPART; i += kWarps * 32) {
-      double v = 0.0;
-      for (int w = 0; w < kWarps; ++w) v += xred[w * C::NPART + i];
-      __stcg(slot + i, v);
+      unsigned long long lo = 0ull;
+      long long hi = 0ll;
+      for (int w = 0; w < kWarps; ++w) {
+        unsigned long long *f = fix_all + (w * C::NPART + i) * 2;
+        fix_add(lo, hi, f[0], (long long)f[1]);
+        f[0] = 0ull;
+        f[1] = 0ull;
+      }
+      fix_atomic_add(p.acc + ((int64_t)it * C::NPART + i) * 2, lo, hi);
     }
     named_bar_sync(1, kWarps * 32);
   };
 
   int stage = 0;
   uint32_t phase = 0;
-  for (int it = 0; it < p.iters; ++it) {
-  PanelParams pt = p;                 // per-iteration view: X^it in, X^{it+1} out, result slot it
-  pt.X = (it & 1) ? p.Xout : p.X;
-  pt.Xout = (it & 1) ? const_cast<void *>(p.X) : p.Xout;
-  pt.result = p.result + (int64_t)it * C::NPART;
-  const bool deferred = p.part_iters != nullptr && p.iters > 1;
-  if (deferred) part_base = p.part_iters + (int64_t)it * 2 * gridDim.x * C::NPART;
-  const T *Xg = static_cast<const T *>(pt.X);
-  unsigned long long *cts = (p.ts && threadIdx.x == 0) ? p.ts + ((int64_t)it * gridDim.x + blockIdx.x) * kTsSlots : nullptr;
-  bool first_stage = true;
-  if (it > 0) {
-#pragma unroll
-    for (int m = 0; m < C::DDL; ++m) {
-      const int e = lane + 32 * m;
-      if (e < C::DD) { gram1[e] = 0.0; gram2[e] = 0.0; }
+  int cur_it = -1;
+  unsigned long long *cts = nullptr;
+  for (;;) {
+    mbar_wait(&full[stage], phase);
+    const int kg = meta[stage].kg;
+    if (kg < 0) break;
+    const int it = kg / p.nunits;
+    if (it != cur_it) {
+      if (cur_it >= 0) {
+        flush(cur_it);
+        if (cts) cts[3] = globaltimer();
+      }
+      cur_it = it;
+      cts = (p.ts && threadIdx.x == 0) ? p.ts + ((int64_t)it * gridDim.x + blockIdx.x) * kTsSlots : nullptr;
+      if (cts) {
+        cts[2] = globaltimer();
+        unsigned sm;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+        cts[11] = sm;
+      }
     }
-    s_own = 0.0;
-    xb = 0.0;
-  }
-  const int64_t my_s0 = sk_bound(p.steps, gridDim.x, blockIdx.x);
-  const int64_t my_s1 = sk_bound(p.steps, gridDim.x, blockIdx.x + 1);
-  const int first_panel = (int)(my_s0 / p.total_tiles);
-  for (int64_t st = my_s0; st < my_s1;) {
-    const int panel = (int)(st / p.total_tiles);
-    const int t0 = (int)(st - (int64_t)panel * p.total_tiles);
-    const int64_t t1l = t0 + (my_s1 - st);
-    const int t1 = t1l < p.total_tiles ? (int)t1l : p.total_tiles;
-    st += t1 - t0;
-    const bool split_panel = !(t0 == 0 && t1 == p.total_tiles);
+    const int4 u = __ldg(p.units + (kg - it * p.nunits));
+    const int panel = u.x, t0 = u.y, t1 = u.z, slot = u.w;
+    PanelParams pt = p;                 // per-iteration view: X^it in, X^{it+1} out
+    pt.X = (it & 1) ? p.Xout : p.X;
+    pt.Xout = (it & 1) ? const_cast<void *>(p.X) : p.Xout;
+    const T *Xg = static_cast<const T *>(pt.X);
     const int64_t node_base = (int64_t)panel * C::NODES + warp * C::NPW;   // local node of q = 0
     const int64_t rem = p.n_local - node_base;
     const int nvalid = rem <= 0 ? 0 : (rem < C::NPW ? (int)rem : C::NPW);
     // X_i of this warp's nodes for the epilogue, in flight during the stream.  Issued after the
-    // segment's first stage has landed: X^it is only guaranteed complete (all CTAs' epilogues
-    // of it-1) once the producer passed the grid barrier and that stage's barrier completed
-    // (writers' release -> producer acquire -> mbarrier arrive/wait).  The loop's own wait on
-    // this phase then returns at once.
-    mbar_wait(&full[stage], phase);
+    // unit's first stage has landed: X^it is only guaranteed complete (every epilogue of it-1)
+    // once the producer passed its readiness wait and that stage's barrier completed (writers'
+    // release -> producer acquire -> mbarrier arrive / wait).
     T xpre[C::EPL];
     epi_load_x<T, D, C::NPW>(pt, Xg, lane, node_base, nvalid, xpre);
 
@@ -314,8 +309,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int kp = 0; kp < C::KP + KL; ++kp) acc2[r][kp] = 0ull;
       for (int t = t0; t < t1; ++t) {
-        mbar_wait(&full[stage], phase);
-        if (cts && first_stage) { cts[2] = globaltimer(); first_stage = false; }
+        if (t > t0) mbar_wait(&full[stage], phase);
         const float *As = reinterpret_cast<const float *>(smem + stage * C::STAGE_BYTES) + (warp * C::RT) * kColTile + 2 * lane;
         const float *Xt = reinterpret_cast<const float *>(smem + stage * C::STAGE_BYTES + C::A_BYTES);
         const float *Xs = Xt + 4 * lane;
@@ -380,7 +374,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int k = 0; k < D; ++k) acc[r][k] = T(0);
       for (int t = t0; t < t1; ++t) {
-        mbar_wait(&full[stage], phase);
+        if (t > t0) mbar_wait(&full[stage], phase);
         const T *As = reinterpret_cast<const T *>(smem + stage * C::STAGE_BYTES) + (warp * C::RT) * kColTile + 2 * lane;
         const T *Xs = reinterpret_cast<const T *>(smem + stage * C::STAGE_BYTES + C::A_BYTES) + 4 * lane;
         T xv[D][4];
@@ -415,61 +409,44 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
 
-    if (cts) cts[5] = globaltimer();   // streaming of this segment done
+    if (cts) cts[5] = globaltimer();   // streaming of this unit done
     // ---- reduce the lane-partial sums: every lane ends with the full B rows of the warp
 #pragma unroll
     for (int r = 0; r < C::RT; ++r)
 #pragma unroll
       for (int k = 0; k < D; ++k) acc[r][k] = warp_sum(acc[r][k]);
-    if (cts) cts[7] = globaltimer();   // lane partials reduced
 
-    if (split_panel) {
-      // partial B of this segment -> slot (CTA, first|last segment); the last covering CTA
-      // to arrive sums all segments in CTA order and runs the epilogue.
-      const int which = (panel == first_panel) ? 0 : 1;
-      T *bp = static_cast<T *>(p.Bpart) + (((int64_t)blockIdx.x * 2 + which) * kWarps + warp) * C::EP;
+    if (slot >= 0) {
+      // Split panel: publish this warp's partial rows; the last of the panel's units to arrive
+      // (counted per (panel, warp), no CTA barrier) sums all of them in column order.
+      T *bp = static_cast<T *>(p.Bpart) + ((int64_t)slot * kWarps + warp) * C::EP;
       lane0_store_rows<T, C::RT, D, true>(bp, acc, lane);
-      const int c_lo = sk_owner((int64_t)panel * p.total_tiles, p.steps, gridDim.x);
-      const int c_hi = sk_owner((int64_t)(panel + 1) * p.total_tiles - 1, p.steps, gridDim.x);
-      // release/acquire through ONE thread: the CTA barrier orders every consumer's stores
-      // before thread 0's (cumulative) fence + arrival; an acquiring fence by thread 0 then the
-      // barrier orders the partial reads after it.  (A fence in every thread serialises: ~4 us.)
-      named_bar_sync(1, kWarps * 32);
-      if (cts) cts[8] = globaltimer();   // partial stored
-      if (threadIdx.x == 0) {
+      __syncwarp();
+      const int2 pi = __ldg(p.pinfo + panel);   // (units of the panel, first slot)
+      int last = 0;
+      if (lane == 0) {
         fence_acq_rel_gpu();
-        const unsigned prev = atomicAdd(&p.panel_cnt[panel], 1u);
-        const int is_last = (prev == (unsigned)(c_hi - c_lo));
-        if (is_last) {
+        unsigned *cnt = p.ucnt + panel * kWarps + warp;
+        last = atomicAdd(cnt, 1u) == (unsigned)(pi.x - 1);
+        if (last) {
           fence_acq_rel_gpu();
-          p.panel_cnt[panel] = 0u;   // ready for the next launch
+          *cnt = 0u;   // ready for the next iteration / launch
         }
-        *flag = is_last;
       }
-      named_bar_sync(1, kWarps * 32);
-      const int last = *flag;
-      if (cts) cts[9] = globaltimer();   // arrival counted
-      named_bar_sync(1, kWarps * 32);   // everyone read flag before it is rewritten
-      if (!last) continue;
-      // Sum the covering CTAs' partials in CTA order.  A covering CTA cb > c_lo starts inside
-      // this panel (slot 0); c_lo used slot 1 iff it started in an earlier panel.  Loads are
-      // issued 4 CTAs x EPL entries at a time (independent L2 round trips), summed in order.
-      const int w2_lo = sk_bound(p.steps, gridDim.x, c_lo) < (int64_t)panel * p.total_tiles ? 1 : 0;
+      if (!__shfl_sync(0xffffffffu, last, 0)) continue;
       const T *bpr = static_cast<const T *>(p.Bpart) + (int64_t)warp * C::EP;
       T v[C::EPL];
 #pragma unroll
       for (int m = 0; m < C::EPL; ++m) v[m] = T(0);
-      for (int cb0 = c_lo; cb0 <= c_hi; cb0 += 4) {
+      for (int j0 = 0; j0 < pi.x; j0 += 4) {   // 4 slots x EPL independent loads in flight
         T part[4][C::EPL];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          const int cb = cb0 + j;
-          const int w2 = cb == c_lo ? w2_lo : 0;
-          const T *src = bpr + ((int64_t)cb * 2 + w2) * kWarps * C::EP;
+          const T *src = bpr + (int64_t)(pi.y + j0 + j) * kWarps * C::EP;
 #pragma unroll
           for (int m = 0; m < C::EPL; ++m) {
             const int e = lane + 32 * m;
-            part[j][m] = (cb <= c_hi && e < C::E) ? __ldcg(src + e) : T(0);
+            part[j][m] = (j0 + j < pi.x && e < C::E) ? __ldcg(src + e) : T(0);
           }
         }
 #pragma unroll
@@ -489,12 +466,41 @@ __global__ void __launch_bounds__(kThreads, 1)
     double g1s[C::DDL], g2s[C::DDL], so = 0.0, xs = 0.0;
     node_epilogue<T, D, C::NPW, MODE, true>(pt, Xg, lane, node_base, nvalid, sX, sG, sH, sS, sM, g1s, g2s, so, xs,
                                             ns_region, err, xpre);
-    commit(split_panel, panel, g1s, g2s, so, xs);
+    // exact partial sums of this (panel, warp) into the warp's fixed-point accumulators
+#pragma unroll
+    for (int m = 0; m < C::DDL; ++m) {
+      const int e = lane + 32 * m;
+      if (e < C::DD) {
+        unsigned long long lo;
+        long long hi;
+        fix_from(g1s[m], lo, hi, err);
+        fix_add(fixw[2 * e], *reinterpret_cast<long long *>(&fixw[2 * e + 1]), lo, hi);
+        fix_from(g2s[m], lo, hi, err);
+        fix_add(fixw[2 * (C::DD + e)], *reinterpret_cast<long long *>(&fixw[2 * (C::DD + e) + 1]), lo, hi);
+      }
+    }
+    so = warp_sum(so);
+    xs = warp_sum(xs);
+    if (lane == 0) {
+      unsigned long long lo;
+      long long hi;
+      fix_from(so, lo, hi, err);
+      fix_add(fixw[2 * (2 * C::DD)], *reinterpret_cast<long long *>(&fixw[2 * (2 * C::DD) + 1]), lo, hi);
+      fix_from(xs, lo, hi, err);
+      fix_add(fixw[2 * (2 * C::DD + 1)], *reinterpret_cast<long long *>(&fixw[2 * (2 * C::DD + 1) + 1]), lo, hi);
+    }
     __syncwarp();
+    if (p.iters > 1 && lane == 0) {   // this warp's rows of X^{it+1} are written
+      fence_acq_rel_gpu();
+      atomicAdd(&p.ctl[1], 1u);
+    }
   }
 
-  // ------------------------------------------------------------------ CTA + grid reduction
-  if (cts) cts[3] = globaltimer();   // all own segments + epilogues done
+  // ------------------------------------------------------------------ exit
+  if (cur_it >= 0) {
+    flush(cur_it);
+    if (cts) cts[3] = globaltimer();
+  }
   if (err) atomicOr(p.err, err);
   if (MODE == kModeRgs || MODE == kModeGpm) {
     float mx = ns_region;
@@ -502,60 +508,31 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     if (lane == 0 && mx > 0.f) atomicMax(p.ns_region, __float_as_uint(mx));
   }
-  s_own = warp_sum(s_own);
-  xb = warp_sum(xb);
-  if (lane == 0) { red[warp * 2] = s_own; red[warp * 2 + 1] = xb; }
   named_bar_sync(1, kWarps * 32);
-  double *cp = part_base + (int64_t)blockIdx.x * C::NPART;
-  for (int i = threadIdx.x; i < C::NPART; i += kWarps * 32) {
-    double v = 0.0;
-    if (i < 2 * C::DD) {
-      for (int w = 0; w < kWarps; ++w) v += gram_all[w * 2 * C::DD + i];
-    } else {
-      for (int w = 0; w < kWarps; ++w) v += red[w * 2 + (i - 2 * C::DD)];
-    }
-    __stcg(cp + i, v);
+  if (threadIdx.x == 0) {
+    fence_acq_rel_gpu();
+    const int is_last = atomicAdd(&p.ctl[2], 1u) == gridDim.x - 1;
+    if (is_last) fence_acq_rel_gpu();
+    *flag = is_last;
   }
-  if (!deferred) {
-    named_bar_sync(1, kWarps * 32);
+  named_bar_sync(1, kWarps * 32);
+  if (*flag) {   // last CTA out: fixed point -> fp64 results, re-zero, reset the queue counters
+    const int nval = p.iters * C::NPART;
+    for (int i = threadIdx.x; i < nval; i += kWarps * 32) {
+      unsigned long long *a = p.acc + (int64_t)i * 2;
+      const unsigned long long lo = __ldcg(a);
+      const long long hi = (long long)__ldcg(a + 1);
+      p.result[i] = fix_to(lo, hi);
+      a[0] = 0ull;
+      a[1] = 0ull;
+    }
     if (threadIdx.x == 0) {
-      fence_acq_rel_gpu();
-      const int is_last = (atomicAdd(p.done_cnt, 1u) == gridDim.x - 1);
-      if (is_last) fence_acq_rel_gpu();
-      *flag = is_last;
-    }
-    named_bar_sync(1, kWarps * 32);
-    if (*flag) {
-      reduce_slots<C::NPART>(p.cta_part, 2 * (int)gridDim.x, pt.result, warp, lane);
-      if (threadIdx.x == 0) *p.done_cnt = 0u;
+      p.ctl[0] = 0u;
+      p.ctl[1] = 0u;
+      p.ctl[2] = 0u;
     }
   }
-  if (cts) cts[4] = globaltimer();   // end-of-iteration reduction done
-  if (p.iters > 1) {   // grid barrier: this CTA's share of X^{it+1} (and partial slots) is done
-    named_bar_sync(1, kWarps * 32);
-    if (threadIdx.x == 0) {
-      fence_acq_rel_gpu();
-      atomicAdd(p.iter_cnt, 1u);
-    }
-  }
-  }  // iterations
-
-  if (p.part_iters != nullptr && p.iters > 1) {
-    // deferred objective reduction: once every CTA has arrived after the last iteration, CTA b
-    // reduces iterations b, b + G, ... (same fixed slot order as the per-iteration path).
-    if (threadIdx.x == 0) {
-      const unsigned target = (unsigned)p.iters * gridDim.x;
-      unsigned spins = 0;
-      while (ld_acquire_gpu(p.iter_cnt) < target) {
-        __nanosleep(64);
-        if (++spins > (1u << 26)) { atomicOr(p.err, kErrTimeout); break; }
-      }
-    }
-    named_bar_sync(1, kWarps * 32);
-    for (int it = blockIdx.x; it < p.iters; it += gridDim.x)
-      reduce_slots<C::NPART>(p.part_iters + (int64_t)it * 2 * gridDim.x * C::NPART, 2 * (int)gridDim.x,
-                             p.result + (int64_t)it * C::NPART, warp, lane);
-  }
+  if (cts) cts[4] = globaltimer();
 }
 
 // ------------------------------------------------------------------ host-side launchers

@@ -131,11 +131,18 @@ struct nsrgs_ctx {
   double *sym_part = nullptr;
   int nblocks = 0, nJ = 0, nI = 0, sym_grid = 0;
   int64_t a_bytes_pass = 0;
-  int64_t steps = 0;
   // scratch
   double *cta_part = nullptr;   // grid * npart
-  unsigned *counters = nullptr; // [0] done_cnt, [1..panels] panel counters, [panels+1] iteration barrier
-  bool coop = false;            // cooperative multi-iteration launches available (world == 1)
+  unsigned *counters = nullptr; // [0] done_cnt (wide kernel)
+  bool coop = false;            // multi-iteration launches available (world == 1)
+  // dense panel kernel: dynamic schedule (panel.cu)
+  int4 *units = nullptr;        // [nunits] (panel, t_begin, t_end, slot)
+  int2 *pinfo = nullptr;        // [panels] (units covering the panel, first slot)
+  int nunits = 0, nslots = 0, split_panels = 0;
+  unsigned *ucnt = nullptr;     // [panels][kWarps]
+  unsigned *ctl = nullptr;      // [4] queue head, epilogues done, CTAs exited
+  unsigned long long *acc = nullptr;   // [acc_cap][npart][2] fixed-point sums
+  int acc_cap = 0;
   void *Bpart = nullptr;
   double *res = nullptr;        // res_cap * npart
   int res_cap = 0;
@@ -150,8 +157,6 @@ struct nsrgs_ctx {
   bool emulated = false;   // test-only: world > 1 without a communicator (collectives are no-ops)
   bool forced_nccl = false; // test-only: world == 1 with a 1-rank NCCL communicator
   unsigned long long *ts = nullptr;   // debug phase timestamps (nsrgs_debug_timestamps)
-  double *part_iters = nullptr;       // deferred per-iteration partial slots [iters][2G][npart]
-  int part_iters_cap = 0;
   // stats / timing
   bool timing = false;
   std::vector<cudaEvent_t> ev;
@@ -209,7 +214,15 @@ int sync_and_check(nsrgs_ctx *c, int *flags_out = nullptr) {
   int flags = 0;
   CUDA_TRY(c, cudaMemcpyAsync(&flags, c->err, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
-  if (flags) CUDA_TRY(c, cudaMemsetAsync(c->err, 0, sizeof(int), c->stream));
+  if (flags) {
+    CUDA_TRY(c, cudaMemsetAsync(c->err, 0, sizeof(int), c->stream));
+    if (flags & kErrTimeout) {   // a timed-out launch may leave the dense kernel's counters dirty
+      if (c->ctl) CUDA_TRY(c, cudaMemsetAsync(c->ctl, 0, sizeof(unsigned) * 4, c->stream));
+      if (c->ucnt) CUDA_TRY(c, cudaMemsetAsync(c->ucnt, 0, sizeof(unsigned) * (size_t)c->panels * kWarps, c->stream));
+      if (c->acc) CUDA_TRY(c, cudaMemsetAsync(c->acc, 0, sizeof(unsigned long long) * 2 * (size_t)c->acc_cap * c->shape.npart, c->stream));
+      CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    }
+  }
   if (flags_out) *flags_out = flags;
   if (c->timing && c->ev_used) {
     for (int i = 0; i + 1 < c->ev_used; i += 2) {
@@ -219,6 +232,9 @@ int sync_and_check(nsrgs_ctx *c, int *flags_out = nullptr) {
     }
     c->ev_used = 0;
   }
+  // a caller that does not inspect the flags still must not return a result built from a
+  // non-finite partial (the fixed-point sums would hide it)
+  if (!flags_out && (flags & kErrNonfinite)) return set_err(c, NSRGS_ERR_NONFINITE, "non-finite partial sum");
   return NSRGS_OK;
 }
 
@@ -255,18 +271,49 @@ int ensure_res(nsrgs_ctx *c, int slots) {
   return NSRGS_OK;
 }
 
-// Deferred partial slots for a multi-iteration launch of `iters` iterations (zeroed once:
-// unused cut-panel slots must read zero, and every launch writes the same used slots).
-int ensure_part_iters(nsrgs_ctx *c, int iters) {
-  if (iters <= c->part_iters_cap) return NSRGS_OK;
-  if (c->part_iters) cudaFree(c->part_iters);
-  c->part_iters = nullptr;
-  c->part_iters_cap = 0;
-  const size_t bytes = sizeof(double) * (size_t)iters * 2 * c->grid * c->shape.npart;
-  CUDA_TRY(c, cudaMalloc(&c->part_iters, bytes));
-  CUDA_TRY(c, cudaMemsetAsync(c->part_iters, 0, bytes, c->stream));
-  c->part_iters_cap = iters;
+// Fixed-point accumulators of the dense kernel for `iters` iterations per launch (zeroed; the
+// kernel re-zeroes what it used).
+int ensure_acc(nsrgs_ctx *c, int iters) {
+  if (iters <= c->acc_cap) return NSRGS_OK;
+  if (c->acc) cudaFree(c->acc);
+  c->acc = nullptr;
+  c->acc_cap = 0;
+  const int cap = std::max(iters, 2 * c->acc_cap);
+  const size_t bytes = sizeof(unsigned long long) * 2 * (size_t)cap * c->shape.npart;
+  CUDA_TRY(c, cudaMalloc(&c->acc, bytes));
+  CUDA_TRY(c, cudaMemsetAsync(c->acc, 0, bytes, c->stream));
+  c->acc_cap = cap;
   return NSRGS_OK;
+}
+
+// Work-unit list of the dense kernel (fixed per context, so results are reproducible).  Whole
+// panels while more than two panels per CTA remain, then the remaining panels cut into equal
+// column ranges of >= 24 tiles (~1/64 of a CTA's share), so the dynamic queue ends with small
+// units and every SM finishes within about half a unit of the others.
+static void build_units(nsrgs_ctx *c, std::vector<int4> &units, std::vector<int2> &pinfo) {
+  const int P = c->panels, TT = c->total_tiles, G = c->sm_count;
+  double tail_panels = 2.0, unit_div = 64.0;
+  int unit_min = 24;
+  if (const char *e = std::getenv("NSRGS_UNITS")) std::sscanf(e, "%lf,%lf,%d", &tail_panels, &unit_div, &unit_min);   // tuning
+  const int whole = std::max(0, P - (int)(tail_panels * G));
+  const double per_cta = (double)P * TT / G;
+  const int unit = std::min(TT, std::max(unit_min, (int)(per_cta / unit_div)));
+  const int S = std::max(1, (TT + unit / 2) / unit);   // units per split panel
+  units.clear();
+  pinfo.assign(P, make_int2(1, -1));
+  int slot = 0;
+  for (int pnl = 0; pnl < P; ++pnl) {
+    if (pnl < whole || S == 1) {
+      units.push_back(make_int4(pnl, 0, TT, -1));
+      continue;
+    }
+    pinfo[pnl] = make_int2(S, slot);
+    for (int u = 0; u < S; ++u)
+      units.push_back(make_int4(pnl, (int)((int64_t)TT * u / S), (int)((int64_t)TT * (u + 1) / S), slot++));
+  }
+  c->nunits = (int)units.size();
+  c->nslots = slot;
+  c->split_panels = S == 1 ? 0 : P - whole;
 }
 
 int ensure_small(nsrgs_ctx *c, int64_t count) {
@@ -310,17 +357,20 @@ int build_tmap(nsrgs_ctx *c) {
 
 // One panel-kernel launch: X[src] -> out (mode), partials into res slot.
 int launch_panel(nsrgs_ctx *c, int mode, const void *Xin, void *Xout, double *result, double eta, int K,
-                 int iters = 1, double *part_iters = nullptr) {
+                 int iters = 1) {
   PanelParams p{};
   p.iters = iters;
-  p.part_iters = iters > 1 ? part_iters : nullptr;
-  p.iter_cnt = c->counters + c->panels + 1;
   p.ts = c->ts;
-  if (iters > 1) CUDA_TRY(c, cudaMemsetAsync(p.iter_cnt, 0, sizeof(unsigned), c->stream));
+  if (c->d <= kMaxNarrowD && !c->sym) NSRGS_TRY(ensure_acc(c, iters));
   p.X = Xin;
   p.Xout = Xout;
+  p.units = c->units;
+  p.pinfo = c->pinfo;
+  p.nunits = c->nunits;
   p.Bpart = c->Bpart;
-  p.panel_cnt = c->counters + 1;
+  p.ucnt = c->ucnt;
+  p.ctl = c->ctl;
+  p.acc = c->acc;
   p.cta_part = c->cta_part;
   p.done_cnt = c->counters;
   p.result = result;
@@ -335,7 +385,6 @@ int launch_panel(nsrgs_ctx *c, int mode, const void *Xin, void *Xout, double *re
   p.rank = c->rank;
   p.panels = c->panels;
   p.total_tiles = c->total_tiles;
-  p.steps = c->steps;
   p.a_keep = c->a_keep;
   p.coef = (double)(c->n - 1);
   p.eta = eta;
@@ -455,7 +504,7 @@ int nsrgs_destroy(nsrgs_ctx *c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   if (c->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(c->comm);
   for (auto e : c->ev) cudaEventDestroy(e);
-  void *bufs[] = {c->part_iters, c->ts, c->X[0], c->X[1], c->stage, c->cta_part, c->counters, c->Bpart, c->res, c->red_part, c->small,
+  void *bufs[] = {c->units, c->pinfo, c->ucnt, c->ctl, c->acc, c->ts, c->X[0], c->X[1], c->stage, c->cta_part, c->counters, c->Bpart, c->res, c->red_part, c->small,
                   c->err, c->ns_region, c->rowpart, c->colpart, c->blocks, c->sym_cnt, c->sym_part};
   for (void *b : bufs)
     if (b) cudaFree(b);
@@ -513,11 +562,13 @@ int nsrgs_create(const nsrgs_desc *desc, nsrgs_ctx **out) {
   } else {
     panel_dispatch(c->dtype, c->d, 0, true, &c->shape, nullptr, nullptr, 0, nullptr);
   }
-  // launch shape: stream-K over panels x column tiles, one persistent CTA per SM
+  // launch shape: persistent CTAs (one per SM) over a dynamic queue of work units; wide: CTA per panel
   c->panels = (int)ceil_div(c->plan.rows_local, c->shape.rows);
   c->total_tiles = (int)(c->world * c->plan.tiles_per_rank);
-  c->steps = (int64_t)c->panels * c->total_tiles;
-  c->grid = c->d > kMaxNarrowD ? c->panels : (int)std::min<int64_t>(c->steps, c->sm_count);   // wide: CTA per panel
+  std::vector<int4> units;
+  std::vector<int2> pinfo;
+  if (c->d <= kMaxNarrowD) build_units(c, units, pinfo);
+  c->grid = c->d > kMaxNarrowD ? c->panels : std::min(c->nunits, c->sm_count);
   {
     int l2 = 0;
     cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, c->device);
@@ -540,10 +591,19 @@ int nsrgs_create(const nsrgs_desc *desc, nsrgs_ctx **out) {
   const size_t xb = c->esz * (size_t)c->plan.x_elems;
   bool ok = alloc(&c->X[0], xb) && alloc(&c->X[1], xb) && alloc(&c->stage, c->esz * (size_t)(c->n * c->d * c->d)) &&
             alloc((void **)&c->cta_part, sizeof(double) * (size_t)c->grid * 2 * c->shape.npart) &&
-            alloc((void **)&c->counters, sizeof(unsigned) * (c->panels + 2)) &&
+            alloc((void **)&c->counters, sizeof(unsigned) * 4) &&
             alloc((void **)&c->err, sizeof(int)) && alloc((void **)&c->ns_region, sizeof(unsigned));
-  if (ok) ok = alloc(&c->Bpart, c->esz * (size_t)c->grid * 2 * (c->shape.rows * c->d + 4 * 8));   // per-warp slots padded to 16 B
+  if (ok && c->d <= kMaxNarrowD) {
+    ok = alloc((void **)&c->units, sizeof(int4) * units.size()) && alloc((void **)&c->pinfo, sizeof(int2) * pinfo.size()) &&
+         alloc((void **)&c->ucnt, sizeof(unsigned) * (size_t)c->panels * kWarps) &&
+         alloc((void **)&c->ctl, sizeof(unsigned) * 4) &&
+         alloc(&c->Bpart, c->esz * (size_t)std::max(1, c->nslots) * (c->shape.rows * c->d + 4 * 8));   // per-warp rows padded to 16 B
+    if (ok) ok = cudaMemcpyAsync(c->units, units.data(), sizeof(int4) * units.size(), cudaMemcpyHostToDevice, c->stream) == cudaSuccess &&
+                 cudaMemcpyAsync(c->pinfo, pinfo.data(), sizeof(int2) * pinfo.size(), cudaMemcpyHostToDevice, c->stream) == cudaSuccess &&
+                 cudaStreamSynchronize(c->stream) == cudaSuccess;
+  }
   if (!ok) return bail(NSRGS_ERR_OOM, "device allocation failed");
+  if (c->d <= kMaxNarrowD && ensure_acc(c, 1)) return bail(NSRGS_ERR_OOM);
   if (ensure_res(c, 128) || ensure_small(c, kSmallOut + 256)) return bail(NSRGS_ERR_OOM);
   // Test-only (NSRGS_FORCE_NCCL=1, world == 1): run every collective through a real 1-rank
   // NCCL communicator so the NCCL plumbing is exercised on a single GPU.
@@ -700,6 +760,7 @@ int nsrgs_init_spectral(nsrgs_ctx *c, uint64_t seed, int max_sweeps, double tol,
     int flags = 0;
     NSRGS_TRY(sync_and_check(c, &flags));
     if (flags & kErrSingular) return set_err(c, NSRGS_ERR_SINGULAR, "Cholesky of Y^T Y failed at sweep %d", sweeps);
+    if (flags & kErrNonfinite) return set_err(c, NSRGS_ERR_NONFINITE, "non-finite Gram partial at sweep %d", sweeps);
     if (!std::isfinite(chg2)) return set_err(c, NSRGS_ERR_NONFINITE, "non-finite subspace change at sweep %d", sweeps);
     const double chg = std::sqrt(chg2);
     if (sweeps >= 2 && chg < tol) { converged = true; break; }
@@ -732,6 +793,7 @@ static int check_run_flags(nsrgs_ctx *c, int flags) {
     return set_err(c, NSRGS_ERR_DIVERGENCE, "Newton-Schulz retraction diverged (||S||_F > 10 sqrt(d) or non-finite)");
   if (flags & kErrSingular)
     return set_err(c, NSRGS_ERR_SINGULAR, "GPM: Newton-Schulz sign of B_i did not converge (rank-deficient block)");
+  if (flags & kErrNonfinite) return set_err(c, NSRGS_ERR_NONFINITE, "non-finite objective / Gram partial");
   return NSRGS_OK;
 }
 
@@ -744,17 +806,8 @@ static int run_impl(nsrgs_ctx *c, int mode, int T, double eta, int K, double *tr
   if (c->coop && !c->sym && T > 1) {
     // one persistent cooperative launch for all T iterations (grid barrier between them, A
     // prefetched across the boundary) — removes launch gaps and pipeline drains
-    // The objective partials of every iteration are reduced once at the end of the launch
-    // (part_iters); launches are chunked so that buffer stays under ~128 MB.
-    const size_t per_iter = sizeof(double) * 2 * (size_t)c->grid * c->shape.npart;
-    const int chunk = (int)std::max<size_t>(2, std::min<size_t>((size_t)T, ((size_t)128 << 20) / per_iter));
-    NSRGS_TRY(ensure_part_iters(c, chunk));
-    for (int t0 = 0; t0 < T; t0 += chunk) {
-      const int Ti = std::min(chunk, T - t0);
-      NSRGS_TRY(launch_panel(c, mode, c->X[c->cur], c->X[1 - c->cur], c->res + (size_t)t0 * c->shape.npart, eta,
-                             K, Ti, c->part_iters));
-      if (Ti & 1) c->cur = 1 - c->cur;
-    }
+    NSRGS_TRY(launch_panel(c, mode, c->X[c->cur], c->X[1 - c->cur], c->res, eta, K, T));
+    if (T & 1) c->cur = 1 - c->cur;
   } else {
     for (int t = 0; t < T; ++t) {
       NSRGS_TRY(launch_panel(c, mode, c->X[c->cur], c->X[1 - c->cur], c->res + (size_t)t * c->shape.npart, eta, K));
@@ -975,13 +1028,7 @@ int nsrgs_get_stats(nsrgs_ctx *c, nsrgs_stats_t *o) {
   o->threads = c->shape.threads;
   o->stages = c->shape.stages;
   o->rows_per_panel = c->shape.rows;
-  int cut = 0;
-  int64_t last_panel = -1;
-  for (int b = 1; b < c->grid; ++b) {
-    const int64_t sb = c->steps * b / c->grid;
-    if (sb % c->total_tiles && sb / c->total_tiles != last_panel) { ++cut; last_panel = sb / c->total_tiles; }
-  }
-  o->cut_panels = cut;
+  o->cut_panels = c->split_panels;
   o->panels = c->panels;
   o->smem_bytes = c->shape.smem;
   o->panel_ms_total = c->panel_ms;

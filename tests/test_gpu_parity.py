@@ -204,6 +204,10 @@ def test_divergence_and_state_errors(nsrgs):
     with pytest.raises(nsrgs.NSRGSError) as e:
         s.step(1.0 / n, 3)
     assert e.value.name in ("DIVERGENCE", "NONFINITE")
+    s.set_X(bad)
+    with pytest.raises(nsrgs.NSRGSError) as e:       # objective partials of a non-finite X
+        s.objective()
+    assert e.value.name == "NONFINITE"
     s.close()
 
 
