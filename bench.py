@@ -323,7 +323,9 @@ def run_gpu(args, cfg):
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (on-device Philox instance, PAPER.md §4.1 model)",
         "config": {**_config_dict(args, cfg, world), "init_sweeps": sweeps,
-                   "storage": "symmetric half (upper triangle read)" if args.symmetric else "dense row-major shard"},
+                   "storage": "symmetric half (upper triangle read)" if args.symmetric else "dense row-major shard",
+                   "x_exchange": ("fused P2P NVLink stores from the epilogue" if st.get("p2p") else "NCCL all-gather")
+                   if world > 1 else "none (1 GPU)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "peak_kind": peak_kind, "kernel": "panel_kernel (fused A.X + epilogue)",
                      "bytes_per_launch": bytes_launch, "avg_launch_ms": avg_ms,

@@ -205,17 +205,28 @@ typedef struct {
   double a_fro2;                /* ||A||_F^2 (global)                                           */
   int32_t symmetric;            /* 1 if the symmetric half-storage pass is active               */
   int64_t a_bytes_per_pass;     /* A bytes one pass requests from memory (full shard or ~half)  */
+  int32_t p2p;                  /* 1 if X^{t+1} is exchanged by the fused NVLink-store path     */
 } nsrgs_stats_t;
 int nsrgs_get_stats(nsrgs_ctx *ctx, nsrgs_stats_t *out);
 int nsrgs_reset_stats(nsrgs_ctx *ctx, int enable_panel_timing);
 
 /* Debug: per-CTA phase timestamps (%globaltimer, ns) of the dense panel kernel.  max_iters > 0
- * arms a [max_iters][grid][16] buffer for the following launches (slots: 0 producer start,
- * 1 X ready after the iteration barrier, 2 first stage consumed, 3 work + epilogues done,
- * 4 iteration reduction done, 5 last segment streamed, 6 its B rows complete, 7..10 cut-panel
- * hand-off sub-steps; unused slots 0); max_iters == 0 copies it to out_host (host, may be NULL) and
- * disarms. */
+ * arms a [max_iters][grid][16] buffer for the following launches (slots, per iteration: 0
+ * producer's first unit, 1 X ready after the readiness wait, 2 consumers' first unit,
+ * 3 partial sums flushed, 4 CTA exit, 5 last unit streamed, 6 its B rows complete, 11 SM id;
+ * unused slots 0); max_iters == 0 copies it to out_host (host, may be NULL) and disarms. */
 int nsrgs_debug_timestamps(nsrgs_ctx *ctx, int max_iters, unsigned long long *out_host);
+
+/* Test-only: link `world` rank contexts created in ONE process with NSRGS_EMULATE_RANKS=1 (no
+ * communicator) so that the fused P2P X exchange runs between them on one GPU: each rank's
+ * epilogue stores X^{t+1} into every linked rank's buffer and bumps its arrival counters.  The
+ * caller must step the ranks one after another (rank 0..world-1 for iteration t, then t+1):
+ * a launch only waits for counters the previous round already completed, so no kernel ever
+ * waits on another.  ctxs[r] must be rank r of the same (n, d, dtype), d <= 10.  Returns
+ * INVALID_ARG otherwise.  Real multi-GPU contexts set this path up in nsrgs_create (CUDA IPC
+ * mapping of every peer's X buffers over NVLink, verified by a write handshake; NCCL
+ * all-gather fallback if any rank cannot map a peer; NSRGS_P2P=0 forces the fallback). */
+int nsrgs_debug_link_peers(nsrgs_ctx **ctxs, int world);
 
 #ifdef __cplusplus
 }

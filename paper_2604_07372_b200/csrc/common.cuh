@@ -11,6 +11,7 @@ constexpr int kColTile = 128;      // X/A column tile (elements); one float4/dou
 constexpr int kTsSlots = 16;   // debug timestamp slots per CTA per iteration
 constexpr int kWarps = 7;          // consumer warps per panel CTA (7 + producer = 8 warps: 2 per SMSP, 255 regs)
 constexpr int kThreads = 32 * (kWarps + 1);   // + 1 TMA producer warp
+constexpr int kMaxWorld = 8;       // ranks of one NVSwitch box (fused P2P exchange)
 
 // ------------------------------------------------------------------------------------------
 // Launch parameters of the panel kernel (panel.cu).  Plain struct, passed by value.
@@ -47,6 +48,16 @@ struct PanelParams {
   // (t odd) and writes the other; X^t is complete once ctl[1] >= t * panels * kWarps
   int iters;
   unsigned long long *ts;   // optional phase timestamps [iters][grid][kTsSlots] (%globaltimer ns), debug
+  // ---- P > 1 fused X exchange over NVLink (dense kernel, RGS / GPM, one iteration per launch):
+  // the epilogue also stores its X^{t+1} rows into every rank's Xout (peer_X[g], IPC-mapped);
+  // at exit each CTA adds its count of (panel, warp) epilogues to every rank's arrival counter
+  // for this rank (peer_cnt[g] + rank) after a system-scope release; the producer reads rank
+  // g's slice of X^t only once xcnt[g] >= xtarget (its acquire).  Replaces the all-gather.
+  int p2p;
+  unsigned xtarget;
+  const unsigned *xcnt;
+  void *peer_X[kMaxWorld];
+  unsigned *peer_cnt[kMaxWorld];
 };
 
 // Symmetric half-storage pass (sym.cu): blocks of GP panels x kSymTilesPerBlock column tiles.
@@ -206,6 +217,15 @@ __device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned *p) {
   return v;
 }
 // generic-proxy writes (other CTAs' X^{t+1} stores, acquired above) before async-proxy reads
+__device__ __forceinline__ unsigned ld_acquire_sys(const unsigned *p) {
+  unsigned v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void fence_acq_rel_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
+__device__ __forceinline__ void red_add_sys(unsigned *p, unsigned v) {
+  asm volatile("red.relaxed.sys.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }

@@ -300,7 +300,11 @@ __device__ __forceinline__ void node_epilogue(const PanelParams &p, const T *Xg,
         const int q = e / DD, a = (e / D) % D, b = e % D;
         if (q < nvalid) {
           const int64_t c = (p.node0 + node_base + q) * D + a;
-          Xo[tile_index(c, b, D, p.rows_local, p.tiles_per_rank)] = sS[e];
+          const int64_t idx = tile_index(c, b, D, p.rows_local, p.tiles_per_rank);
+          Xo[idx] = sS[e];
+          if (p.p2p)   // fused exchange: the same rows into every peer's X^{t+1} (NVLink stores)
+            for (int g = 0; g < p.world; ++g)
+              if (g != p.rank) static_cast<T *>(p.peer_X[g])[idx] = sS[e];
         }
       }
     }

@@ -17,6 +17,8 @@ struct PanelShape {
 cudaError_t panel_dispatch(int dtype, int d, int mode, bool shape_only, PanelShape *shape,
                            const CUtensorMap *tm, const PanelParams *p, int grid, cudaStream_t s);
 
+cudaError_t launch_p2p_wait(const unsigned *xcnt, int world, unsigned target, int *err, cudaStream_t s);
+
 // wide.cu: d > 10 (one node per warp, lane = component).
 bool wide_supported(int d);
 cudaError_t wide_dispatch(int d, int mode, bool shape_only, PanelShape *shape, const CUtensorMap *tm,

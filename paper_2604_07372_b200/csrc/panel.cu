@@ -163,6 +163,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       reinterpret_cast<unsigned long long *>(reinterpret_cast<uint8_t *>(scr_all) + C::SCR_T_BYTES);   // [kWarps][NPART][2]
   UnitMeta *meta = reinterpret_cast<UnitMeta *>(fix_all + kWarps * C::NPART * 2);                     // [8]
   int *flag = reinterpret_cast<int *>(meta + 8);
+  unsigned *epi_tot = reinterpret_cast<unsigned *>(flag + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -171,6 +172,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&empty[s], kWarps);
     }
     fence_mbar_init();
+    *epi_tot = 0u;
   }
   for (int i = threadIdx.x; i < kWarps * C::NPART * 2; i += kThreads) fix_all[i] = 0ull;
   __syncthreads();
@@ -186,6 +188,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       int ready_it = 0;   // X^it known complete for it <= ready_it
+      unsigned slice_ready = 0u;   // P2P: rank slices of X^0 known complete
       int ts_it = -1;
       for (;;) {
         const int kg = (int)atomicAdd(&p.ctl[0], 1u);
@@ -209,6 +212,17 @@ __global__ void __launch_bounds__(kThreads, 1)
           uint8_t *sb = smem + stage * C::STAGE_BYTES;
           mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
           tma_load_3d(sb, &tmA, &full[stage], jt * kColTile, g, u.x * C::ROWS, pol_a);
+          if (p.p2p && !((slice_ready >> g) & 1u)) {
+            // fused exchange: rank g's slice of X^t is complete once all its (panel, warp)
+            // epilogues of the previous iteration have been counted here
+            unsigned spins = 0;
+            while (ld_acquire_sys(p.xcnt + g) < p.xtarget) {
+              __nanosleep(128);
+              if (++spins > (1u << 26)) { atomicOr(p.err, kErrTimeout); break; }
+            }
+            fence_proxy_async_global();
+            slice_ready |= 1u << g;
+          }
           if (it > ready_it) {
             // A of this unit is in flight; X^it needs every (panel, warp) epilogue of it-1
             const unsigned target = (unsigned)it * epi_per_iter;
@@ -238,6 +252,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   unsigned long long *fixw = fix_all + warp * C::NPART * 2;   // this warp's fixed-point sums
   float ns_region = 0.f;
   int err = 0;
+  unsigned n_epi = 0;   // (panel, warp) epilogues run by this warp (P2P arrival count)
 
   // CTA-wide: add the warps' fixed-point sums of iteration `it` to the global accumulators.
   // All consumer warps process the same unit sequence, so they all reach this together.
@@ -490,6 +505,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       fix_add(fixw[2 * (2 * C::DD + 1)], *reinterpret_cast<long long *>(&fixw[2 * (2 * C::DD + 1) + 1]), lo, hi);
     }
     __syncwarp();
+    ++n_epi;
     if (p.iters > 1 && lane == 0) {   // this warp's rows of X^{it+1} are written
       fence_acq_rel_gpu();
       atomicAdd(&p.ctl[1], 1u);
@@ -508,8 +524,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     if (lane == 0 && mx > 0.f) atomicMax(p.ns_region, __float_as_uint(mx));
   }
+  if (p.p2p && lane == 0 && n_epi) atomicAdd(epi_tot, n_epi);
   named_bar_sync(1, kWarps * 32);
   if (threadIdx.x == 0) {
+    if (p.p2p && *epi_tot) {
+      // every consumer's X^{t+1} stores (local and remote) precede the barrier; one
+      // system-scope release, then this CTA's epilogue count to every rank's counter[rank]
+      fence_acq_rel_sys();
+      for (int g = 0; g < p.world; ++g) red_add_sys(p.peer_cnt[g] + p.rank, *epi_tot);
+    }
     fence_acq_rel_gpu();
     const int is_last = atomicAdd(&p.ctl[2], 1u) == gridDim.x - 1;
     if (is_last) fence_acq_rel_gpu();
@@ -533,6 +556,22 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
   if (cts) cts[4] = globaltimer();
+}
+
+// End of a fused-exchange run: every peer's stores into this rank's X buffers have landed once
+// all arrival counters reached `target` (so the host may reuse / overwrite X afterwards).
+__global__ void p2p_wait_kernel(const unsigned *xcnt, int world, unsigned target, int *err) {
+  if (threadIdx.x < world) {
+    unsigned spins = 0;
+    while (ld_acquire_sys(xcnt + threadIdx.x) < target) {
+      __nanosleep(256);
+      if (++spins > (1u << 26)) { atomicOr(err, kErrTimeout); break; }
+    }
+  }
+}
+cudaError_t launch_p2p_wait(const unsigned *xcnt, int world, unsigned target, int *err, cudaStream_t s) {
+  p2p_wait_kernel<<<1, 32, 0, s>>>(xcnt, world, target, err);
+  return cudaGetLastError();
 }
 
 // ------------------------------------------------------------------ host-side launchers

@@ -64,6 +64,10 @@ using EncodeTiledFn = CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_
                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
 int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+// arrival counters [kMaxWorld] (then handshake words [kMaxWorld]) after X0 | X1 in an xblock
+unsigned *xcnt_of(void *block, size_t xstride) {
+  return reinterpret_cast<unsigned *>(static_cast<char *>(block) + 2 * xstride);
+}
 
 int plan_impl(int64_t n, int32_t d, int32_t world, int32_t rank, nsrgs_plan_t *out, std::string *why) {
   auto fail = [&](const char *m) {
@@ -114,7 +118,14 @@ struct nsrgs_ctx {
   CUtensorMap tmA;
   double a_fro2 = 0.0;
   // iterate
-  void *X[2] = {nullptr, nullptr};
+  void *X[2] = {nullptr, nullptr};   // both inside xblock (one IPC-shareable allocation)
+  void *xblock = nullptr;            // [X0 | X1 | xcnt[kMaxWorld] | hello[kMaxWorld]]
+  size_t xstride = 0;                // bytes from X0 to X1 (and X1 to xcnt)
+  // fused P2P exchange (world > 1): peers' xblock mapped into this process
+  bool p2p = false;
+  void *peer_block[kMaxWorld] = {};
+  bool peer_opened[kMaxWorld] = {};
+  unsigned p2p_epoch = 0;            // P2P iterations completed on this context (all ranks in lockstep)
   int cur = 0;
   bool have_X = false;
   void *stage = nullptr;   // n*d*d elements (host<->device staging for set/get/Z)
@@ -357,9 +368,19 @@ int build_tmap(nsrgs_ctx *c) {
 
 // One panel-kernel launch: X[src] -> out (mode), partials into res slot.
 int launch_panel(nsrgs_ctx *c, int mode, const void *Xin, void *Xout, double *result, double eta, int K,
-                 int iters = 1) {
+                 int iters = 1, bool p2p = false) {
   PanelParams p{};
   p.iters = iters;
+  if (p2p) {   // fused exchange (one iteration per launch): see PanelParams
+    const size_t off = static_cast<char *>(Xout) - static_cast<char *>(c->xblock);
+    p.p2p = 1;
+    p.xtarget = c->p2p_epoch * (unsigned)c->panels * (unsigned)kWarps;
+    p.xcnt = xcnt_of(c->xblock, c->xstride);
+    for (int g = 0; g < c->world; ++g) {
+      p.peer_X[g] = static_cast<char *>(c->peer_block[g]) + off;
+      p.peer_cnt[g] = xcnt_of(c->peer_block[g], c->xstride);
+    }
+  }
   p.ts = c->ts;
   if (c->d <= kMaxNarrowD && !c->sym) NSRGS_TRY(ensure_acc(c, iters));
   p.X = Xin;
@@ -498,13 +519,84 @@ static thread_local std::string g_create_msg;
 
 const char *nsrgs_last_error(const nsrgs_ctx *ctx) { return ctx ? ctx->msg.c_str() : g_create_msg.c_str(); }
 
+// Fused-exchange setup, collective over the communicator (world > 1, not emulated): map every
+// peer's xblock with CUDA IPC and prove each mapping with a write handshake.  Any failure on any
+// rank leaves every rank on the NCCL all-gather path (same decision everywhere).
+static int setup_p2p(nsrgs_ctx *c) {
+  const char *env = getenv("NSRGS_P2P");
+  bool ok = c->world <= kMaxWorld && c->d <= kMaxNarrowD && !(env && env[0] == '0');
+  constexpr int kH = (int)sizeof(cudaIpcMemHandle_t);   // 64 bytes
+  char *dh = nullptr;   // [world][kH] handles, then one double for the agreement sums
+  CUDA_TRY(c, cudaMalloc(&dh, (size_t)kH * c->world + 16));
+  cudaIpcMemHandle_t mine{};
+  if (ok) ok = cudaIpcGetMemHandle(&mine, c->xblock) == cudaSuccess;
+  cudaGetLastError();
+  std::vector<cudaIpcMemHandle_t> all(c->world);
+  double *flag = reinterpret_cast<double *>(dh + (size_t)kH * c->world);
+  int rc = NSRGS_OK;
+  auto agree = [&](bool mine_ok, bool *all_ok) -> int {   // all ranks ok?
+    const double bad = mine_ok ? 0.0 : 1.0;
+    CUDA_TRY(c, cudaMemcpyAsync(flag, &bad, sizeof bad, cudaMemcpyHostToDevice, c->stream));
+    NCCL_TRY(c, g_nccl.AllReduce(flag, flag, 1, ncclFloat64, ncclSum, c->comm, c->stream));
+    double tot = 0.0;
+    CUDA_TRY(c, cudaMemcpyAsync(&tot, flag, sizeof tot, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    *all_ok = tot == 0.0;
+    return NSRGS_OK;
+  };
+  do {
+    CUDA_TRY(c, cudaMemcpyAsync(dh + (size_t)kH * c->rank, &mine, kH, cudaMemcpyHostToDevice, c->stream));
+    NCCL_TRY(c, g_nccl.AllGather(dh + (size_t)kH * c->rank, dh, kH, ncclInt8, c->comm, c->stream));
+    CUDA_TRY(c, cudaMemcpyAsync(all.data(), dh, (size_t)kH * c->world, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    bool all_ok = false;
+    if ((rc = agree(ok, &all_ok)) != NSRGS_OK) break;
+    if (!all_ok) { ok = false; break; }
+    for (int g = 0; g < c->world && ok; ++g) {
+      if (g == c->rank) { c->peer_block[g] = c->xblock; continue; }
+      ok = cudaIpcOpenMemHandle(&c->peer_block[g], all[g], cudaIpcMemLazyEnablePeerAccess) == cudaSuccess;
+      c->peer_opened[g] = ok;
+    }
+    cudaGetLastError();
+    // handshake: write a token into every peer's hello[rank], barrier, check our hello[]
+    const unsigned token = 0x5EED0000u;
+    for (int g = 0; g < c->world && ok; ++g) {
+      if (g == c->rank) continue;
+      const unsigned v = token + (unsigned)c->rank;
+      unsigned *hello = xcnt_of(c->peer_block[g], c->xstride) + kMaxWorld;
+      ok = cudaMemcpy(hello + c->rank, &v, sizeof v, cudaMemcpyHostToDevice) == cudaSuccess;
+    }
+    cudaGetLastError();
+    if ((rc = agree(ok, &all_ok)) != NSRGS_OK) break;   // also the barrier after the writes
+    if (!all_ok) { ok = false; break; }
+    unsigned hello[kMaxWorld] = {};
+    CUDA_TRY(c, cudaMemcpy(hello, xcnt_of(c->xblock, c->xstride) + kMaxWorld, sizeof(unsigned) * c->world,
+                           cudaMemcpyDeviceToHost));
+    for (int g = 0; g < c->world; ++g)
+      if (g != c->rank && hello[g] != token + (unsigned)g) ok = false;
+    if ((rc = agree(ok, &all_ok)) != NSRGS_OK) break;
+    ok = all_ok;
+  } while (false);
+  cudaFree(dh);
+  if (rc != NSRGS_OK) return rc;
+  if (!ok) {
+    for (int g = 0; g < kMaxWorld; ++g)
+      if (c->peer_opened[g]) cudaIpcCloseMemHandle(c->peer_block[g]);
+    for (int g = 0; g < kMaxWorld; ++g) { c->peer_opened[g] = false; c->peer_block[g] = nullptr; }
+  }
+  c->p2p = ok;
+  return NSRGS_OK;
+}
+
 int nsrgs_destroy(nsrgs_ctx *c) {
   if (!c) return NSRGS_OK;
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   if (c->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(c->comm);
   for (auto e : c->ev) cudaEventDestroy(e);
-  void *bufs[] = {c->units, c->pinfo, c->ucnt, c->ctl, c->acc, c->ts, c->X[0], c->X[1], c->stage, c->cta_part, c->counters, c->Bpart, c->res, c->red_part, c->small,
+  for (int g = 0; g < kMaxWorld; ++g)
+    if (c->peer_opened[g]) cudaIpcCloseMemHandle(c->peer_block[g]);
+  void *bufs[] = {c->units, c->pinfo, c->ucnt, c->ctl, c->acc, c->ts, c->xblock, c->stage, c->cta_part, c->counters, c->Bpart, c->res, c->red_part, c->small,
                   c->err, c->ns_region, c->rowpart, c->colpart, c->blocks, c->sym_cnt, c->sym_part};
   for (void *b : bufs)
     if (b) cudaFree(b);
@@ -589,7 +681,13 @@ int nsrgs_create(const nsrgs_desc *desc, nsrgs_ctx **out) {
     return cudaMemsetAsync(*p, 0, bytes, c->stream) == cudaSuccess;
   };
   const size_t xb = c->esz * (size_t)c->plan.x_elems;
-  bool ok = alloc(&c->X[0], xb) && alloc(&c->X[1], xb) && alloc(&c->stage, c->esz * (size_t)(c->n * c->d * c->d)) &&
+  c->xstride = (xb + 255) / 256 * 256;
+  bool ok = alloc(&c->xblock, 2 * c->xstride + 2 * sizeof(unsigned) * kMaxWorld);
+  if (ok) {
+    c->X[0] = c->xblock;
+    c->X[1] = static_cast<char *>(c->xblock) + c->xstride;
+  }
+  ok = ok && alloc(&c->stage, c->esz * (size_t)(c->n * c->d * c->d)) &&
             alloc((void **)&c->cta_part, sizeof(double) * (size_t)c->grid * 2 * c->shape.npart) &&
             alloc((void **)&c->counters, sizeof(unsigned) * 4) &&
             alloc((void **)&c->err, sizeof(int)) && alloc((void **)&c->ns_region, sizeof(unsigned));
@@ -618,6 +716,10 @@ int nsrgs_create(const nsrgs_desc *desc, nsrgs_ctx **out) {
       std::memcpy(&id, desc->nccl_unique_id, sizeof id);
     }
     if (g_nccl.CommInitRank(&c->comm, c->world, id, c->rank) != ncclSuccess) return bail(NSRGS_ERR_NCCL, "ncclCommInitRank failed");
+    if (c->world > 1) {
+      const int r = setup_p2p(c);
+      if (r != NSRGS_OK) return bail(r, c->msg.c_str());
+    }
   }
   {
     int coop = 0;
@@ -803,7 +905,23 @@ static int run_impl(nsrgs_ctx *c, int mode, int T, double eta, int K, double *tr
     return set_err(c, NSRGS_ERR_INVALID_ARG, "run: need T >= 0, K >= 0, eta > 0");
   if (T == 0) return NSRGS_OK;
   NSRGS_TRY(ensure_res(c, T));
-  if (c->coop && !c->sym && T > 1) {
+  if (c->p2p && !c->sym) {
+    // fused exchange: peers' X^{t+1} rows arrive by NVLink stores from their epilogues; no
+    // all-gather.  Barrier first: every rank has finished its earlier work on its X buffers.
+    if (!c->emulated) NSRGS_TRY(allreduce_sum(c, c->small + kSmallChg, 1));
+    for (int t = 0; t < T; ++t) {
+      NSRGS_TRY(launch_panel(c, mode, c->X[c->cur], c->X[1 - c->cur], c->res + (size_t)t * c->shape.npart, eta, K,
+                             1, true));
+      c->p2p_epoch++;
+      c->cur = 1 - c->cur;
+    }
+    // every peer's stores into this rank's buffers have landed before the call returns
+    if (!c->emulated) {
+      CUDA_TRY(c, launch_p2p_wait(xcnt_of(c->xblock, c->xstride), c->world,
+                                  c->p2p_epoch * (unsigned)c->panels * (unsigned)kWarps, c->err, c->stream));
+      c->kernel_launches++;
+    }
+  } else if (c->coop && !c->sym && T > 1) {
     // one persistent cooperative launch for all T iterations (grid barrier between them, A
     // prefetched across the boundary) — removes launch gaps and pipeline drains
     NSRGS_TRY(launch_panel(c, mode, c->X[c->cur], c->X[1 - c->cur], c->res, eta, K, T));
@@ -1022,6 +1140,27 @@ int nsrgs_debug_timestamps(nsrgs_ctx *c, int max_iters, unsigned long long *out_
   return NSRGS_OK;
 }
 
+int nsrgs_debug_link_peers(nsrgs_ctx **ctxs, int world) {
+  if (!ctxs || world < 2 || world > kMaxWorld) return NSRGS_ERR_INVALID_ARG;
+  for (int r = 0; r < world; ++r) {
+    nsrgs_ctx *c = ctxs[r];
+    if (!c || !c->emulated || c->world != world || c->rank != r || c->n != ctxs[0]->n || c->d != ctxs[0]->d ||
+        c->dtype != ctxs[0]->dtype || c->d > kMaxNarrowD || c->device != ctxs[0]->device)
+      return c ? set_err(c, NSRGS_ERR_INVALID_ARG, "link_peers: need emulated ranks 0..world-1 of one instance, d <= 10")
+               : NSRGS_ERR_INVALID_ARG;
+  }
+  for (int r = 0; r < world; ++r) {
+    nsrgs_ctx *c = ctxs[r];
+    NSRGS_TRY(enter(c));
+    NSRGS_TRY(sync_and_check(c));
+    for (int g = 0; g < world; ++g) c->peer_block[g] = ctxs[g]->xblock;
+    CUDA_TRY(c, cudaMemset(xcnt_of(c->xblock, c->xstride), 0, sizeof(unsigned) * kMaxWorld));
+    c->p2p = true;
+    c->p2p_epoch = 0;
+  }
+  return NSRGS_OK;
+}
+
 int nsrgs_get_stats(nsrgs_ctx *c, nsrgs_stats_t *o) {
   if (!c || !o) return NSRGS_ERR_INVALID_ARG;
   o->grid = c->grid;
@@ -1038,6 +1177,7 @@ int nsrgs_get_stats(nsrgs_ctx *c, nsrgs_stats_t *o) {
   o->a_fro2 = c->a_fro2;
   o->symmetric = c->sym ? 1 : 0;
   o->a_bytes_per_pass = c->sym ? c->a_bytes_pass : (int64_t)c->esz * c->plan.rows_local * c->N;
+  o->p2p = c->p2p ? 1 : 0;
   return NSRGS_OK;
 }
 

@@ -46,7 +46,7 @@ class Stats(ct.Structure):
                 ("rows_per_panel", ct.c_int32), ("cut_panels", ct.c_int32), ("panels", ct.c_int64),
                 ("smem_bytes", ct.c_int64), ("panel_ms_total", ct.c_double), ("panel_launches", ct.c_int64),
                 ("kernel_launches", ct.c_int64), ("ns_region_max", ct.c_double), ("a_fro2", ct.c_double),
-                ("symmetric", ct.c_int32), ("a_bytes_per_pass", ct.c_int64)]
+                ("symmetric", ct.c_int32), ("a_bytes_per_pass", ct.c_int64), ("p2p", ct.c_int32)]
 
 
 _P = ct.c_void_p
@@ -76,6 +76,7 @@ _SIGS = {
     "nsrgs_get_stats": ([_P, ct.POINTER(Stats)], ct.c_int),
     "nsrgs_set_symmetric": ([_P, ct.c_int], ct.c_int),
     "nsrgs_debug_timestamps": ([_P, ct.c_int, _P], ct.c_int),
+    "nsrgs_debug_link_peers": ([_P, ct.c_int], ct.c_int),
     "nsrgs_reset_stats": ([_P, ct.c_int], ct.c_int),
 }
 for _name, (_args, _res) in _SIGS.items():
@@ -92,6 +93,14 @@ def _np_dtype(dtype: int):
 
 def version() -> int:
     return _lib.nsrgs_version()
+
+
+def link_peers(solvers) -> None:
+    """Test-only (NSRGS_EMULATE_RANKS=1): fused P2P exchange between rank contexts of one process."""
+    arr = (_P * len(solvers))(*[s._h.value for s in solvers])
+    rc = _lib.nsrgs_debug_link_peers(arr, len(solvers))
+    if rc != 0:
+        raise NSRGSError(rc, (_lib.nsrgs_last_error(solvers[0]._h) or b"").decode())
 
 
 def plan(n: int, d: int, world: int = 1, rank: int = 0) -> dict:

@@ -662,3 +662,61 @@ def test_multi_iteration_launch_bitwise_equals_per_iteration_launches(nsrgs, mon
     (a, b, c, e), (a1, b1, c1, e1) = outs
     assert np.array_equal(a, a1) and np.array_equal(b, b1)
     assert np.array_equal(c, c1) and np.array_equal(e, e1)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,d,world,dtype", [(64, 2, 2, "f32"), (160, 5, 4, "f32"), (8000, 4, 8, "f32"),
+                                             (96, 3, 2, "f64"), (400, 10, 4, "f32")])
+def test_fused_p2p_exchange_rank_by_rank(nsrgs, monkeypatch, n, d, world, dtype):
+    """Fused X exchange (P > 1): each rank's epilogue stores X^{t+1} into every rank's buffer and
+    bumps their arrival counters; the producer reads rank g's slice only once g's count is
+    complete.  Emulated ranks of one process are linked (nsrgs_debug_link_peers) and stepped one
+    after another, so every wait is already satisfied when a launch starts.  After T steps
+    every rank must hold the same full X^T, equal to the single-GPU iteration; same for GPM."""
+    monkeypatch.setenv("NSRGS_EMULATE_RANKS", "1")
+    dt = nsrgs.F32 if dtype == "f32" else nsrgs.F64
+    tol = 1e-6 if dtype == "f32" else 1e-12
+    sigma, K, T = 0.7, 3, 4
+    Z = inst.ground_truth(6, n, d)
+    X = oracle_iterate_near(Z, 0.1, 5)
+    full = nsrgs.Solver(n, d, dtype=dt)
+    full.generate(6, sigma, want_Z=False)
+    full.set_X(X.astype(full.np_dtype))
+    full.run(T, 1.0 / n, K, trace=False)
+    Xref = full.get_X()
+    full.gpm_run(2, trace=False)
+    Xref_gpm = full.get_X()
+    full.close()
+    ranks = [nsrgs.Solver(n, d, dtype=dt, rank=r, world=world) for r in range(world)]
+    for s in ranks:
+        s.generate(6, sigma, want_Z=False)
+        s.set_X(X.astype(s.np_dtype))
+        assert s.stats()["p2p"] == 0
+    nsrgs.link_peers(ranks)
+    assert all(s.stats()["p2p"] == 1 for s in ranks)
+    for _ in range(T):
+        for s in ranks:
+            s.step(1.0 / n, K)
+    Xs = [s.get_X() for s in ranks]
+    for Xr in Xs[1:]:
+        assert np.array_equal(Xr, Xs[0])
+    assert rel_fro(Xs[0], Xref) <= tol
+    for _ in range(2):
+        for s in ranks:
+            s.gpm_run(1, trace=False)
+    Xg = [s.get_X() for s in ranks]
+    for Xr in Xg[1:]:
+        assert np.array_equal(Xr, Xg[0])
+    assert rel_fro(Xg[0], Xref_gpm) <= tol
+    for s in ranks:
+        s.close()
+
+
+def test_link_peers_rejects_non_emulated(nsrgs):
+    s0 = nsrgs.Solver(64, 2)
+    s1 = nsrgs.Solver(64, 2)
+    with pytest.raises(nsrgs.NSRGSError) as e:
+        nsrgs.link_peers([s0, s1])
+    assert e.value.name == "INVALID_ARG"
+    s0.close()
+    s1.close()
