@@ -41,8 +41,10 @@ __device__ __forceinline__ void epi_load_x(const PanelParams &p, const T *Xg, in
 }
 
 // XPRE: the caller passes the epi_load_x registers in xpre (else they are loaded here).
+// Xout: where X^{t+1} (RGS / GPM) or W (PRODUCT) goes (explicit: the panel kernel alternates
+// buffers per iteration without copying its parameter block).
 template <typename T, int D, int NPW, int MODE, bool XPRE = false>
-__device__ __forceinline__ void node_epilogue(const PanelParams &p, const T *Xg, int lane, int64_t node_base,
+__device__ __forceinline__ void node_epilogue(const PanelParams &p, const T *Xg, void *Xout, int lane, int64_t node_base,
                                               int nvalid, T *sX, T *sG, T *sH, T *sS, T *sM,
                                               double (&g1s)[(D * D + 31) / 32], double (&g2s)[(D * D + 31) / 32],
                                               double &so, double &xs, float &ns_region, int &err,
@@ -68,7 +70,7 @@ __device__ __forceinline__ void node_epilogue(const PanelParams &p, const T *Xg,
 
   if constexpr (MODE == kModeProduct) {
     // W = A Y rows -> Xout; Gram partials W^T W and Y^T W (Cholesky-QR of the sweep).
-    T *Wout = static_cast<T *>(p.Xout);
+    T *Wout = static_cast<T *>(Xout);
 #pragma unroll
     for (int m = 0; m < EPL; ++m) {
       const int e = lane + 32 * m;
@@ -292,7 +294,7 @@ __device__ __forceinline__ void node_epilogue(const PanelParams &p, const T *Xg,
       for (int e2 = 0; e2 < DD; ++e2) f2 += (double)Sq[e2] * (double)Sq[e2];
       if (!(f2 <= 100.0 * D)) err |= kErrDivergence;
     }
-    T *Xo = static_cast<T *>(p.Xout);
+    T *Xo = static_cast<T *>(Xout);
 #pragma unroll
     for (int m = 0; m < EPL; ++m) {
       const int e = lane + 32 * m;

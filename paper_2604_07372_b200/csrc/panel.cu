@@ -149,7 +149,7 @@ struct UnitMeta {   // published by the producer per stage: global unit index (-
 // units to arrive (per warp) sums them in column order and runs the epilogue for its nodes.
 template <typename T, int D, int MODE>
 __global__ void __launch_bounds__(kThreads, 1)
-    panel_kernel(const __grid_constant__ CUtensorMap tmA, const PanelParams p) {
+    panel_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ PanelParams p) {
   using C = PanelCfg<T, D>;
   using V = typename Vec4<T>::type;
   extern __shared__ uint8_t smem_raw[];
@@ -297,10 +297,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     const int4 u = __ldg(p.units + (kg - it * p.nunits));
     const int panel = u.x, t0 = u.y, t1 = u.z, slot = u.w;
-    PanelParams pt = p;                 // per-iteration view: X^it in, X^{it+1} out
-    pt.X = (it & 1) ? p.Xout : p.X;
-    pt.Xout = (it & 1) ? const_cast<void *>(p.X) : p.Xout;
-    const T *Xg = static_cast<const T *>(pt.X);
+    // iteration it reads X^it and writes X^{it+1} (buffers alternate; no parameter copy)
+    const T *Xg = static_cast<const T *>((it & 1) ? p.Xout : p.X);
+    void *Xo_it = (it & 1) ? const_cast<void *>(p.X) : p.Xout;
     const int64_t node_base = (int64_t)panel * C::NODES + warp * C::NPW;   // local node of q = 0
     const int64_t rem = p.n_local - node_base;
     const int nvalid = rem <= 0 ? 0 : (rem < C::NPW ? (int)rem : C::NPW);
@@ -309,7 +308,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // once the producer passed its readiness wait and that stage's barrier completed (writers'
     // release -> producer acquire -> mbarrier arrive / wait).
     T xpre[C::EPL];
-    epi_load_x<T, D, C::NPW>(pt, Xg, lane, node_base, nvalid, xpre);
+    epi_load_x<T, D, C::NPW>(p, Xg, lane, node_base, nvalid, xpre);
 
     // Lane l owns columns {2l, 2l+1, 64+2l, 65+2l} of each 128-column tile: A row pieces are
     // conflict-free 64-bit smem loads, X component pairs conflict-free 128-bit loads.
@@ -479,7 +478,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (cts) cts[6] = globaltimer();   // B rows of the panel complete (combine done)
     // ---- per-node epilogue (epilogue.cuh), entry-parallel in warp-private smem.
     double g1s[C::DDL], g2s[C::DDL], so = 0.0, xs = 0.0;
-    node_epilogue<T, D, C::NPW, MODE, true>(pt, Xg, lane, node_base, nvalid, sX, sG, sH, sS, sM, g1s, g2s, so, xs,
+    node_epilogue<T, D, C::NPW, MODE, true>(p, Xg, Xo_it, lane, node_base, nvalid, sX, sG, sH, sS, sM, g1s, g2s, so, xs,
                                             ns_region, err, xpre);
     // exact partial sums of this (panel, warp) into the warp's fixed-point accumulators
 #pragma unroll

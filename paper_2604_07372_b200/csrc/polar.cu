@@ -33,7 +33,7 @@ __global__ void __launch_bounds__(128) polar_warp_kernel(const PanelParams p) {
   double g1s[DDL], g2s[DDL], so = 0.0, xs = 0.0;
   float nsr = 0.f;
   int err = 0;
-  node_epilogue<T, D, C::NPW, kModeGpm>(p, Y, lane, node_base, nvalid, sX, sG, sH, sS, sM, g1s, g2s, so, xs, nsr, err);
+  node_epilogue<T, D, C::NPW, kModeGpm>(p, Y, p.Xout, lane, node_base, nvalid, sX, sG, sH, sS, sM, g1s, g2s, so, xs, nsr, err);
   if (err) atomicOr(p.err, err);
 }
 

@@ -400,7 +400,7 @@ __global__ void __launch_bounds__(256)
   double g1s[DDL], g2s[DDL], so = 0.0, xs = 0.0;
   float ns_region = 0.f;
   int err = 0;
-  node_epilogue<float, D, C::NPW, MODE>(sp.e, static_cast<const float *>(sp.e.X), lane, node_base, nvalid, sX, sG,
+  node_epilogue<float, D, C::NPW, MODE>(sp.e, static_cast<const float *>(sp.e.X), sp.e.Xout, lane, node_base, nvalid, sX, sG,
                                         sH, sS, sM, g1s, g2s, so, xs, ns_region, err);
   if (err) atomicOr(sp.e.err, err);
   {

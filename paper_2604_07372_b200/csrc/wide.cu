@@ -136,7 +136,7 @@ __global__ void __launch_bounds__(WideCfg<D>::THREADS, 1)
   double g1s[C::DDL], g2s[C::DDL], so = 0.0, xs = 0.0;
   float ns_region = 0.f;
   int err = 0;
-  node_epilogue<float, D, 1, MODE>(p, Xg, lane, node, nvalid, sX, sG, sH, sS, sM, g1s, g2s, so, xs, ns_region, err);
+  node_epilogue<float, D, 1, MODE>(p, Xg, p.Xout, lane, node, nvalid, sX, sG, sH, sS, sM, g1s, g2s, so, xs, ns_region, err);
   if (err) atomicOr(p.err, err);
   if (lane == 0 && ns_region > 0.f) atomicMax(p.ns_region, __float_as_uint(ns_region));
 
