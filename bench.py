@@ -307,6 +307,42 @@ def run_gpu(args, cfg):
                        "achieved_gbs": (a_sym + 4 * N * d + 4 * rows_local * d) / (avg2 / 1e3) / 1e9,
                        "rel_err": met_sym[0], "clocks": clk2.summary(),
                        "note": "upper-triangle stream, 2 FMA directions per element (FFMA2/issue-bound, not HBM-bound)"}
+    # §8(f) row 2 alongside: incomplete observations (p < 1) on block-sparse
+    # storage — the same (n, d, sigma, T, K) with each pair observed with probability p,
+    # mu = 1/(np); only observed blocks are stored and streamed
+    bsr_variant = None
+    if world == 1 and args.bsr_p > 0 and not args.no_bsr_variant:
+        pb = args.bsr_p
+        sb = nsrgs.Solver(n, d, nsrgs.F32, device=local, stream=stream)
+        Zb = torch.from_numpy(sb.generate(0, cfg["sigma"], p=pb, storage="bsr")).to(f"cuda:{local}")
+
+        def solve_b():
+            sb.init_spectral(0, INIT_MAX_SWEEPS, INIT_TOL, allow_unconverged=True)
+            sb.run(T, 1.0 / (n * pb), K, trace=True)
+            return sb.alignment_error(Zb)
+
+        for _ in range(max(1, args.warmup - 1)):
+            solve_b()
+        sb.reset_stats(timing=True)
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            met_b = solve_b()
+        e1.record(stream)
+        barrier()
+        ms_b = e0.elapsed_time(e1)
+        stb = sb.stats()
+        avgb = stb["panel_ms_total"] / max(1, stb["panel_launches"])
+        bsr_variant = {"p": pb, "value": T * args.steps / (ms_b / 1e3), "unit": "it/s", "ms_per_step": ms_b / args.steps,
+                       "avg_pass_ms": avgb, "stored_bytes_per_pass": stb["a_bytes_per_pass"],
+                       "dense_bytes_per_pass": 4 * rows_local * N, "nnzb": stb["bsr_nnzb"],
+                       "achieved_gbs": stb["a_bytes_per_pass"] / (avgb / 1e3) / 1e9,
+                       "frac_of_peak": stb["a_bytes_per_pass"] / (avgb / 1e3) / 1e9 / _peaks()[0],
+                       "rel_err": met_b[0], "rel_err_first_order": cfg["sigma"] * np.sqrt((d - 1) / (n * pb)),
+                       "kernel": "bsr_kernel (warp per node row: bulk-copied A chunks, gathered X_j records, "
+                                 "fused epilogue)"}
+        sb.close()
     if rank != 0:
         s.close()
         return
@@ -349,6 +385,8 @@ def run_gpu(args, cfg):
         line["cpu_baseline"] = cpu
     if sym_variant:
         line["symmetric_variant"] = sym_variant
+    if bsr_variant:
+        line["bsr_variant"] = bsr_variant
     print(json.dumps(line), flush=True)
     s.close()
     if world > 1:
@@ -367,6 +405,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--symmetric", action="store_true", help="symmetric half-storage pass (d <= 6, 1 GPU)")
     ap.add_argument("--no-sym-variant", action="store_true", help="skip the extra symmetric-variant measurement")
+    ap.add_argument("--bsr-p", type=float, default=0.5, help="observation probability of the block-sparse variant")
+    ap.add_argument("--no-bsr-variant", action="store_true", help="skip the block-sparse (p < 1) variant")
     args = ap.parse_args()
     if args.config is None:
         args.config = "c3"

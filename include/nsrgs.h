@@ -133,6 +133,27 @@ int nsrgs_generate(nsrgs_ctx *ctx, uint64_t seed, double sigma, void *Z_out_host
  * shrink).  Use eta = 1/(n p) in nsrgs_run.  p in (0, 1]. */
 int nsrgs_generate_observed(nsrgs_ctx *ctx, uint64_t seed, double sigma, double p, void *Z_out_host);
 
+/* Block-sparse (BSR) storage of an incompletely observed instance (
+ * PAPER.md:300-310 §4.1: each pair {i, j} observed with probability p, unobserved A_ij = 0;
+ * use eta = 1/(n p)).  Only observed blocks are stored, so an A pass reads ~p
+ * of the dense bytes.  Layout (device, library-OWNED after generate, BORROWED after attach):
+ *   rowptr[n_local + 1] (int64): local node row il owns blocks [rowptr[il], rowptr[il+1]);
+ *   col[nnzb] (int32): global node j of block b (ascending within a row; a row may end with
+ *                      zero blocks whose col is the row's own node — the generator pads each
+ *                      row to a multiple of 4 blocks);
+ *   vals[nnzb][d][d] (float, row-major): A_{node0+il, col[b]}.
+ * The diagonal block A_ii must not be stored unless it is zero.
+ * nsrgs_generate_observed_bsr builds the SAME instance as nsrgs_generate_observed (same
+ * counters; every stored block is bitwise the dense block; the dense shard is released).
+ * F32 contexts, every supported d, any world.  nsrgs_set_symmetric and nsrgs_copy_A_rows
+ * return NSRGS_ERR_STATE while block-sparse storage is active; a dense generate / attach
+ * switches back.  nsrgs_get_A_bsr copies the arrays to host (each pointer nullable;
+ * *nnzb_out receives nnzb). */
+int nsrgs_generate_observed_bsr(nsrgs_ctx *ctx, uint64_t seed, double sigma, double p, void *Z_out_host);
+int nsrgs_attach_A_bsr(nsrgs_ctx *ctx, const int64_t *rowptr_dev, const int32_t *col_dev, const void *vals_dev,
+                       int64_t nnzb);
+int nsrgs_get_A_bsr(nsrgs_ctx *ctx, int64_t *nnzb_out, int64_t *rowptr_host, int32_t *col_host, void *vals_host);
+
 /* Copy rows [row0, row0+nrows) of THIS rank's A shard (local row index) to host `out`
  * (nrows x n d, dense).  Diagnostic / sampled-parity helper. */
 int nsrgs_copy_A_rows(nsrgs_ctx *ctx, int64_t row0, int64_t nrows, void *out_host);
@@ -204,8 +225,11 @@ typedef struct {
   double ns_region_max;         /* max over nodes of ||I - F_i^T F_i||_F seen since reset        */
   double a_fro2;                /* ||A||_F^2 (global)                                           */
   int32_t symmetric;            /* 1 if the symmetric half-storage pass is active               */
-  int64_t a_bytes_per_pass;     /* A bytes one pass requests from memory (full shard or ~half)  */
+  int64_t a_bytes_per_pass;     /* A bytes one pass requests from memory (full shard, ~half for
+                                   the symmetric pass; values + col + rowptr for block-sparse)    */
   int32_t p2p;                  /* 1 if X^{t+1} is exchanged by the fused NVLink-store path     */
+  int32_t bsr;                  /* 1 if the block-sparse storage is active                      */
+  int64_t bsr_nnzb;             /* stored blocks of this rank (incl. zero padding blocks)       */
 } nsrgs_stats_t;
 int nsrgs_get_stats(nsrgs_ctx *ctx, nsrgs_stats_t *out);
 int nsrgs_reset_stats(nsrgs_ctx *ctx, int enable_panel_timing);

@@ -73,6 +73,17 @@ struct SymParams {
   int64_t N;
 };
 
+// Block-sparse storage of an incompletely observed instance (bsr.cu):
+// local node row il owns blocks [rowptr[il], rowptr[il+1]) (a multiple of 4, zero-padded),
+// block b = A_{node0+il, col[b]} at vals + b*d*d (row-major d x d).
+struct BsrParams {
+  PanelParams e;          // epilogue + partial-reduction fields (X, Xout, n_local, coef, eta, K, ...)
+  const int64_t *rowptr;  // [n_local + 1]
+  const int *col;         // [nnzb] global block column (node) j
+  const float *vals;      // [nnzb][d][d]
+  const float *Xs;        // d <= 10: padded node-major copy of X^t (bsr_xs_stride(d) floats per node)
+};
+
 constexpr int kErrDivergence = 1;   // ||S||_F > 10 sqrt(d) or non-finite after NS
 constexpr int kErrSingular = 2;     // init polar did not converge / Cholesky failed
 constexpr int kErrNonfinite = 4;

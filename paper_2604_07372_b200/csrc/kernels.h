@@ -31,6 +31,19 @@ struct SymShape {
 cudaError_t sym_dispatch(int d, int mode, bool shape_only, SymShape *shape, const CUtensorMap *tm, const SymParams *sp,
                          int grid, cudaStream_t s);
 
+// bsr.cu: block-sparse storage (fp32, any supported d).
+int bsr_xs_stride(int d);
+int bsr_grid(int d, int64_t n_local);
+cudaError_t bsr_dispatch(int d, int mode, const BsrParams *bp, cudaStream_t s);
+cudaError_t launch_bsr_pack_x(int d, const void *X, float *Xs, int64_t n, int64_t rows_local, int64_t tpr,
+                              cudaStream_t s);
+cudaError_t launch_bsr_count(int64_t n, int64_t node0, int64_t n_local, uint64_t seed, double p_obs, int64_t *cnt,
+                             int64_t *rowptr, cudaStream_t s);
+cudaError_t launch_bsr_fill(int d, int64_t n, int64_t node0, int64_t n_local, uint64_t seed, double sigma, double p_obs,
+                            const double *Z64, const int64_t *rowptr, int *col, float *vals, double *part,
+                            cudaStream_t s);
+cudaError_t launch_bsr_sumsq(const float *vals, int64_t count, double *part, int *nblocks, cudaStream_t s);
+
 // aux.cu
 cudaError_t launch_gen_Z(int dtype, int d, int64_t n, uint64_t seed, double *Z64, void *Zt, cudaStream_t s);
 cudaError_t launch_gen_A(int dtype, int d, int64_t n, int64_t node0, int64_t n_local, uint64_t seed,

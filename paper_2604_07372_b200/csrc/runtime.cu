@@ -142,6 +142,15 @@ struct nsrgs_ctx {
   double *sym_part = nullptr;
   int nblocks = 0, nJ = 0, nI = 0, sym_grid = 0;
   int64_t a_bytes_pass = 0;
+  // block-sparse storage (bsr.cu)
+  bool bsr = false, own_bsr = false;
+  int64_t *bsr_rowptr = nullptr;
+  int *bsr_col = nullptr;
+  float *bsr_vals = nullptr;
+  int64_t bsr_nnzb = 0;
+  float *bsr_xs = nullptr;        // padded node-major X copy (d <= 10)
+  double *bsr_part = nullptr;     // [bsr grid][npart]
+  unsigned *bsr_cnt = nullptr;    // [0] last-CTA counter
   // scratch
   double *cta_part = nullptr;   // grid * npart
   unsigned *counters = nullptr; // [0] done_cnt (wide kernel)
@@ -382,7 +391,7 @@ int launch_panel(nsrgs_ctx *c, int mode, const void *Xin, void *Xout, double *re
     }
   }
   p.ts = c->ts;
-  if (c->d <= kMaxNarrowD && !c->sym) NSRGS_TRY(ensure_acc(c, iters));
+  if (c->d <= kMaxNarrowD && !c->sym && !c->bsr) NSRGS_TRY(ensure_acc(c, iters));
   p.X = Xin;
   p.Xout = Xout;
   p.units = c->units;
@@ -418,7 +427,21 @@ int launch_panel(nsrgs_ctx *c, int mode, const void *Xin, void *Xout, double *re
     }
     CUDA_TRY(c, cudaEventRecord(c->ev[c->ev_used], c->stream));
   }
-  if (c->sym) {
+  if (c->bsr) {
+    BsrParams bp{};
+    bp.e = p;
+    bp.e.cta_part = c->bsr_part;
+    bp.e.done_cnt = c->bsr_cnt;
+    bp.rowptr = c->bsr_rowptr;
+    bp.col = c->bsr_col;
+    bp.vals = c->bsr_vals;
+    if (c->d <= kMaxNarrowD) {   // X^t -> padded node-major records for the per-lane gathers
+      CUDA_TRY(c, launch_bsr_pack_x(c->d, Xin, c->bsr_xs, c->n, c->plan.rows_local, c->plan.tiles_per_rank, c->stream));
+      c->kernel_launches++;
+      bp.Xs = c->bsr_xs;
+    }
+    CUDA_TRY(c, bsr_dispatch(c->d, mode, &bp, c->stream));
+  } else if (c->sym) {
     SymParams sp{};
     sp.e = p;
     sp.e.cta_part = c->sym_part;
@@ -464,6 +487,35 @@ int fro2_finish(nsrgs_ctx *c, int nblocks) {
   NSRGS_TRY(allreduce_sum(c, c->small + kSmallFro, 1));
   CUDA_TRY(c, cudaMemcpyAsync(&c->a_fro2, c->small + kSmallFro, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   NSRGS_TRY(sync_and_check(c));
+  return NSRGS_OK;
+}
+
+// Leave block-sparse storage (a dense A is being attached / generated).
+void drop_bsr(nsrgs_ctx *c) {
+  if (c->own_bsr) {
+    cudaFree(c->bsr_rowptr);
+    cudaFree(c->bsr_col);
+    cudaFree(c->bsr_vals);
+  }
+  c->bsr_rowptr = nullptr;
+  c->bsr_col = nullptr;
+  c->bsr_vals = nullptr;
+  c->own_bsr = false;
+  c->bsr = false;
+  c->bsr_nnzb = 0;
+}
+
+// Scratch of the block-sparse pass: padded X copy (d <= 10), per-CTA partial slots, counter.
+int bsr_scratch(nsrgs_ctx *c) {
+  if (c->d <= kMaxNarrowD && !c->bsr_xs)
+    CUDA_TRY(c, cudaMalloc(&c->bsr_xs, sizeof(float) * (size_t)c->n * bsr_xs_stride(c->d)));
+  if (!c->bsr_part)
+    CUDA_TRY(c, cudaMalloc(&c->bsr_part, sizeof(double) * (size_t)bsr_grid(c->d, c->plan.n_local) * c->shape.npart));
+  if (!c->bsr_cnt) {
+    CUDA_TRY(c, cudaMalloc(&c->bsr_cnt, 4 * sizeof(unsigned)));
+    CUDA_TRY(c, cudaMemsetAsync(c->bsr_cnt, 0, 4 * sizeof(unsigned), c->stream));
+  }
+  c->a_bytes_pass = c->bsr_nnzb * (int64_t)(c->d * c->d * 4 + 4) + 8 * (c->plan.n_local + 1);
   return NSRGS_OK;
 }
 
@@ -597,10 +649,16 @@ int nsrgs_destroy(nsrgs_ctx *c) {
   for (int g = 0; g < kMaxWorld; ++g)
     if (c->peer_opened[g]) cudaIpcCloseMemHandle(c->peer_block[g]);
   void *bufs[] = {c->units, c->pinfo, c->ucnt, c->ctl, c->acc, c->ts, c->xblock, c->stage, c->cta_part, c->counters, c->Bpart, c->res, c->red_part, c->small,
-                  c->err, c->ns_region, c->rowpart, c->colpart, c->blocks, c->sym_cnt, c->sym_part};
+                  c->err, c->ns_region, c->rowpart, c->colpart, c->blocks, c->sym_cnt, c->sym_part,
+                  c->bsr_xs, c->bsr_part, c->bsr_cnt};
   for (void *b : bufs)
     if (b) cudaFree(b);
   if (c->own_A && c->A) cudaFree(c->A);
+  if (c->own_bsr) {
+    cudaFree(c->bsr_rowptr);
+    cudaFree(c->bsr_col);
+    cudaFree(c->bsr_vals);
+  }
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   delete c;
   return NSRGS_OK;
@@ -736,6 +794,7 @@ int nsrgs_attach_A(nsrgs_ctx *c, const void *A_shard_dev, int64_t lda) {
   NSRGS_TRY(enter(c));
   if (!A_shard_dev || lda < c->N || (lda * (int64_t)c->esz) % 16 || (reinterpret_cast<uintptr_t>(A_shard_dev) % 16))
     return set_err(c, NSRGS_ERR_INVALID_ARG, "attach_A: need non-NULL 16-byte aligned A, lda >= n d, lda*esz %% 16 == 0");
+  drop_bsr(c);
   if (c->own_A && c->A) cudaFree(c->A);
   c->A = const_cast<void *>(A_shard_dev);
   c->lda = lda;
@@ -758,6 +817,7 @@ int nsrgs_generate_observed(nsrgs_ctx *c, uint64_t seed, double sigma, double p_
   NSRGS_TRY(enter(c));
   if (!(sigma >= 0.0) || !std::isfinite(sigma)) return set_err(c, NSRGS_ERR_INVALID_ARG, "sigma must be finite, >= 0");
   if (!(p_obs > 0.0 && p_obs <= 1.0)) return set_err(c, NSRGS_ERR_INVALID_ARG, "p must be in (0, 1]");
+  drop_bsr(c);
   const int64_t align = 16 / (int64_t)c->esz;
   const int64_t lda = ceil_div(c->N, align) * align;
   if (!(c->own_A && c->A && c->lda == lda)) {
@@ -794,10 +854,103 @@ int nsrgs_generate_observed(nsrgs_ctx *c, uint64_t seed, double sigma, double p_
 int nsrgs_copy_A_rows(nsrgs_ctx *c, int64_t row0, int64_t nrows, void *out_host) {
   NSRGS_TRY(enter(c));
   if (!c->have_A) return set_err(c, NSRGS_ERR_STATE, "no A");
+  if (c->bsr) return set_err(c, NSRGS_ERR_STATE, "copy_A_rows: A is block-sparse (use nsrgs_get_A_bsr)");
   if (!out_host || row0 < 0 || nrows < 0 || row0 + nrows > c->plan.rows_local)
     return set_err(c, NSRGS_ERR_INVALID_ARG, "copy_A_rows: bad range");
   CUDA_TRY(c, cudaMemcpy2DAsync(out_host, c->esz * c->N, static_cast<char *>(c->A) + c->esz * row0 * c->lda,
                                 c->esz * c->lda, c->esz * c->N, nrows, cudaMemcpyDeviceToHost, c->stream));
+  return sync_and_check(c);
+}
+
+int nsrgs_generate_observed_bsr(nsrgs_ctx *c, uint64_t seed, double sigma, double p_obs, void *Z_out_host) {
+  NSRGS_TRY(enter(c));
+  if (c->dtype != NSRGS_F32) return set_err(c, NSRGS_ERR_INVALID_ARG, "block-sparse storage: F32 only");
+  if (!(sigma >= 0.0) || !std::isfinite(sigma)) return set_err(c, NSRGS_ERR_INVALID_ARG, "sigma must be finite, >= 0");
+  if (!(p_obs > 0.0 && p_obs <= 1.0)) return set_err(c, NSRGS_ERR_INVALID_ARG, "p must be in (0, 1]");
+  drop_bsr(c);
+  if (c->own_A && c->A) cudaFree(c->A);   // the dense shard is not needed any more
+  c->A = nullptr;
+  c->own_A = false;
+  c->have_A = false;
+  c->sym = false;
+  const int64_t nl = c->plan.n_local, DD = (int64_t)c->d * c->d;
+  double *Z64 = nullptr;
+  int64_t *cnt = nullptr;
+  CUDA_TRY(c, cudaMalloc(&Z64, sizeof(double) * (size_t)(c->n * DD)));
+  CUDA_TRY(c, cudaMalloc(&cnt, sizeof(int64_t) * (size_t)nl));
+  CUDA_TRY(c, cudaMalloc(&c->bsr_rowptr, sizeof(int64_t) * (size_t)(nl + 1)));
+  c->own_bsr = true;
+  CUDA_TRY(c, launch_gen_Z(c->dtype, c->d, c->n, seed, Z64, Z_out_host ? c->stage : nullptr, c->stream));
+  CUDA_TRY(c, launch_bsr_count(c->n, c->plan.node0, nl, seed, p_obs, cnt, c->bsr_rowptr, c->stream));
+  c->kernel_launches += (Z_out_host ? 2 : 1) + 2;
+  int64_t nnzb = 0;
+  CUDA_TRY(c, cudaMemcpyAsync(&nnzb, c->bsr_rowptr + nl, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+  NSRGS_TRY(sync_and_check(c));
+  cudaError_t e1 = cudaMalloc(&c->bsr_col, sizeof(int) * (size_t)std::max<int64_t>(nnzb, 1));
+  cudaError_t e2 = cudaMalloc(&c->bsr_vals, sizeof(float) * (size_t)std::max<int64_t>(nnzb * DD, 1));
+  if (e1 != cudaSuccess || e2 != cudaSuccess) {
+    cudaFree(Z64);
+    cudaFree(cnt);
+    drop_bsr(c);
+    return set_err(c, NSRGS_ERR_OOM, "block-sparse A: cannot allocate %lld blocks", (long long)nnzb);
+  }
+  c->bsr_nnzb = nnzb;
+  NSRGS_TRY(ensure_red(c, std::max<int64_t>(nl, 1)));
+  CUDA_TRY(c, launch_bsr_fill(c->d, c->n, c->plan.node0, nl, seed, sigma, p_obs, Z64, c->bsr_rowptr, c->bsr_col,
+                              c->bsr_vals, c->red_part, c->stream));
+  c->kernel_launches++;
+  if (Z_out_host)
+    CUDA_TRY(c, cudaMemcpyAsync(Z_out_host, c->stage, c->esz * (size_t)(c->n * DD), cudaMemcpyDeviceToHost, c->stream));
+  int st = fro2_finish(c, (int)nl);
+  cudaFree(Z64);
+  cudaFree(cnt);
+  if (st) return st;
+  NSRGS_TRY(bsr_scratch(c));
+  c->bsr = true;
+  c->have_A = true;
+  return sync_and_check(c);
+}
+
+int nsrgs_attach_A_bsr(nsrgs_ctx *c, const int64_t *rowptr_dev, const int32_t *col_dev, const void *vals_dev,
+                       int64_t nnzb) {
+  NSRGS_TRY(enter(c));
+  if (c->dtype != NSRGS_F32) return set_err(c, NSRGS_ERR_INVALID_ARG, "block-sparse storage: F32 only");
+  if (!rowptr_dev || nnzb < 0 || (nnzb > 0 && (!col_dev || !vals_dev)) || (reinterpret_cast<uintptr_t>(vals_dev) % 4))
+    return set_err(c, NSRGS_ERR_INVALID_ARG, "attach_A_bsr: need rowptr, col, vals (4-byte aligned), nnzb >= 0");
+  drop_bsr(c);
+  if (c->own_A && c->A) cudaFree(c->A);
+  c->A = nullptr;
+  c->own_A = false;
+  c->sym = false;
+  c->bsr_rowptr = const_cast<int64_t *>(rowptr_dev);
+  c->bsr_col = const_cast<int *>(col_dev);
+  c->bsr_vals = static_cast<float *>(const_cast<void *>(vals_dev));
+  c->bsr_nnzb = nnzb;
+  int nb = 0;
+  NSRGS_TRY(ensure_red(c, 1024));
+  CUDA_TRY(c, launch_bsr_sumsq(c->bsr_vals, nnzb * c->d * c->d, c->red_part, &nb, c->stream));
+  c->kernel_launches++;
+  NSRGS_TRY(fro2_finish(c, nb));
+  NSRGS_TRY(bsr_scratch(c));
+  c->bsr = true;
+  c->have_A = true;
+  return sync_and_check(c);
+}
+
+int nsrgs_get_A_bsr(nsrgs_ctx *c, int64_t *nnzb_out, int64_t *rowptr_host, int32_t *col_host, void *vals_host) {
+  NSRGS_TRY(enter(c));
+  if (!c->bsr) return set_err(c, NSRGS_ERR_STATE, "get_A_bsr: A is not block-sparse");
+  if (nnzb_out) *nnzb_out = c->bsr_nnzb;
+  const int64_t DD = (int64_t)c->d * c->d;
+  if (rowptr_host)
+    CUDA_TRY(c, cudaMemcpyAsync(rowptr_host, c->bsr_rowptr, sizeof(int64_t) * (size_t)(c->plan.n_local + 1),
+                                cudaMemcpyDeviceToHost, c->stream));
+  if (col_host && c->bsr_nnzb)
+    CUDA_TRY(c, cudaMemcpyAsync(col_host, c->bsr_col, sizeof(int) * (size_t)c->bsr_nnzb, cudaMemcpyDeviceToHost,
+                                c->stream));
+  if (vals_host && c->bsr_nnzb)
+    CUDA_TRY(c, cudaMemcpyAsync(vals_host, c->bsr_vals, sizeof(float) * (size_t)(c->bsr_nnzb * DD),
+                                cudaMemcpyDeviceToHost, c->stream));
   return sync_and_check(c);
 }
 
@@ -905,7 +1058,7 @@ static int run_impl(nsrgs_ctx *c, int mode, int T, double eta, int K, double *tr
     return set_err(c, NSRGS_ERR_INVALID_ARG, "run: need T >= 0, K >= 0, eta > 0");
   if (T == 0) return NSRGS_OK;
   NSRGS_TRY(ensure_res(c, T));
-  if (c->p2p && !c->sym) {
+  if (c->p2p && !c->sym && !c->bsr) {
     // fused exchange: peers' X^{t+1} rows arrive by NVLink stores from their epilogues; no
     // all-gather.  Barrier first: every rank has finished its earlier work on its X buffers.
     if (!c->emulated) NSRGS_TRY(allreduce_sum(c, c->small + kSmallChg, 1));
@@ -921,7 +1074,7 @@ static int run_impl(nsrgs_ctx *c, int mode, int T, double eta, int K, double *tr
                                   c->p2p_epoch * (unsigned)c->panels * (unsigned)kWarps, c->err, c->stream));
       c->kernel_launches++;
     }
-  } else if (c->coop && !c->sym && T > 1) {
+  } else if (c->coop && !c->sym && !c->bsr && T > 1) {
     // one persistent cooperative launch for all T iterations (grid barrier between them, A
     // prefetched across the boundary) — removes launch gaps and pipeline drains
     NSRGS_TRY(launch_panel(c, mode, c->X[c->cur], c->X[1 - c->cur], c->res, eta, K, T));
@@ -1061,6 +1214,7 @@ int nsrgs_set_symmetric(nsrgs_ctx *c, int enable) {
   }
   if (c->world != 1 || c->dtype != NSRGS_F32 || c->d > 6)
     return set_err(c, NSRGS_ERR_INVALID_ARG, "symmetric storage: world == 1, F32, d in [2, 6] only");
+  if (c->bsr) return set_err(c, NSRGS_ERR_STATE, "symmetric storage needs the dense A (block-sparse A is active)");
   if (c->sym) return NSRGS_OK;
   CUDA_TRY(c, sym_dispatch(c->d, 0, true, &c->symshape, nullptr, nullptr, 0, nullptr));
   if (c->symshape.rows != c->shape.rows)
@@ -1176,7 +1330,9 @@ int nsrgs_get_stats(nsrgs_ctx *c, nsrgs_stats_t *o) {
   o->ns_region_max = c->ns_region_max;
   o->a_fro2 = c->a_fro2;
   o->symmetric = c->sym ? 1 : 0;
-  o->a_bytes_per_pass = c->sym ? c->a_bytes_pass : (int64_t)c->esz * c->plan.rows_local * c->N;
+  o->a_bytes_per_pass = (c->sym || c->bsr) ? c->a_bytes_pass : (int64_t)c->esz * c->plan.rows_local * c->N;
+  o->bsr = c->bsr ? 1 : 0;
+  o->bsr_nnzb = c->bsr ? c->bsr_nnzb : 0;
   o->p2p = c->p2p ? 1 : 0;
   return NSRGS_OK;
 }

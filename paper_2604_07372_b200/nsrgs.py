@@ -46,7 +46,8 @@ class Stats(ct.Structure):
                 ("rows_per_panel", ct.c_int32), ("cut_panels", ct.c_int32), ("panels", ct.c_int64),
                 ("smem_bytes", ct.c_int64), ("panel_ms_total", ct.c_double), ("panel_launches", ct.c_int64),
                 ("kernel_launches", ct.c_int64), ("ns_region_max", ct.c_double), ("a_fro2", ct.c_double),
-                ("symmetric", ct.c_int32), ("a_bytes_per_pass", ct.c_int64), ("p2p", ct.c_int32)]
+                ("symmetric", ct.c_int32), ("a_bytes_per_pass", ct.c_int64), ("p2p", ct.c_int32),
+                ("bsr", ct.c_int32), ("bsr_nnzb", ct.c_int64)]
 
 
 _P = ct.c_void_p
@@ -63,6 +64,9 @@ _SIGS = {
     "nsrgs_generate": ([_P, ct.c_uint64, ct.c_double, _P], ct.c_int),
     "nsrgs_generate_observed": ([_P, ct.c_uint64, ct.c_double, ct.c_double, _P], ct.c_int),
     "nsrgs_copy_A_rows": ([_P, ct.c_int64, ct.c_int64, _P], ct.c_int),
+    "nsrgs_generate_observed_bsr": ([_P, ct.c_uint64, ct.c_double, ct.c_double, _P], ct.c_int),
+    "nsrgs_attach_A_bsr": ([_P, _P, _P, _P, ct.c_int64], ct.c_int),
+    "nsrgs_get_A_bsr": ([_P, ct.POINTER(ct.c_int64), _P, _P, _P], ct.c_int),
     "nsrgs_init_spectral": ([_P, ct.c_uint64, ct.c_int, ct.c_double, ct.POINTER(ct.c_int)], ct.c_int),
     "nsrgs_step": ([_P, ct.c_double, ct.c_int, ct.POINTER(ct.c_double)], ct.c_int),
     "nsrgs_run": ([_P, ct.c_int, ct.c_double, ct.c_int, ct.POINTER(ct.c_double)], ct.c_int),
@@ -193,10 +197,15 @@ class Solver:
         return x.data_ptr(), int(x.is_cuda)
 
     # ------------------------------------------------------------------ C-ABI calls
-    def generate(self, seed: int, sigma: float, want_Z: bool = True, p: float = 1.0):
+    def generate(self, seed: int, sigma: float, want_Z: bool = True, p: float = 1.0, storage: str = "dense"):
+        """storage="dense" (row-major shard) or "bsr" (observed blocks only)."""
         Z = np.empty((self.n, self.d, self.d), dtype=self.np_dtype) if want_Z else None
         zp = Z.ctypes.data if want_Z else None
-        if p == 1.0:
+        if storage == "bsr":
+            self._check(_lib.nsrgs_generate_observed_bsr(self._h, seed, sigma, p, zp))
+        elif storage != "dense":
+            raise ValueError(storage)
+        elif p == 1.0:
             self._check(_lib.nsrgs_generate(self._h, seed, sigma, zp))
         else:
             self._check(_lib.nsrgs_generate_observed(self._h, seed, sigma, p, zp))
@@ -207,6 +216,26 @@ class Solver:
         assert dev, "attach_A needs a device tensor"
         self._A_ref = A_shard
         self._check(_lib.nsrgs_attach_A(self._h, ptr, lda if lda is not None else A_shard.stride(0)))
+
+    def attach_A_bsr(self, rowptr, col, vals):
+        """Borrow a caller-owned block-sparse A (device tensors: int64 rowptr, int32 col, float32 vals)."""
+        for t in (rowptr, col, vals):
+            assert t.is_cuda and t.is_contiguous()
+        self._A_ref = (rowptr, col, vals)
+        nnzb = col.numel()
+        self._check(_lib.nsrgs_attach_A_bsr(self._h, rowptr.data_ptr(), col.data_ptr(), vals.data_ptr(), nnzb))
+
+    def get_A_bsr(self):
+        """(rowptr int64[n_local+1], col int32[nnzb], vals float32[nnzb, d, d]) on the host."""
+        nnzb = ct.c_int64(0)
+        self._check(_lib.nsrgs_get_A_bsr(self._h, ct.byref(nnzb), None, None, None))
+        nl = self.n // self.world
+        rowptr = np.empty(nl + 1, dtype=np.int64)
+        col = np.empty(nnzb.value, dtype=np.int32)
+        vals = np.empty((nnzb.value, self.d, self.d), dtype=np.float32)
+        self._check(_lib.nsrgs_get_A_bsr(self._h, ct.byref(nnzb), rowptr.ctypes.data, col.ctypes.data,
+                                         vals.ctypes.data))
+        return rowptr, col, vals
 
     def copy_A_rows(self, row0: int, nrows: int) -> np.ndarray:
         out = np.empty((nrows, self.n * self.d), dtype=self.np_dtype)
