@@ -217,7 +217,7 @@ int nsrgs_set_symmetric(nsrgs_ctx *ctx, int enable);
 /* Launch configuration + measurement hooks (bench / tests).  */
 typedef struct {
   int32_t grid, threads, stages, rows_per_panel;     /* panel kernel launch shape              */
-  int32_t cut_panels;   /* panels split across CTAs by the stream-K schedule (combined in order) */
+  int32_t cut_panels;   /* panels split into column-range units by the work queue (combined in order) */
   int64_t panels, smem_bytes;
   double panel_ms_total;        /* summed CUDA-event time of panel kernel launches since reset */
   int64_t panel_launches;       /* number of panel kernel launches since reset                 */
