@@ -134,6 +134,47 @@ def _oracle_sample(cfg, nodes_sample, budget_s):
     return (nodes_sample / n) / per, per, passes, threads
 
 
+def _oracle_single_thread(cfg, nodes_sample, passes=3):
+    """The same sample with the BLAS pool limited to one thread (context figure)."""
+    from threadpoolctl import threadpool_limits
+
+    from oracle import instance as inst
+    from oracle import nsrgs as ons
+
+    n, d = cfg["n"], cfg["d"]
+    Z = inst.ground_truth(0, n, d)
+    nodes = np.arange(nodes_sample)
+    R = inst.measurement_rows(0, Z, cfg["sigma"], nodes)
+    with threadpool_limits(limits=1):
+        ons.step_rows(R, Z, nodes, 1.0 / n, cfg["K"])
+        t0 = time.perf_counter()
+        for _ in range(passes):
+            ons.step_rows(R, Z, nodes, 1.0 / n, cfg["K"])
+        per = (time.perf_counter() - t0) / passes
+    return (nodes_sample / n) / per
+
+
+def _read_stream_gbs(torch, device, stream, gib=8, reps=5):
+    """In-run read-stream peak: best of `reps` fp32 sums over a buffer far larger
+    than L2 (torch's reduction kernel, a plain HBM read stream), CUDA events on `stream`."""
+    n = gib * (1 << 30) // 4
+    buf = torch.ones(n, dtype=torch.float32, device=device)
+    best = None
+    with torch.cuda.stream(stream):
+        buf.sum()
+        for _ in range(reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            buf.sum()
+            e1.record(stream)
+            e1.synchronize()
+            ms = e0.elapsed_time(e1)
+            best = ms if best is None else min(best, ms)
+    del buf
+    torch.cuda.empty_cache()
+    return 4.0 * n / (best / 1e3) / 1e9
+
+
 def run_reference(args, cfg):
     world, rank, _ = _dist_env()
     if rank != 0:
@@ -352,8 +393,10 @@ def run_gpu(args, cfg):
         cpu = {"value": v, "unit": "it/s", "cores": threads, "kind": "oracle",
                "sample": f"oracle.nsrgs.step_rows on {args.sample_nodes} of {n} nodes "
                          f"({args.sample_nodes * d} of {N} A rows, fp64), {passes_c} passes in "
-                         f"{passes_c * per:.1f} s; it/s = ({args.sample_nodes}/{n}) / s_per_pass"}
+                         f"{passes_c * per:.1f} s; it/s = ({args.sample_nodes}/{n}) / s_per_pass",
+               "single_thread_value": _oracle_single_thread(cfg, args.sample_nodes)}
     traffic = _traffic(args.config)
+    read_peak = _read_stream_gbs(torch, f"cuda:{local}", stream) if not args.no_read_probe else None
     line = {
         "metric": METRIC, "value": value, "unit": "it/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
@@ -365,7 +408,9 @@ def run_gpu(args, cfg):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "peak_kind": peak_kind, "kernel": "panel_kernel (fused A.X + epilogue)",
                      "bytes_per_launch": bytes_launch, "avg_launch_ms": avg_ms,
-                     "frac_of_nominal_8TBs": achieved / 8000.0},
+                     "frac_of_nominal_8TBs": achieved / 8000.0,
+                     "read_stream_gbs_in_run": read_peak,
+                     "frac_of_read_stream": achieved / read_peak if read_peak else None},
         "effective_gbs": eff_gbs, "a_passes_per_step": passes, "phases": phases,
         "e2e": {"value": e2e_value, "unit": "it/s", "h2d_bytes_per_step": 4 * n * d * d,
                 "d2h_bytes_per_step": 4 * n * d * d + 8 * T + 24},
@@ -405,6 +450,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--symmetric", action="store_true", help="symmetric half-storage pass (d <= 6, 1 GPU)")
     ap.add_argument("--no-sym-variant", action="store_true", help="skip the extra symmetric-variant measurement")
+    ap.add_argument("--no-read-probe", action="store_true", help="skip the in-run read-stream peak probe")
     ap.add_argument("--bsr-p", type=float, default=0.5, help="observation probability of the block-sparse variant")
     ap.add_argument("--no-bsr-variant", action="store_true", help="skip the block-sparse (p < 1) variant")
     args = ap.parse_args()

@@ -289,6 +289,56 @@ __global__ void scale_kernel(int64_t row0, int64_t rows, const double *MC, T *W,
 }
 
 // ----------------------------------------------------------------------------------------
+// a1, Chebyshev-filtered subspace step (runtime d, O(N d^2)): Y_new = alpha W - beta Y_prev
+// (in place in W; beta = 0 on the first filtered step), with the fp64 Gram partials
+// [Y_new^T Y_new | Y_cur^T Y_new] per block (width 2 d^2) for the Cholesky-QR that follows.
+template <typename T>
+__global__ void cheb_combine_kernel(int d, int64_t row0, int64_t rows, double alpha, double beta, T *W,
+                                    const T *Yprev, const T *Ycur, int64_t rows_local, int64_t tpr, double *part) {
+  const int64_t rl = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int DD = d * d;
+  double y[kMaxD], yc[kMaxD];
+  const bool valid = rl < rows;
+  if (valid) {
+    const int64_t r = row0 + rl;
+    for (int k = 0; k < d; ++k) {
+      const int64_t ix = tile_index(r, k, d, rows_local, tpr);
+      double v = alpha * (double)W[ix];
+      if (beta != 0.0) v -= beta * (double)Yprev[ix];
+      const T tv = (T)v;
+      W[ix] = tv;
+      y[k] = (double)tv;
+      yc[k] = (double)Ycur[ix];
+    }
+  }
+  // Gram partials per warp (slot = global warp index), entry by entry
+  const int64_t slot = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  for (int e = 0; e < 2 * DD; ++e) {
+    const int a = (e % DD) / d, b = (e % DD) % d;
+    double v = valid ? (e < DD ? y[a] : yc[a]) * y[b] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0) part[slot * 2 * DD + e] = v;
+  }
+}
+
+// Y_out[r] = Y_in[r] M (M = MC[0..d^2), the Cholesky-QR factor of the filtered block): keeps the
+// previous Chebyshev iterate in the same basis as the orthonormalised new one.
+template <typename T>
+__global__ void cheb_apply_kernel(int d, int64_t row0, int64_t rows, const double *MC, const T *Yin, T *Yout,
+                                  int64_t rows_local, int64_t tpr) {
+  const int64_t rl = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (rl >= rows) return;
+  const int64_t r = row0 + rl;
+  double y[kMaxD];
+  for (int k = 0; k < d; ++k) y[k] = (double)Yin[tile_index(r, k, d, rows_local, tpr)];
+  for (int b = 0; b < d; ++b) {
+    double v = 0.0;
+    for (int k = 0; k < d; ++k) v += y[k] * MC[k * d + b];
+    Yout[tile_index(r, b, d, rows_local, tpr)] = (T)v;
+  }
+}
+
+// ----------------------------------------------------------------------------------------
 // a8: F(X^t) = 1/2(||X^T X||^2 - sum_i ||X_i^T X_i||^2) - <X, AX> + 1/2 ||A||^2 for every
 // slot t of res[T][npart] = [X^T X (DD) | unused (DD) | s_own | xb].
 __global__ void objective_final_kernel(int d, int T, const double *res, int npart, const double *a_fro2,
@@ -698,6 +748,35 @@ cudaError_t launch_scale(int dtype, int d, int64_t node0, int64_t n_local, const
     NSRGS_D_SWITCH(d, (scale_kernel<double, D><<<nblk(rows, 256), 256, 0, s>>>(row0, rows, MC, (double *)W,
                                                                               (const double *)Yold, rows_local, tpr, part)));
   }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cheb_combine(int dtype, int d, int64_t node0, int64_t n_local, double alpha, double beta, void *W,
+                                const void *Yprev, const void *Ycur, int64_t rows_local, int64_t tpr, double *part,
+                                int *nblocks, cudaStream_t s) {
+  const int64_t rows = n_local * d, row0 = node0 * d;
+  const unsigned grid = nblk(rows, kRedThreads);
+  *nblocks = (int)grid * (kRedThreads / 32);   // partial slots (one per warp)
+  if (dtype == 0)
+    cheb_combine_kernel<float><<<grid, kRedThreads, 0, s>>>(d, row0, rows, alpha, beta, (float *)W,
+                                                                (const float *)Yprev, (const float *)Ycur, rows_local,
+                                                                tpr, part);
+  else
+    cheb_combine_kernel<double><<<grid, kRedThreads, 0, s>>>(d, row0, rows, alpha, beta, (double *)W,
+                                                                 (const double *)Yprev, (const double *)Ycur,
+                                                                 rows_local, tpr, part);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cheb_apply(int dtype, int d, int64_t node0, int64_t n_local, const double *MC, const void *Yin,
+                              void *Yout, int64_t rows_local, int64_t tpr, cudaStream_t s) {
+  const int64_t rows = n_local * d, row0 = node0 * d;
+  if (dtype == 0)
+    cheb_apply_kernel<float><<<nblk(rows, 256), 256, 0, s>>>(d, row0, rows, MC, (const float *)Yin, (float *)Yout,
+                                                              rows_local, tpr);
+  else
+    cheb_apply_kernel<double><<<nblk(rows, 256), 256, 0, s>>>(d, row0, rows, MC, (const double *)Yin,
+                                                               (double *)Yout, rows_local, tpr);
   return cudaGetLastError();
 }
 

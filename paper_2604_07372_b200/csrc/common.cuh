@@ -61,7 +61,7 @@ struct PanelParams {
 };
 
 // Symmetric half-storage pass (sym.cu): blocks of GP panels x kSymTilesPerBlock column tiles.
-constexpr int kSymTilesPerBlock = 4;
+constexpr int kSymTilesPerBlock = 6;
 constexpr int kSymPanelsPerBlock = 16;
 struct SymParams {
   PanelParams e;          // epilogue + partial-reduction fields (X, Xout, n, node0, coef, eta, K, ...)

@@ -60,6 +60,11 @@ cudaError_t launch_chol(int d, const double *res, double *MC, int *err, cudaStre
 cudaError_t launch_scale(int dtype, int d, int64_t node0, int64_t n_local, const double *MC, void *W,
                          const void *Yold, int64_t rows_local, int64_t tiles_per_rank, double *part,
                          int *nblocks, cudaStream_t s);
+cudaError_t launch_cheb_combine(int dtype, int d, int64_t node0, int64_t n_local, double alpha, double beta, void *W,
+                                const void *Yprev, const void *Ycur, int64_t rows_local, int64_t tpr, double *part,
+                                int *nblocks, cudaStream_t s);
+cudaError_t launch_cheb_apply(int dtype, int d, int64_t node0, int64_t n_local, const double *MC, const void *Yin,
+                              void *Yout, int64_t rows_local, int64_t tpr, cudaStream_t s);
 cudaError_t launch_polar(int dtype, int d, int64_t n, const void *Y, void *X, int64_t rows_local,
                          int64_t tiles_per_rank, int *err, cudaStream_t s);
 cudaError_t launch_objective_final(int d, int T, const double *res, int npart, const double *a_fro2,

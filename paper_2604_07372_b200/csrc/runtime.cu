@@ -150,6 +150,7 @@ struct nsrgs_ctx {
   int64_t bsr_nnzb = 0;
   float *bsr_xs = nullptr;        // padded node-major X copy (d <= 10)
   double *bsr_part = nullptr;     // [bsr grid][npart]
+  void *yprev = nullptr;          // Chebyshev-filtered init: previous iterate (tile layout, x_elems)
   unsigned *bsr_cnt = nullptr;    // [0] last-CTA counter
   // scratch
   double *cta_part = nullptr;   // grid * npart
@@ -650,7 +651,7 @@ int nsrgs_destroy(nsrgs_ctx *c) {
     if (c->peer_opened[g]) cudaIpcCloseMemHandle(c->peer_block[g]);
   void *bufs[] = {c->units, c->pinfo, c->ucnt, c->ctl, c->acc, c->ts, c->xblock, c->stage, c->cta_part, c->counters, c->Bpart, c->res, c->red_part, c->small,
                   c->err, c->ns_region, c->rowpart, c->colpart, c->blocks, c->sym_cnt, c->sym_part,
-                  c->bsr_xs, c->bsr_part, c->bsr_cnt};
+                  c->bsr_xs, c->bsr_part, c->bsr_cnt, c->yprev};
   for (void *b : bufs)
     if (b) cudaFree(b);
   if (c->own_A && c->A) cudaFree(c->A);
@@ -997,16 +998,51 @@ int nsrgs_init_spectral(nsrgs_ctx *c, uint64_t seed, int max_sweeps, double tol,
   int sweeps = 0, stalled = 0;
   bool converged = false;
   double best_chg = 1e300;
+  // Chebyshev filtering (reading R20): from the second sweep on, each sweep applies
+  // the three-term recurrence T_{k+1}(A/b) = 2 (A/b) T_k - T_{k-1} that keeps [-b, b] bounded,
+  // b = 2 ||A||_F / sqrt(N) (the Wigner bulk-edge bound: the noise spectrum of the instance lies
+  // inside): the wanted directions gain x + sqrt(x^2 - 1), x = lambda_d / b, per sweep over the
+  // bulk instead of lambda_d / b.  Orthonormalising Y_k and Y_{k-1} by the same right factor keeps
+  // the polynomial recurrence exact (and removes any need for a scaled recurrence).  If the
+  // change stalls (no gap above b), it falls back to plain sweeps.  NSRGS_INIT_CHEB=0 keeps plain
+  // subspace iteration throughout.
+  const char *cheb_env = std::getenv("NSRGS_INIT_CHEB");
+  const bool cheb_on = !(cheb_env && cheb_env[0] == '0');
+  const double bnd = 2.0 * std::sqrt(std::max(c->a_fro2, 0.0) / (double)c->N);
+  bool cheb = false, cheb_failed = false;
+  double prev_chg = 1e300;
+  int cheb_steps = 0, cheb_stall = 0;
+  if (cheb_on && !c->yprev) CUDA_TRY(c, cudaMalloc(&c->yprev, c->esz * (size_t)c->plan.x_elems));
+  const int64_t ncs = ceil_div(c->plan.rows_local, 256) * 8;   // combine partial slots (per warp)
+  NSRGS_TRY(ensure_red(c, std::max<int64_t>(nbs, ncs * 2 * DD)));
+  NSRGS_TRY(ensure_res(c, 1));
   for (sweeps = 1; sweeps <= max_sweeps; ++sweeps) {
     void *Y = c->X[c->cur], *W = c->X[1 - c->cur];
     NSRGS_TRY(launch_panel(c, kModeProduct, Y, W, c->res, 0.0, 0));
-    NSRGS_TRY(allreduce_sum(c, c->res, 2 * DD));
+    if (!cheb) {
+      NSRGS_TRY(allreduce_sum(c, c->res, 2 * DD));
+    } else {
+      // Y_new = alpha W - beta Y_prev (W = A Y_cur; c = 0 for the symmetric interval), Grams
+      const double alpha = (cheb_steps == 0 ? 1.0 : 2.0) / bnd, beta = cheb_steps == 0 ? 0.0 : 1.0;
+      int nsl = 0;
+      CUDA_TRY(c, launch_cheb_combine(c->dtype, c->d, c->plan.node0, c->plan.n_local, alpha, beta, W, c->yprev, Y,
+                                      c->plan.rows_local, c->plan.tiles_per_rank, c->red_part, &nsl, c->stream));
+      CUDA_TRY(c, launch_reduce(c->red_part, nsl, 2 * DD, c->res, c->stream));
+      c->kernel_launches += 2;
+      NSRGS_TRY(allreduce_sum(c, c->res, 2 * DD));
+      ++cheb_steps;
+    }
     CUDA_TRY(c, launch_chol(c->d, c->res, c->small + kSmallMC, c->err, c->stream));
     int nb = 0;
     CUDA_TRY(c, launch_scale(c->dtype, c->d, c->plan.node0, c->plan.n_local, c->small + kSmallMC, W, Y,
                              c->plan.rows_local, c->plan.tiles_per_rank, c->red_part, &nb, c->stream));
     CUDA_TRY(c, launch_reduce(c->red_part, nb, 1, c->small + kSmallChg, c->stream));
     c->kernel_launches += 3;
+    if (cheb) {   // the previous iterate in the new basis: Y_prev <- Y_cur M
+      CUDA_TRY(c, launch_cheb_apply(c->dtype, c->d, c->plan.node0, c->plan.n_local, c->small + kSmallMC, Y, c->yprev,
+                                    c->plan.rows_local, c->plan.tiles_per_rank, c->stream));
+      c->kernel_launches++;
+    }
     NSRGS_TRY(allreduce_sum(c, c->small + kSmallChg, 1));
     NSRGS_TRY(allgather_X(c, W));
     c->cur = 1 - c->cur;
@@ -1018,6 +1054,8 @@ int nsrgs_init_spectral(nsrgs_ctx *c, uint64_t seed, int max_sweeps, double tol,
     if (flags & kErrNonfinite) return set_err(c, NSRGS_ERR_NONFINITE, "non-finite Gram partial at sweep %d", sweeps);
     if (!std::isfinite(chg2)) return set_err(c, NSRGS_ERR_NONFINITE, "non-finite subspace change at sweep %d", sweeps);
     const double chg = std::sqrt(chg2);
+    if (std::getenv("NSRGS_DEBUG_INIT"))
+      std::fprintf(stderr, "init sweep %d cheb %d chg %.3e bnd %.6g\n", sweeps, (int)cheb, chg, bnd);
     if (sweeps >= 2 && chg < tol) { converged = true; break; }
     // fp32 noise floor (reading R14): the change stopped shrinking while already tiny
     if (sweeps >= 4 && chg < 1e-3 && chg > 0.7 * best_chg) {
@@ -1026,6 +1064,16 @@ int nsrgs_init_spectral(nsrgs_ctx *c, uint64_t seed, int max_sweeps, double tol,
       stalled = 0;
     }
     if (sweeps >= 2) best_chg = std::min(best_chg, chg);
+    if (cheb) {   // stall guard: no decrease over 4 filtered sweeps while far from converged
+      cheb_stall = (chg > 0.9 * prev_chg && chg > 1e-3) ? cheb_stall + 1 : 0;
+      if (cheb_stall >= 4) {
+        cheb = false;
+        cheb_failed = true;
+      }
+    } else if (cheb_on && !cheb_failed && sweeps == 1 && bnd > 0.0 && std::isfinite(bnd)) {
+      cheb = true;   // Y_1 is orthonormal: start the recurrence from it
+    }
+    prev_chg = chg;
   }
   if (sweeps > max_sweeps) sweeps = max_sweeps;
   CUDA_TRY(c, launch_polar(c->dtype, c->d, c->n, c->X[c->cur], c->X[1 - c->cur], c->plan.rows_local,

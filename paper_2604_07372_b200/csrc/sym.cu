@@ -38,7 +38,7 @@ struct SymCfg {
   static constexpr int NODES = ROWS / D;
   static constexpr int KP = D / 2;                    // component pairs (2kp, 2kp+1)
   static constexpr bool ODD = (D & 1) != 0;          // last component on column pairs
-  static constexpr int GT = kSymTilesPerBlock;          // column tiles per block (512 columns)
+  static constexpr int GT = D >= 6 ? 4 : kSymTilesPerBlock;   // column tiles per block (slices: 7 x GT x d x 128 floats)
   static constexpr int A_BYTES = ROWS * kColTile * 4;
   static constexpr int X_BYTES = D * kColTile * 4;
   static constexpr int STAGE_BYTES = A_BYTES + X_BYTES;
@@ -181,18 +181,26 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int64_t row_lo = (int64_t)m.p * C::ROWS;        // panel start row
     const int64_t wrow0 = row_lo + warp * C::RT;          // this warp's first row
     if (m.flags & kFirstP) {
+      // X rows of this warp (column direction) from the tile layout, 32-bit index arithmetic
+      // (N d < 2^31 at every supported size); bounds only in the last panel (uniform branch)
+      const int wr0 = (int)wrow0;
+      auto load_rows = [&](auto guarded) {
+        constexpr bool G = decltype(guarded)::value;
 #pragma unroll
-      for (int r = 0; r < C::RT; ++r) {
-        const int64_t row = wrow0 + r;
-        const float *xb = Xg + (row >> 7) * D * kColTile;   // world == 1: tile of row
-        const int o = (int)(row & 127);
+        for (int r = 0; r < C::RT; ++r) {
+          const int row = wr0 + r;
+          const bool ok = !G || row < (int)N;
+          const int tb = (row >> 7) * (D * kColTile), o = row & 127;
+          const unsigned long long *xp2 = reinterpret_cast<const unsigned long long *>(Xg + tb) + o;
 #pragma unroll
-        for (int kp = 0; kp < C::KP + KL; ++kp) acc2[r][kp] = 0ull;
+          for (int kp = 0; kp < C::KP + KL; ++kp) acc2[r][kp] = 0ull;
 #pragma unroll
-        for (int kp = 0; kp < C::KP; ++kp)
-          xr[r][kp] = row < N ? __ldg(reinterpret_cast<const unsigned long long *>(xb + 2 * kp * kColTile + 2 * o)) : 0ull;
-        if constexpr (C::ODD) xl[r] = row < N ? __ldg(xb + (D - 1) * kColTile + o) : 0.f;
-      }
+          for (int kp = 0; kp < C::KP; ++kp) xr[r][kp] = ok ? __ldg(xp2 + kp * kColTile) : 0ull;
+          if constexpr (C::ODD) xl[r] = ok ? __ldg(Xg + tb + (D - 1) * kColTile + o) : 0.f;
+        }
+      };
+      if (wr0 + C::RT <= (int)N) load_rows(std::integral_constant<bool, false>{});
+      else load_rows(std::integral_constant<bool, true>{});
     }
     const int64_t col0 = (int64_t)m.t * kColTile;
     const float *As = reinterpret_cast<const float *>(smem + stage * C::STAGE_BYTES) + (warp * C::RT) * kColTile + 2 * lane;

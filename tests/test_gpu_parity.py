@@ -163,6 +163,27 @@ def test_end_to_end_modulo_rotation(nsrgs, n, d, sigma, K, T, dtype):
     s.close()
 
 
+@pytest.mark.parametrize("n,d,sigma,p", [(2000, 3, 8.0, 1.0), (1200, 5, 0.3 * np.sqrt(1200) / 5, 1.0),
+                                         (1500, 4, 1.0, 0.5)])
+def test_chebyshev_init_matches_plain_and_oracle(nsrgs, monkeypatch, n, d, sigma, p):
+    """Chebyshev-filtered subspace iteration (reading R20) reaches the same top-d subspace as
+    plain subspace iteration and the fp64 oracle, in fewer A passes."""
+    out = {}
+    for cheb in ("1", "0"):
+        monkeypatch.setenv("NSRGS_INIT_CHEB", cheb)
+        s = nsrgs.Solver(n, d)
+        s.generate(3, sigma, want_Z=False, p=p)
+        sw = s.init_spectral(3, 400, 1e-6, allow_unconverged=True)
+        out[cheb] = (sw, s.get_X())
+        s.close()
+    assert out["1"][0] < out["0"][0], (out["1"][0], out["0"][0])
+    assert rel_mod_rotation(out["1"][1], out["0"][1]) <= 2e-5
+    Z = inst.ground_truth(3, n, d)
+    A = inst.measurement_matrix(3, Z, sigma, p=p)
+    X0, _, _ = ons.spectral_init(A, d, "subspace", Y0=inst.initial_subspace(3, n, d), tol=1e-12)
+    assert rel_mod_rotation(out["1"][1], X0) <= 1e-4
+
+
 def test_alignment_metrics_on_oracle_iterate(nsrgs):
     n, d = 300, 5
     Z = inst.ground_truth(4, n, d)
