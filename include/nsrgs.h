@@ -230,6 +230,7 @@ typedef struct {
   int32_t p2p;                  /* 1 if X^{t+1} is exchanged by the fused NVLink-store path     */
   int32_t bsr;                  /* 1 if the block-sparse storage is active                      */
   int64_t bsr_nnzb;             /* stored blocks of this rank (incl. zero padding blocks)       */
+  int32_t bsr_slab;             /* 1 if the block-sparse pass runs the column-group slab variant  */
 } nsrgs_stats_t;
 int nsrgs_get_stats(nsrgs_ctx *ctx, nsrgs_stats_t *out);
 int nsrgs_reset_stats(nsrgs_ctx *ctx, int enable_panel_timing);

@@ -144,6 +144,8 @@ struct nsrgs_ctx {
   int64_t a_bytes_pass = 0;
   // block-sparse storage (bsr.cu)
   bool bsr = false, own_bsr = false;
+  bool bsr_sorted = false;        // every row's columns non-decreasing (generator layout): slab pass
+  int bsr_lg2g = -1;              // slab pass column-group size (log2), -1: per-block gather pass
   int64_t *bsr_rowptr = nullptr;
   int *bsr_col = nullptr;
   float *bsr_vals = nullptr;
@@ -441,7 +443,7 @@ int launch_panel(nsrgs_ctx *c, int mode, const void *Xin, void *Xout, double *re
       c->kernel_launches++;
       bp.Xs = c->bsr_xs;
     }
-    CUDA_TRY(c, bsr_dispatch(c->d, mode, &bp, c->stream));
+    CUDA_TRY(c, bsr_dispatch(c->d, mode, &bp, c->bsr_lg2g, c->stream));
   } else if (c->sym) {
     SymParams sp{};
     sp.e = p;
@@ -503,6 +505,7 @@ void drop_bsr(nsrgs_ctx *c) {
   c->bsr_vals = nullptr;
   c->own_bsr = false;
   c->bsr = false;
+  c->bsr_sorted = false;
   c->bsr_nnzb = 0;
 }
 
@@ -517,6 +520,9 @@ int bsr_scratch(nsrgs_ctx *c) {
     CUDA_TRY(c, cudaMemsetAsync(c->bsr_cnt, 0, 4 * sizeof(unsigned), c->stream));
   }
   c->a_bytes_pass = c->bsr_nnzb * (int64_t)(c->d * c->d * 4 + 4) + 8 * (c->plan.n_local + 1);
+  const char *env = std::getenv("NSRGS_BSR_SLAB");
+  const double p_eff = (double)c->bsr_nnzb / ((double)c->plan.n_local * (double)c->n);
+  c->bsr_lg2g = (c->bsr_sorted && !(env && env[0] == '0')) ? bsr_slab_lg2g(c->d, p_eff) : -1;
   return NSRGS_OK;
 }
 
@@ -906,6 +912,7 @@ int nsrgs_generate_observed_bsr(nsrgs_ctx *c, uint64_t seed, double sigma, doubl
   cudaFree(Z64);
   cudaFree(cnt);
   if (st) return st;
+  c->bsr_sorted = true;
   NSRGS_TRY(bsr_scratch(c));
   c->bsr = true;
   c->have_A = true;
@@ -1381,6 +1388,7 @@ int nsrgs_get_stats(nsrgs_ctx *c, nsrgs_stats_t *o) {
   o->a_bytes_per_pass = (c->sym || c->bsr) ? c->a_bytes_pass : (int64_t)c->esz * c->plan.rows_local * c->N;
   o->bsr = c->bsr ? 1 : 0;
   o->bsr_nnzb = c->bsr ? c->bsr_nnzb : 0;
+  o->bsr_slab = (c->bsr && c->bsr_lg2g >= 0) ? 1 : 0;
   o->p2p = c->p2p ? 1 : 0;
   return NSRGS_OK;
 }

@@ -69,7 +69,8 @@ def test_bsr_generator(nsrgs, n, d, p):
         obs = obs[obs != i]
         m = len(obs)
         assert np.array_equal(c[:m], obs)                        # the oracle's edge set, ascending
-        assert np.all(c[m:] == i) and np.all(v[m:] == 0.0) and len(c) - m < 4
+        pad = obs[-1] if m else i                                # padding keeps the row sorted
+        assert np.all(c[m:] == pad) and np.all(v[m:] == 0.0) and len(c) - m < 4
     A = expand(rowptr, col, vals, n, d)
     assert np.array_equal(A, Ad)                                 # bitwise the dense generator
     Ao = inst.measurement_matrix(seed, Z, sigma, p=p)
@@ -103,6 +104,31 @@ def test_bsr_step_gpm_objective(nsrgs, n, d, sigma, p, K):
     s.gpm_run(1)
     assert rel_fro(s.get_X(), ons.gpm_step(A, Xd)) <= 1e-6
     s.close()
+
+
+@pytest.mark.parametrize("n,d,p", [(3000, 5, 0.9), (2000, 3, 0.8), (1000, 2, 1.0), (700, 6, 0.75), (500, 4, 1.0)])
+def test_bsr_slab_pass_equals_gather_pass(nsrgs, monkeypatch, n, d, p):
+    """The slab pass (sorted rows: column-group X slabs shared by the CTA's rows) and the
+    per-block gather pass multiply the same blocks in the same per-lane order: identical X^{t+1};
+    the objective partials differ only by the fp64 CTA grouping."""
+    sigma, K = 0.4, 3
+    X = oracle_iterate_near(inst.ground_truth(12, n, d), 0.2, 4).astype(np.float32)
+    out = []
+    for slab in ("1", "0"):
+        monkeypatch.setenv("NSRGS_BSR_SLAB", slab)
+        s = nsrgs.Solver(n, d)
+        s.generate(12, sigma, want_Z=False, p=p, storage="bsr")
+        assert s.stats()["bsr_slab"] == (slab == "1")
+        s.set_X(X)
+        f = s.step(1.0 / (n * p), K)
+        out.append((s.get_X(), f))
+        s.close()
+    assert np.array_equal(out[0][0], out[1][0])
+    assert abs(out[0][1] - out[1][1]) <= 1e-12 * abs(out[1][1])
+    if n <= 1000:
+        A = inst.measurement_matrix(12, inst.ground_truth(12, n, d), sigma, p=p)
+        Xo, _, _ = ons.step(A, X.astype(np.float64), 1.0 / (n * p), K)
+        assert rel_fro(out[0][0], Xo) <= 1e-6
 
 
 def test_bsr_matches_dense_pass(nsrgs):
