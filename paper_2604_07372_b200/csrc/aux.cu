@@ -172,11 +172,18 @@ __global__ void reduce_kernel(const double *part, int nblocks, int width, double
     if (threadIdx.x == 0) out[0] = sh[0];
     return;
   }
-  for (int i = threadIdx.x; i < width; i += blockDim.x) {
-    double v = 0.0;
-    for (int b = 0; b < nblocks; ++b) v += part[(int64_t)b * width + i];
-    out[i] = v;
+  // width > 1: one CTA per column i, threads over the slots in a fixed partition, fixed-order tree
+  __shared__ double sh2[256];
+  const int i = blockIdx.x;
+  double v = 0.0;
+  for (int b = threadIdx.x; b < nblocks; b += blockDim.x) v += part[(int64_t)b * width + i];
+  sh2[threadIdx.x] = v;
+  __syncthreads();
+  for (int st = blockDim.x / 2; st > 0; st >>= 1) {
+    if ((int)threadIdx.x < st) sh2[threadIdx.x] += sh2[threadIdx.x + st];
+    __syncthreads();
   }
+  if (threadIdx.x == 0) out[i] = sh2[0];
 }
 
 template <typename T>
@@ -707,7 +714,7 @@ cudaError_t launch_sumsq(int dtype, const void *A, int64_t rows, int64_t cols, i
 }
 
 cudaError_t launch_reduce(const double *part, int nblocks, int width, double *out, cudaStream_t s) {
-  reduce_kernel<<<1, width == 1 ? 1024 : 256, 0, s>>>(part, nblocks, width, out);
+  reduce_kernel<<<width == 1 ? 1 : width, width == 1 ? 1024 : 256, 0, s>>>(part, nblocks, width, out);
   return cudaGetLastError();
 }
 

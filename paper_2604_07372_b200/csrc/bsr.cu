@@ -198,12 +198,12 @@ template <int D>
 struct BsrCfg {
   static constexpr int DD = D * D;
   static constexpr int DP = D + (D & 1);                // even row stride of the padded X record
-  static constexpr int DS0 = (D * DP + 3) / 4 * 4;
-  static constexpr int DS = (DS0 % 8 == 4) ? DS0 : DS0 + 4;   // node stride of the padded X copy: 16 B
-                                                        // aligned and 4 mod 8 words, so records read
-                                                        // straight from a linear slab copy spread
-                                                        // over the banks
-  static constexpr int XSS = DS;                        // smem record stride = 4 mod 8 words:
+  static constexpr int DS = (D * DP + 3) / 4 * 4;       // node stride of the padded X copy (16 B;
+                                                        // 128 B = one L2 line at d = 5)
+  static constexpr int DSS = (DS % 8 == 4) ? DS : DS + 4;   // slab pass: 4 mod 8 words, so records
+                                                        // read straight from a linear slab copy
+                                                        // spread over the banks
+  static constexpr int XSS = DSS;                       // smem record stride = 4 mod 8 words:
                                                         // conflict-free LDS.64 / LDS.128 per lane
   static constexpr int Q4 = DS / 4;                     // float4 per record
   static constexpr int KP = DP / 2;                     // component pairs
@@ -449,7 +449,7 @@ struct BsrSlabCfg {
   static constexpr int NW = W + 1;             // + producer warp
   static constexpr int S = 4;                  // slab slots
   static constexpr int SLAB = 2304;            // floats per slot (9 KB)
-  static constexpr int GMAX = SLAB / B::DS;    // nodes per column group, at most
+  static constexpr int GMAX = SLAB / B::DSS;    // nodes per column group, at most
   static constexpr int SMEM = (S * SLAB + W * (2 * B::SAB + 5 * B::EP)) * 4 + NW * B::NPART * 8 + (2 * S + 2 * W) * 8 + 16;
 };
 
@@ -495,9 +495,9 @@ __global__ void __launch_bounds__(32 * BsrSlabCfg<D>::NW) bsr_slab_kernel(const 
         if (g >= C::S) mbar_wait(&empty[slot], (uint32_t)(((g / C::S) - 1) & 1));
         const int64_t n0 = (int64_t)g << lg2g;
         const int cntn = (int)min((int64_t)G, p.n - n0);
-        const uint32_t bytes = (uint32_t)(cntn * B::DS * 4);
+        const uint32_t bytes = (uint32_t)(cntn * B::DSS * 4);
         mbar_arrive_expect_tx(&full[slot], bytes);
-        bulk_load(slab + slot * C::SLAB, bp.Xs + n0 * B::DS, bytes, &full[slot], pol_x);
+        bulk_load(slab + slot * C::SLAB, bp.Xs + n0 * B::DSS, bytes, &full[slot], pol_x);
       }
     }
     __syncwarp();
@@ -566,8 +566,8 @@ __global__ void __launch_bounds__(32 * BsrSlabCfg<D>::NW) bsr_slab_kernel(const 
         const int ghi = min(gl, glo + C::S - 2);
         for (int g = glo; g <= ghi; ++g) mbar_wait(&full[g % C::S], (uint32_t)((g / C::S) & 1));
         if (lane < cnt && gme >= glo && gme <= ghi) {
-          const float *xr = slab + (gme % C::S) * C::SLAB + (jc - (gme << lg2g)) * B::DS;
-          uint64_t rec[B::DS / 2];
+          const float *xr = slab + (gme % C::S) * C::SLAB + (jc - (gme << lg2g)) * B::DSS;
+          uint64_t rec[B::DSS / 2];
 #pragma unroll
           for (int q = 0; q < B::Q4; ++q) {
             const ulonglong2 v = *reinterpret_cast<const ulonglong2 *>(xr + 4 * q);
@@ -725,12 +725,12 @@ __global__ void __launch_bounds__(128) bsr_wide_kernel(const BsrParams bp) {
 // tile layout X -> padded node-major copy (record of DS floats per node, row stride DP, zeros
 // in the padding), d <= 10
 template <int D>
-__global__ void bsr_pack_x_kernel(const float *X, float *Xs, int64_t n, int64_t rows_local, int64_t tpr) {
+__global__ void bsr_pack_x_kernel(const float *X, float *Xs, int64_t n, int64_t rows_local, int64_t tpr, int ds) {
   using C = BsrCfg<D>;
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= n * C::DS) return;
-  const int64_t j = idx / C::DS;
-  const int r = (int)(idx - j * C::DS), c = r / C::DP, k = r - c * C::DP;
+  if (idx >= n * ds) return;
+  const int64_t j = idx / ds;
+  const int r = (int)(idx - j * ds), c = r / C::DP, k = r - c * C::DP;
   Xs[idx] = (c < D && k < D) ? X[tile_index(j * D + c, k, D, rows_local, tpr)] : 0.f;
 }
 
@@ -801,10 +801,10 @@ cudaError_t bsr_mode_switch(int mode, const BsrParams &bp, int lg2g, cudaStream_
 
 }  // namespace
 
-int bsr_xs_stride(int d) {   // floats per node record of the padded X copy (d <= 10)
+int bsr_xs_stride(int d, bool slab) {   // floats per node record of the padded X copy (d <= 10)
   const int dp = d + (d & 1);
   const int ds = (d * dp + 3) / 4 * 4;
-  return ds % 8 == 4 ? ds : ds + 4;
+  return (!slab || ds % 8 == 4) ? ds : ds + 4;
 }
 
 int bsr_grid(int d, int64_t n_local) {
@@ -859,13 +859,14 @@ cudaError_t bsr_dispatch(int d, int mode, const BsrParams *bp, int lg2g, cudaStr
   }
 }
 
-cudaError_t launch_bsr_pack_x(int d, const void *X, float *Xs, int64_t n, int64_t rows_local, int64_t tpr,
+cudaError_t launch_bsr_pack_x(int d, const void *X, float *Xs, int64_t n, int64_t rows_local, int64_t tpr, bool slab,
                               cudaStream_t s) {
-  const int64_t cnt = n * bsr_xs_stride(d);
+  const int ds = bsr_xs_stride(d, slab);
+  const int64_t cnt = n * ds;
   const unsigned grid = (unsigned)((cnt + 255) / 256);
   switch (d) {
 #define NSRGS_PACK_CASE(DV) \
-  case DV: bsr_pack_x_kernel<DV><<<grid, 256, 0, s>>>(static_cast<const float *>(X), Xs, n, rows_local, tpr); break;
+  case DV: bsr_pack_x_kernel<DV><<<grid, 256, 0, s>>>(static_cast<const float *>(X), Xs, n, rows_local, tpr, ds); break;
     NSRGS_PACK_CASE(2)
     NSRGS_PACK_CASE(3)
     NSRGS_PACK_CASE(4)

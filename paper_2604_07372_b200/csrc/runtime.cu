@@ -116,6 +116,7 @@ struct nsrgs_ctx {
   int64_t lda = 0;
   bool own_A = false, have_A = false;
   CUtensorMap tmA;
+  CUtensorMap tmA_sym;   // symmetric pass: same A, its own panel height
   double a_fro2 = 0.0;
   // iterate
   void *X[2] = {nullptr, nullptr};   // both inside xblock (one IPC-shareable allocation)
@@ -355,7 +356,9 @@ int ensure_small(nsrgs_ctx *c, int64_t count) {
 }
 constexpr int kSmallFro = 0, kSmallChg = 1, kSmallMC = 8, kSmallOut = 8 + 2 * kMaxD * kMaxD;   // MC holds 2 d^2
 
-int build_tmap(nsrgs_ctx *c) {
+int build_tmap(nsrgs_ctx *c, CUtensorMap *out = nullptr, int rows = 0) {
+  if (!out) out = &c->tmA;
+  if (rows <= 0) rows = c->shape.rows;
   static EncodeTiledFn encode = nullptr;
   if (!encode) {
     void *fn = nullptr;
@@ -369,9 +372,9 @@ int build_tmap(nsrgs_ctx *c) {
   cuuint64_t dims[3] = {c->world == 1 ? (cuuint64_t)c->N : Nr, (cuuint64_t)c->world, (cuuint64_t)c->plan.rows_local};
   cuuint64_t strides[2] = {c->world == 1 ? (cuuint64_t)(c->lda * c->esz) : (cuuint64_t)(Nr * c->esz),
                            (cuuint64_t)(c->lda * c->esz)};
-  cuuint32_t box[3] = {(cuuint32_t)col_tile(c->d), 1u, (cuuint32_t)c->shape.rows};
+  cuuint32_t box[3] = {(cuuint32_t)col_tile(c->d), 1u, (cuuint32_t)rows};
   cuuint32_t estr[3] = {1u, 1u, 1u};
-  CUresult r = encode(&c->tmA, c->dtype == NSRGS_F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64,
+  CUresult r = encode(out, c->dtype == NSRGS_F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64,
                       3, c->A, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return set_err(c, NSRGS_ERR_CUDA, "cuTensorMapEncodeTiled failed (CUresult %d)", (int)r);
@@ -439,7 +442,8 @@ int launch_panel(nsrgs_ctx *c, int mode, const void *Xin, void *Xout, double *re
     bp.col = c->bsr_col;
     bp.vals = c->bsr_vals;
     if (c->d <= kMaxNarrowD) {   // X^t -> padded node-major records for the per-lane gathers
-      CUDA_TRY(c, launch_bsr_pack_x(c->d, Xin, c->bsr_xs, c->n, c->plan.rows_local, c->plan.tiles_per_rank, c->stream));
+      CUDA_TRY(c, launch_bsr_pack_x(c->d, Xin, c->bsr_xs, c->n, c->plan.rows_local, c->plan.tiles_per_rank,
+                                    c->bsr_lg2g >= 0, c->stream));
       c->kernel_launches++;
       bp.Xs = c->bsr_xs;
     }
@@ -458,7 +462,7 @@ int launch_panel(nsrgs_ctx *c, int mode, const void *Xin, void *Xout, double *re
     sp.nJ = c->nJ;
     sp.gp = kSymPanelsPerBlock;
     sp.N = c->N;
-    CUDA_TRY(c, sym_dispatch(c->d, mode, false, nullptr, &c->tmA, &sp, c->sym_grid, c->stream));
+    CUDA_TRY(c, sym_dispatch(c->d, mode, false, nullptr, &c->tmA_sym, &sp, c->sym_grid, c->stream));
     c->kernel_launches++;
   } else if (c->d > kMaxNarrowD) {
     CUDA_TRY(c, wide_dispatch(c->d, mode, false, nullptr, &c->tmA, &p, c->grid, c->stream));
@@ -512,7 +516,7 @@ void drop_bsr(nsrgs_ctx *c) {
 // Scratch of the block-sparse pass: padded X copy (d <= 10), per-CTA partial slots, counter.
 int bsr_scratch(nsrgs_ctx *c) {
   if (c->d <= kMaxNarrowD && !c->bsr_xs)
-    CUDA_TRY(c, cudaMalloc(&c->bsr_xs, sizeof(float) * (size_t)c->n * bsr_xs_stride(c->d)));
+    CUDA_TRY(c, cudaMalloc(&c->bsr_xs, sizeof(float) * (size_t)c->n * bsr_xs_stride(c->d, true)));
   if (!c->bsr_part)
     CUDA_TRY(c, cudaMalloc(&c->bsr_part, sizeof(double) * (size_t)bsr_grid(c->d, c->plan.n_local) * c->shape.npart));
   if (!c->bsr_cnt) {
@@ -807,6 +811,7 @@ int nsrgs_attach_A(nsrgs_ctx *c, const void *A_shard_dev, int64_t lda) {
   c->lda = lda;
   c->own_A = false;
   NSRGS_TRY(build_tmap(c));
+  if (c->sym) NSRGS_TRY(build_tmap(c, &c->tmA_sym, c->symshape.rows));
   int nb = 0;
   NSRGS_TRY(ensure_red(c, 8 * 4096));
   CUDA_TRY(c, launch_sumsq(c->dtype, c->A, c->plan.rows_local, c->N, c->lda, c->red_part, &nb, c->stream));
@@ -851,6 +856,7 @@ int nsrgs_generate_observed(nsrgs_ctx *c, uint64_t seed, double sigma, double p_
     CUDA_TRY(c, cudaMemcpyAsync(Z_out_host, c->stage, c->esz * (size_t)(c->n * c->d * c->d), cudaMemcpyDeviceToHost,
                                 c->stream));
   NSRGS_TRY(build_tmap(c));
+  if (c->sym) NSRGS_TRY(build_tmap(c, &c->tmA_sym, c->symshape.rows));
   int s = fro2_finish(c, nb);
   cudaFree(Z64);
   if (s) return s;
@@ -1272,11 +1278,10 @@ int nsrgs_set_symmetric(nsrgs_ctx *c, int enable) {
   if (c->bsr) return set_err(c, NSRGS_ERR_STATE, "symmetric storage needs the dense A (block-sparse A is active)");
   if (c->sym) return NSRGS_OK;
   CUDA_TRY(c, sym_dispatch(c->d, 0, true, &c->symshape, nullptr, nullptr, 0, nullptr));
-  if (c->symshape.rows != c->shape.rows)
-    return set_err(c, NSRGS_ERR_STATE, "symmetric storage: panel height mismatch (internal)");
+  NSRGS_TRY(build_tmap(c, &c->tmA_sym, c->symshape.rows));
   const int64_t R = c->symshape.rows, N = c->N, nt = c->plan.tiles_per_rank;
   const int GT = c->symshape.gt, GP = kSymPanelsPerBlock;
-  const int np = c->panels;
+  const int np = (int)ceil_div(c->plan.rows_local, R);   // symmetric panels (its own height)
   c->nJ = (int)ceil_div(nt, GT);
   c->nI = (int)ceil_div(np, GP);
   struct Blk { int I, J, p0, p1; int64_t cost; };
