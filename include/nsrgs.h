@@ -231,6 +231,7 @@ typedef struct {
   int32_t bsr;                  /* 1 if the block-sparse storage is active                      */
   int64_t bsr_nnzb;             /* stored blocks of this rank (incl. zero padding blocks)       */
   int32_t bsr_slab;             /* 1 if the block-sparse pass runs the column-group slab variant  */
+  int32_t bsr_g4;               /* 1 if it gathers X records with TMA tile::gather4              */
 } nsrgs_stats_t;
 int nsrgs_get_stats(nsrgs_ctx *ctx, nsrgs_stats_t *out);
 int nsrgs_reset_stats(nsrgs_ctx *ctx, int enable_panel_timing);

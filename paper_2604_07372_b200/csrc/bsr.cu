@@ -430,6 +430,157 @@ __global__ void __launch_bounds__(32 * BsrCfg<D>::W) bsr_kernel(const BsrParams 
   bsr_partials<C::NPART, C::W>(p, red, flag, warp, lane, g1s, g2s, C::DD, C::DDL, so, xs);
 }
 
+// ---------------------------------------------------------------------------------- gather4 pass
+// As bsr_kernel, but the chunk's X_j records arrive by TMA tile::gather4 (UTMALDG.2D.GATHER4:
+// 4 rows of the padded X copy, viewed as an n x DSS tensor, by row index per instruction) into a
+// double-buffered smem area at the conflict-free record stride, on the same mbarrier as the
+// chunk's A bulk copy: 8 + 1 TMA operations per 32 blocks, no LSU gather, no register staging.
+template <int D>
+struct BsrG4Cfg {
+  using B = BsrCfg<D>;
+  static constexpr int W = 4;
+  // TMA tensor destinations are 128-byte aligned: a gather group (4 records of DSS floats) starts
+  // at a multiple of 32 floats, so record r sits at (r / 4) GS + (r % 4) DSS (<= 2-way bank
+  // conflicts on the per-lane record reads)
+  static constexpr int GS = (4 * B::DSS + 31) / 32 * 32;
+  static constexpr int SXB = (B::CH / 4) * GS;
+  static constexpr int SAB = (B::SAB + 31) / 32 * 32;   // keeps every buffer 128-byte aligned
+  static constexpr int SA = 2 * SXB + 2 * SAB;
+  static constexpr int SMEM = 128 + W * (SA + 5 * B::EP) * 4 + W * B::NPART * 8 + W * 16 + 16;
+};
+
+__device__ __forceinline__ void tma_gather4(void *smem_dst, const void *tmap, uint64_t *bar, int c0, int r0, int r1,
+                                            int r2, int r3, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2], %8;" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(smem_u32(bar)), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "l"(policy)
+      : "memory");
+}
+
+template <int D, int MODE>
+__global__ void __launch_bounds__(32 * BsrG4Cfg<D>::W) bsr_g4_kernel(const __grid_constant__ CUtensorMap tmX,
+                                                                     const BsrParams bp) {
+  using B = BsrCfg<D>;
+  using C = BsrG4Cfg<D>;
+  extern __shared__ float4 smem4[];
+  uint8_t *raw = reinterpret_cast<uint8_t *>(smem4);
+  float *smem = reinterpret_cast<float *>(raw + (((smem_u32(raw) + 127u) & ~127u) - smem_u32(raw)));   // 128 B
+  const PanelParams &p = bp.e;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float *sXr = smem + warp * C::SA;         // [2][CH/4][GS]: gather4 targets
+  float *sA = sXr + 2 * C::SXB;             // [2][SAB]
+  float *scr = smem + C::W * C::SA + warp * 5 * B::EP;
+  double *red = reinterpret_cast<double *>(smem + C::W * (C::SA + 5 * B::EP));
+  uint64_t *bar = reinterpret_cast<uint64_t *>(red + C::W * B::NPART) + 2 * warp;
+  int *flag = reinterpret_cast<int *>(reinterpret_cast<uint64_t *>(red + C::W * B::NPART) + 2 * C::W);
+  const int64_t il = (int64_t)blockIdx.x * C::W + warp;
+  const int nvalid = il < p.n_local ? 1 : 0;
+  if (lane == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_mbar_init();
+    prefetch_tmap(&tmX);
+  }
+  __syncwarp();
+
+  uint64_t acc2[D][B::NKP];
+#pragma unroll
+  for (int a = 0; a < D; ++a)
+#pragma unroll
+    for (int t = 0; t < B::NKP; ++t) acc2[a][t] = 0ull;
+  if (nvalid) {
+    const int64_t r0 = bp.rowptr[il], r1 = bp.rowptr[il + 1];
+    const int nb = (int)(r1 - r0), nch = (nb + B::CH - 1) / B::CH;
+    const bool tma = ((r0 * B::DD) & 3) == 0 && (((int64_t)nb * B::DD) & 3) == 0 &&
+                     (reinterpret_cast<uintptr_t>(bp.vals) & 15) == 0;
+    const uint64_t pol_a = policy_evict_first(), pol_x = policy_evict_last();
+    auto cnt_of = [&](int k) { return min(B::CH, nb - k * B::CH); };
+    auto col_of = [&](int k) -> int {
+      if (k >= nch) return 0;
+      const int c = cnt_of(k);
+      return __ldg(bp.col + r0 + (int64_t)k * B::CH + min(lane, c - 1));   // past the chunk: its last column
+    };
+    // chunk k -> buffers buf: A (one bulk copy, or registers for ragged rows) and the X records
+    // (gather4 by groups of 4 blocks), all completing on bar[buf]
+    auto issue = [&](int k, int buf, int jk) {
+      const int cnt = cnt_of(k), ng = (cnt + 3) >> 2;
+      const float *src = bp.vals + (r0 + (int64_t)k * B::CH) * B::DD;
+      float *dst = sA + buf * C::SAB;
+      const int g0 = __shfl_sync(0xffffffffu, jk, (4 * lane) & 31), g1 = __shfl_sync(0xffffffffu, jk, (4 * lane + 1) & 31);
+      const int g2 = __shfl_sync(0xffffffffu, jk, (4 * lane + 2) & 31), g3 = __shfl_sync(0xffffffffu, jk, (4 * lane + 3) & 31);
+      if (lane == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive_expect_tx(&bar[buf], (uint32_t)((tma ? cnt * B::DD * 4 : 0) + ng * 4 * B::DSS * 4));
+      }
+      __syncwarp();
+      if (lane < ng) tma_gather4(sXr + buf * C::SXB + lane * C::GS, &tmX, &bar[buf], 0, g0, g1, g2, g3, pol_x);
+      if (tma) {
+        if (lane == 0) bulk_load(dst, src, (uint32_t)(cnt * B::DD * 4), &bar[buf], pol_a);
+      } else {
+        for (int e = lane; e < cnt * B::DD; e += 32) dst[e] = __ldcs(src + e);
+      }
+    };
+    int jn = col_of(1);
+    issue(0, 0, col_of(0));
+    for (int k = 0; k < nch; ++k) {
+      const int buf = k & 1;
+      const int jnn = col_of(k + 2);
+      if (k + 1 < nch) issue(k + 1, buf ^ 1, jn);
+      mbar_wait(&bar[buf], (uint32_t)((k >> 1) & 1));
+      __syncwarp();   // register-path A stores of this chunk (ragged rows) visible to all lanes
+      if (lane < cnt_of(k)) {
+        const float *xr = sXr + buf * C::SXB + (lane >> 2) * C::GS + (lane & 3) * B::DSS;
+        uint64_t rec[B::DS / 2];
+#pragma unroll
+        for (int q = 0; q < B::Q4; ++q) {
+          const ulonglong2 v = *reinterpret_cast<const ulonglong2 *>(xr + 4 * q);
+          rec[2 * q] = v.x;
+          rec[2 * q + 1] = v.y;
+        }
+        const float *ab = sA + buf * C::SAB + lane * B::DD;
+#pragma unroll
+        for (int a = 0; a < D; ++a)
+#pragma unroll
+          for (int c = 0; c < D; ++c) {
+            const float av = ab[a * D + c];
+            const uint64_t b2 = bpack(av, av);
+#pragma unroll
+            for (int t = 0; t < B::NKP; ++t) acc2[a][t] = bffma2(b2, rec[(c * B::DP) / 2 + t], acc2[a][t]);
+          }
+      }
+      __syncwarp();   // buffers `buf` are free for chunk k + 2
+      jn = jnn;
+    }
+  }
+  float *sX = scr, *sG = sX + B::EP, *sH = sG + B::EP, *sS = sH + B::EP, *sM = sS + B::EP;
+#pragma unroll
+  for (int a = 0; a < D; ++a)
+#pragma unroll
+    for (int t = 0; t < B::NKP; ++t) {
+      float lo, hi;
+      bunpack(acc2[a][t], lo, hi);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        lo += __shfl_xor_sync(0xffffffffu, lo, o);
+        hi += __shfl_xor_sync(0xffffffffu, hi, o);
+      }
+      if (lane == 0 && t < B::KP) {
+        sG[a * D + 2 * t] = lo;
+        if (2 * t + 1 < D) sG[a * D + 2 * t + 1] = hi;
+      }
+    }
+  __syncwarp();
+  double g1s[B::DDL], g2s[B::DDL], so = 0.0, xs = 0.0;
+  float ns_region = 0.f;
+  int err = 0;
+  node_epilogue<float, D, 1, MODE>(p, static_cast<const float *>(p.X), p.Xout, lane, il, nvalid, sX, sG, sH, sS, sM,
+                                   g1s, g2s, so, xs, ns_region, err);
+  if (err) atomicOr(p.err, err);
+  if (lane == 0 && ns_region > 0.f) atomicMax(p.ns_region, __float_as_uint(ns_region));
+  bsr_partials<B::NPART, C::W>(p, red, flag, warp, lane, g1s, g2s, B::DD, B::DDL, so, xs);
+}
+
 // ---------------------------------------------------------------------------------- slab pass
 // Rows sorted by column (the generator's layout), d <= 6: the CTA's W rows walk their sorted
 // block lists in lockstep, and one producer warp streams the X records of each column group of
@@ -781,8 +932,35 @@ cudaError_t bsr_slab_launch(const BsrParams &bp, int lg2g, cudaStream_t s) {
   }
 }
 
+template <int D, int MODE>
+cudaError_t bsr_g4_launch(const BsrParams &bp, const CUtensorMap *tmX, cudaStream_t s) {
+  if constexpr (D <= 6) {
+    using C = BsrG4Cfg<D>;
+    auto kern = bsr_g4_kernel<D, MODE>;
+    static bool attr = false;
+    if (!attr) {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+      if (e != cudaSuccess) return e;
+      attr = true;
+    }
+    const unsigned grid = (unsigned)((bp.e.n_local + C::W - 1) / C::W);
+    kern<<<grid, 32 * C::W, C::SMEM, s>>>(*tmX, bp);
+    return cudaGetLastError();
+  } else {
+    return cudaErrorInvalidValue;
+  }
+}
+
 template <int D>
-cudaError_t bsr_mode_switch(int mode, const BsrParams &bp, int lg2g, cudaStream_t s) {
+cudaError_t bsr_mode_switch(int mode, const BsrParams &bp, int lg2g, const CUtensorMap *tmX, cudaStream_t s) {
+  if (lg2g < 0 && tmX && D <= 6) {
+    switch (mode) {
+      case kModeRgs: return bsr_g4_launch<D, kModeRgs>(bp, tmX, s);
+      case kModeObjective: return bsr_g4_launch<D, kModeObjective>(bp, tmX, s);
+      case kModeGpm: return bsr_g4_launch<D, kModeGpm>(bp, tmX, s);
+      default: return bsr_g4_launch<D, kModeProduct>(bp, tmX, s);
+    }
+  }
   if (lg2g >= 0) {
     switch (mode) {
       case kModeRgs: return bsr_slab_launch<D, kModeRgs>(bp, lg2g, s);
@@ -835,10 +1013,10 @@ int bsr_slab_lg2g(int d, double p_eff) {
   return lg;
 }
 
-cudaError_t bsr_dispatch(int d, int mode, const BsrParams *bp, int lg2g, cudaStream_t s) {
+cudaError_t bsr_dispatch(int d, int mode, const BsrParams *bp, int lg2g, const CUtensorMap *tmX, cudaStream_t s) {
   switch (d) {
 #define NSRGS_BSR_CASE(DV) \
-  case DV: return bsr_mode_switch<DV>(mode, *bp, lg2g, s);
+  case DV: return bsr_mode_switch<DV>(mode, *bp, lg2g, tmX, s);
     NSRGS_BSR_CASE(2)
     NSRGS_BSR_CASE(3)
     NSRGS_BSR_CASE(4)

@@ -35,7 +35,7 @@ cudaError_t sym_dispatch(int d, int mode, bool shape_only, SymShape *shape, cons
 int bsr_xs_stride(int d, bool slab);
 int bsr_grid(int d, int64_t n_local);
 int bsr_slab_lg2g(int d, double p_eff);
-cudaError_t bsr_dispatch(int d, int mode, const BsrParams *bp, int lg2g, cudaStream_t s);
+cudaError_t bsr_dispatch(int d, int mode, const BsrParams *bp, int lg2g, const CUtensorMap *tmX, cudaStream_t s);
 cudaError_t launch_bsr_pack_x(int d, const void *X, float *Xs, int64_t n, int64_t rows_local, int64_t tpr, bool slab,
                               cudaStream_t s);
 cudaError_t launch_bsr_count(int64_t n, int64_t node0, int64_t n_local, uint64_t seed, double p_obs, int64_t *cnt,

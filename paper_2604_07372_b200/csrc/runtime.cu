@@ -147,6 +147,8 @@ struct nsrgs_ctx {
   bool bsr = false, own_bsr = false;
   bool bsr_sorted = false;        // every row's columns non-decreasing (generator layout): slab pass
   int bsr_lg2g = -1;              // slab pass column-group size (log2), -1: per-block gather pass
+  bool bsr_g4 = false;            // per-block gather by TMA tile::gather4 (tmXs over the padded X copy)
+  CUtensorMap tmXs;
   int64_t *bsr_rowptr = nullptr;
   int *bsr_col = nullptr;
   float *bsr_vals = nullptr;
@@ -443,11 +445,11 @@ int launch_panel(nsrgs_ctx *c, int mode, const void *Xin, void *Xout, double *re
     bp.vals = c->bsr_vals;
     if (c->d <= kMaxNarrowD) {   // X^t -> padded node-major records for the per-lane gathers
       CUDA_TRY(c, launch_bsr_pack_x(c->d, Xin, c->bsr_xs, c->n, c->plan.rows_local, c->plan.tiles_per_rank,
-                                    c->bsr_lg2g >= 0, c->stream));
+                                    c->bsr_lg2g >= 0 || c->bsr_g4, c->stream));
       c->kernel_launches++;
       bp.Xs = c->bsr_xs;
     }
-    CUDA_TRY(c, bsr_dispatch(c->d, mode, &bp, c->bsr_lg2g, c->stream));
+    CUDA_TRY(c, bsr_dispatch(c->d, mode, &bp, c->bsr_lg2g, c->bsr_g4 ? &c->tmXs : nullptr, c->stream));
   } else if (c->sym) {
     SymParams sp{};
     sp.e = p;
@@ -527,6 +529,30 @@ int bsr_scratch(nsrgs_ctx *c) {
   const char *env = std::getenv("NSRGS_BSR_SLAB");
   const double p_eff = (double)c->bsr_nnzb / ((double)c->plan.n_local * (double)c->n);
   c->bsr_lg2g = (c->bsr_sorted && !(env && env[0] == '0')) ? bsr_slab_lg2g(c->d, p_eff) : -1;
+  const char *env4 = std::getenv("NSRGS_BSR_G4");
+  // opt-in (measured slower than the LSU gather at n 20000: d 5 p 0.5 4.40 vs 4.14 ms, d 3 2.39 vs
+  // 1.86 ms; p 0.1 1.18 vs 1.23 ms — the TMA unit's per-operation cost dominates 4-row gathers)
+  c->bsr_g4 = c->bsr_lg2g < 0 && c->d <= 6 && env4 && env4[0] == '1';
+  if (c->bsr_g4) {   // the padded X copy as an n x DSS tensor, one row (record) per gathered box row
+    static EncodeTiledFn encode = nullptr;
+    if (!encode) {
+      void *fn = nullptr;
+      cudaDriverEntryPointQueryResult q;
+      CUDA_TRY(c, cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+      if (!fn || q != cudaDriverEntryPointSuccess)
+        return set_err(c, NSRGS_ERR_CUDA, "cuTensorMapEncodeTiled not available from the driver");
+      encode = reinterpret_cast<EncodeTiledFn>(fn);
+    }
+    const int dss = bsr_xs_stride(c->d, true);
+    cuuint64_t dims[2] = {(cuuint64_t)dss, (cuuint64_t)c->n};
+    cuuint64_t strides[1] = {(cuuint64_t)dss * 4};
+    cuuint32_t box[2] = {(cuuint32_t)dss, 1u};
+    cuuint32_t estr[2] = {1u, 1u};
+    CUresult r = encode(&c->tmXs, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, c->bsr_xs, dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) c->bsr_g4 = false;   // fall back to the LSU gather
+  }
   return NSRGS_OK;
 }
 
@@ -1394,6 +1420,7 @@ int nsrgs_get_stats(nsrgs_ctx *c, nsrgs_stats_t *o) {
   o->bsr = c->bsr ? 1 : 0;
   o->bsr_nnzb = c->bsr ? c->bsr_nnzb : 0;
   o->bsr_slab = (c->bsr && c->bsr_lg2g >= 0) ? 1 : 0;
+  o->bsr_g4 = (c->bsr && c->bsr_g4) ? 1 : 0;
   o->p2p = c->p2p ? 1 : 0;
   return NSRGS_OK;
 }

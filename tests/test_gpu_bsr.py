@@ -131,6 +131,30 @@ def test_bsr_slab_pass_equals_gather_pass(nsrgs, monkeypatch, n, d, p):
         assert rel_fro(out[0][0], Xo) <= 1e-6
 
 
+@pytest.mark.parametrize("n,d,p", [(3000, 5, 0.5), (2000, 3, 0.2), (800, 2, 0.6), (700, 6, 0.3), (500, 4, 0.05)])
+def test_bsr_gather4_pass_equals_lsu_gather(nsrgs, monkeypatch, n, d, p):
+    """X records by TMA tile::gather4 vs the LSU gather: same blocks, same per-lane order ->
+    identical X^{t+1}; against the oracle for the small cases."""
+    sigma, K = 0.4, 3
+    X = oracle_iterate_near(inst.ground_truth(13, n, d), 0.2, 4).astype(np.float32)
+    out = []
+    for g4 in ("1", "0"):
+        monkeypatch.setenv("NSRGS_BSR_G4", g4)
+        s = nsrgs.Solver(n, d)
+        s.generate(13, sigma, want_Z=False, p=p, storage="bsr")
+        assert s.stats()["bsr_g4"] == (g4 == "1")
+        s.set_X(X)
+        f = s.step(1.0 / (n * p), K)
+        out.append((s.get_X(), f))
+        s.close()
+    assert np.array_equal(out[0][0], out[1][0])
+    assert abs(out[0][1] - out[1][1]) <= 1e-12 * abs(out[1][1])
+    if n <= 1000:
+        A = inst.measurement_matrix(13, inst.ground_truth(13, n, d), sigma, p=p)
+        Xo, _, _ = ons.step(A, X.astype(np.float64), 1.0 / (n * p), K)
+        assert rel_fro(out[0][0], Xo) <= 1e-6
+
+
 def test_bsr_matches_dense_pass(nsrgs):
     """Same instance in both storages: T iterations agree to fp32 summation-order noise."""
     n, d, sigma, p, K, T = 500, 5, 0.6, 0.5, 5, 20
