@@ -777,28 +777,33 @@ template <int D>
 struct BsrWideCfg {
   static constexpr int DD = D * D;
   static constexpr int D4 = (D + 3) / 4 * 4;            // smem row stride (float4 broadcast reads)
-  static constexpr int CHW = 2;                          // blocks per chunk
+  static constexpr int CHW = 2;                          // blocks per chunk (per warp)
   static constexpr int LD = (CHW * DD + 31) / 32;
-  static constexpr int W = 4;                            // warps (nodes) per CTA
+  static constexpr int W = 8;                            // warps splitting ONE node row (CTA = node)
   static constexpr int E = DD, EP = (DD + 3) / 4 * 4;
   static constexpr int DDL = (DD + 31) / 32;
   static constexpr int NPART = 2 * DD + 2;
   static constexpr int SA = CHW * D * D4;
-  static constexpr int SMEM = W * (SA + 5 * EP) * 4 + W * NPART * 8 + 16;
+  static constexpr int SRED = W * D * 32;                // per-warp partial B rows (lane = component)
+  static constexpr int SMEM = (W * SA + SRED + 5 * EP) * 4 + W * NPART * 8 + 16;
 };
 
+// One CTA per node row; its W warps take the row's blocks round-robin by chunks of CHW (the
+// Table 1 sizes have n = 500 rows: one warp per row left ~3 warps per SM), and warp 0 sums the
+// W partial B_i in fixed order and runs the epilogue.
 template <int D, int MODE>
-__global__ void __launch_bounds__(128) bsr_wide_kernel(const BsrParams bp) {
+__global__ void __launch_bounds__(32 * BsrWideCfg<D>::W) bsr_wide_kernel(const BsrParams bp) {
   using C = BsrWideCfg<D>;
   extern __shared__ float4 smem4[];
   float *smem = reinterpret_cast<float *>(smem4);
   const PanelParams &p = bp.e;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   float *sA = smem + warp * C::SA;
-  float *scr = smem + C::W * C::SA + warp * 5 * C::EP;
-  double *red = reinterpret_cast<double *>(smem + C::W * (C::SA + 5 * C::EP));
+  float *sred = smem + C::W * C::SA;                     // [W][D][32]
+  float *scr = sred + C::SRED;
+  double *red = reinterpret_cast<double *>(scr + 5 * C::EP);
   int *flag = reinterpret_cast<int *>(red + C::W * C::NPART);
-  const int64_t il = (int64_t)blockIdx.x * C::W + warp;
+  const int64_t il = blockIdx.x;
   const int nvalid = il < p.n_local ? 1 : 0;
   const int kk = lane < D ? lane : D - 1;
   // zero the row padding columns once (never written by the chunk copies)
@@ -810,7 +815,7 @@ __global__ void __launch_bounds__(128) bsr_wide_kernel(const BsrParams bp) {
   const float *Xg = static_cast<const float *>(p.X);
   if (nvalid) {
     const int64_t r0 = bp.rowptr[il], r1 = bp.rowptr[il + 1];
-    for (int64_t b0 = r0; b0 < r1; b0 += C::CHW) {
+    for (int64_t b0 = r0 + (int64_t)warp * C::CHW; b0 < r1; b0 += (int64_t)C::W * C::CHW) {
       const int cnt = (int)min((int64_t)C::CHW, r1 - b0);
       const int tot = cnt * C::DD;
       const float *src = bp.vals + b0 * C::DD;
@@ -855,21 +860,32 @@ __global__ void __launch_bounds__(128) bsr_wide_kernel(const BsrParams bp) {
       __syncwarp();
     }
   }
-  float *sX = scr, *sG = sX + C::EP, *sH = sG + C::EP, *sS = sH + C::EP, *sM = sS + C::EP;
+  // the W partial rows -> smem; warp 0 sums them in warp order (deterministic)
 #pragma unroll
   for (int a = 0; a < D; ++a) {
     float lo, hi;
     bunpack(acc2[a], lo, hi);
-    if (lane < D) sG[a * D + lane] = lo + hi;   // entry (a, b = lane) of B_i
+    sred[(warp * D + a) * 32 + lane] = lo + hi;
   }
-  __syncwarp();
+  __syncthreads();
   double g1s[C::DDL], g2s[C::DDL], so = 0.0, xs = 0.0;
-  float ns_region = 0.f;
-  int err = 0;
-  node_epilogue<float, D, 1, MODE>(p, Xg, p.Xout, lane, il, nvalid, sX, sG, sH, sS, sM, g1s, g2s, so, xs, ns_region,
-                                   err);
-  if (err) atomicOr(p.err, err);
-  if (lane == 0 && ns_region > 0.f) atomicMax(p.ns_region, __float_as_uint(ns_region));
+#pragma unroll
+  for (int m = 0; m < C::DDL; ++m) g1s[m] = g2s[m] = 0.0;
+  if (warp == 0) {
+    float *sX = scr, *sG = sX + C::EP, *sH = sG + C::EP, *sS = sH + C::EP, *sM = sS + C::EP;
+    for (int a = 0; a < D; ++a) {
+      float t = 0.f;
+      for (int w = 0; w < C::W; ++w) t += sred[(w * D + a) * 32 + lane];
+      if (lane < D) sG[a * D + lane] = t;   // entry (a, b = lane) of B_i
+    }
+    __syncwarp();
+    float ns_region = 0.f;
+    int err = 0;
+    node_epilogue<float, D, 1, MODE>(p, Xg, p.Xout, lane, il, nvalid, sX, sG, sH, sS, sM, g1s, g2s, so, xs, ns_region,
+                                     err);
+    if (err) atomicOr(p.err, err);
+    if (lane == 0 && ns_region > 0.f) atomicMax(p.ns_region, __float_as_uint(ns_region));
+  }
   bsr_partials<C::NPART, C::W>(p, red, flag, warp, lane, g1s, g2s, C::DD, C::DDL, so, xs);
 }
 
@@ -907,7 +923,7 @@ cudaError_t bsr_launch(const BsrParams &bp, cudaStream_t s) {
       if (e != cudaSuccess) return e;
       attr = true;
     }
-    const unsigned grid = (unsigned)((bp.e.n_local + C::W - 1) / C::W);
+    const unsigned grid = (unsigned)bp.e.n_local;   // one CTA per node row
     kern<<<grid, 32 * C::W, C::SMEM, s>>>(bp);
   }
   return cudaGetLastError();
@@ -986,7 +1002,7 @@ int bsr_xs_stride(int d, bool slab) {   // floats per node record of the padded 
 }
 
 int bsr_grid(int d, int64_t n_local) {
-  const int w = d <= 6 ? 4 : d <= kMaxNarrowD ? 2 : 4;
+  const int w = d <= 6 ? 4 : d <= kMaxNarrowD ? 2 : 1;   // wide: one CTA per node row
   return (int)((n_local + w - 1) / w);
 }
 
