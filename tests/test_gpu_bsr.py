@@ -304,3 +304,40 @@ def test_bsr_bench_size_sampled(nsrgs):
     Xo = ons.step_rows(R, X.astype(np.float64), nodes, 1.0 / (n * p), K)
     assert rel_fro(Xg[nodes], Xo) <= 1e-6
     s.close()
+
+
+def test_bsr_c4_size_sampled(nsrgs):
+    """n = 12000, d = 10, p = 0.5 (two lanes per block, 16-block chunks): one step, sampled nodes
+    against the oracle on independently regenerated rows."""
+    n, d, p, K = 12000, 10, 0.5, 6
+    sigma = 0.2 * np.sqrt(n) / d
+    s = nsrgs.Solver(n, d)
+    s.generate(1, sigma, want_Z=False, p=p, storage="bsr")
+    Z = inst.ground_truth(1, n, d)
+    X = oracle_iterate_near(Z, 0.1, 2).astype(np.float32)
+    s.set_X(X)
+    s.step(1.0 / (n * p), K)
+    Xg = s.get_X()
+    nodes = np.array([0, 5, 4097, 9999, n - 1])
+    R = inst.measurement_rows(1, Z, sigma, nodes, p=p)
+    Xo = ons.step_rows(R, X.astype(np.float64), nodes, 1.0 / (n * p), K)
+    assert rel_fro(Xg[nodes], Xo) <= 1e-6
+    s.close()
+
+
+@pytest.mark.parametrize("n,d,p", [(2, 3, 1.0), (3, 5, 1.0), (4, 2, 0.5), (2, 25, 1.0)])
+def test_bsr_tiny_instances(nsrgs, n, d, p):
+    """Degenerate sizes: a row has 0-3 observed blocks plus padding; step and objective match the
+    oracle (and an unobserved pair gives an all-zero row)."""
+    s = nsrgs.Solver(n, d)
+    s.generate(21, 0.3, want_Z=False, p=p, storage="bsr")
+    Z = inst.ground_truth(21, n, d)
+    A = inst.measurement_matrix(21, Z, 0.3, p=p)
+    X = oracle_iterate_near(Z, 0.2, 1).astype(np.float32)
+    s.set_X(X)
+    f = s.step(1.0 / (n * p), 3)
+    Xo, _, _ = ons.step(A, X.astype(np.float64), 1.0 / (n * p), 3)
+    assert rel_fro(s.get_X(), Xo) <= 1e-6
+    fo = ons.objective(A, X.astype(np.float64))
+    assert abs(f - fo) <= 2e-6 * abs(fo) + 1e-9
+    s.close()
