@@ -41,6 +41,8 @@ struct PanelParams {
   int world, rank;
   int panels, total_tiles;   // total_tiles = column tiles per panel (all ranks' slices)
   float a_keep;         // fraction of A accesses tagged L2 evict_last (A shard ~ L2 size), else evict_first
+  int keep_panels;      // > 0: panels [0, keep_panels) always evict_last, the rest evict_first (an
+                        // address-deterministic resident subset; replaces the random fraction)
   double coef;          // n - 1   (identity term of G_i)
   double eta;           // step size mu
   int K;                // Newton-Schulz steps (Algorithm 1)

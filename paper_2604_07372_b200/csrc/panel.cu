@@ -183,7 +183,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == kWarps) {
     if (lane == 0) {
       prefetch_tmap(&tmA);
-      const uint64_t pol_a = p.a_keep > 0.f ? policy_keep_fraction(p.a_keep) : policy_evict_first();
+      const uint64_t pol_frac = p.a_keep > 0.f ? policy_keep_fraction(p.a_keep) : policy_evict_first();
+      const uint64_t pol_keep = policy_evict_last(), pol_stream = policy_evict_first();
       const uint64_t pol_x = policy_evict_last();
       int stage = 0;
       uint32_t phase = 0;
@@ -200,6 +201,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         const int it = kg / p.nunits;
         const int4 u = __ldg(p.units + (kg - it * p.nunits));
+        const uint64_t pol_a = p.keep_panels > 0 ? (u.x < p.keep_panels ? pol_keep : pol_stream) : pol_frac;
         const T *Xin = static_cast<const T *>((it & 1) ? p.Xout : p.X);
         unsigned long long *ts = p.ts ? p.ts + ((int64_t)it * gridDim.x + blockIdx.x) * kTsSlots : nullptr;
         if (ts && it != ts_it) { ts[0] = globaltimer(); ts_it = it; }

@@ -134,6 +134,7 @@ struct nsrgs_ctx {
   PanelShape shape{};
   int sm_count = 0, grid = 0, panels = 0, total_tiles = 0;
   float a_keep = 0.f;   // L2 evict_last fraction for A (only when the shard is within ~4x of L2)
+  int keep_panels = 0;  // dense pass: panels [0, keep_panels) evict_last (deterministic resident subset)
   // symmetric half-storage pass (sym.cu)
   bool sym = false;
   SymShape symshape{};
@@ -424,6 +425,7 @@ int launch_panel(nsrgs_ctx *c, int mode, const void *Xin, void *Xout, double *re
   p.panels = c->panels;
   p.total_tiles = c->total_tiles;
   p.a_keep = c->a_keep;
+  p.keep_panels = c->keep_panels;
   p.coef = (double)(c->n - 1);
   p.eta = eta;
   p.K = K;
@@ -760,15 +762,25 @@ int nsrgs_create(const nsrgs_desc *desc, nsrgs_ctx **out) {
     int l2 = 0;
     cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, c->device);
     const double a_bytes = (double)c->esz * (double)c->plan.rows_local * (double)c->N;
-    // Share of A tagged evict_last so that part of it stays L2-resident across passes.
-    // Measured on B200 (tools/keep_sweep.sh, coop per-iteration time): best kept bytes are
-    // ~0.55 L2 for A <= 1.5 L2 (n=2000 d=3, 144 MB: 22.8 us vs 31.3 without, 31.9 keeping
-    // 0.7 L2 — over-keeping thrashes), ~0.4 L2 up to 2.8 L2 (324 MB: 49.7 vs 57.1 us), none
-    // beyond (400 MB: keeping anything is 3 % slower).
+    // Part of A stays L2-resident across passes: the first panels (an address-deterministic
+    // subset of ~0.45 L2) are loaded evict_last, the rest evict_first.  Measured on B200 (coop
+    // per-iteration time, tools/keep_sweep2.sh): n=2000 d=3 (144 MB) 22.1 us vs 23.1 with the
+    // earlier random-fraction policy (createpolicy.fractional, best at 0.55 L2) and 31.3 with
+    // none; 324 MB 56.3 vs 59.3 us; keeping more than ~0.5 L2 thrashes (0.7: 27.1 us), as the
+    // evict_last capacity is about half of the split L2.  None beyond 2.8 L2 (400 MB: keeping
+    // anything was 3 % slower).
     const double ratio = a_bytes / std::max(1.0, (double)l2);
+    const double panel_bytes = (double)c->esz * (double)c->shape.rows * (double)c->N;
+    if (ratio <= 2.8) c->keep_panels = (int)(0.45 * (double)l2 / std::max(1.0, panel_bytes));
+    // the symmetric and wide passes keep the random-fraction policy (0.55 / 0.4 L2 of A)
     const double kept = ratio <= 1.5 ? 0.55 * l2 : ratio <= 2.8 ? 0.4 * l2 : 0.0;
     c->a_keep = (float)std::min(1.0, kept / std::max(1.0, a_bytes));
-    if (const char *ek = std::getenv("NSRGS_A_KEEP")) c->a_keep = (float)std::atof(ek);   // tuning experiments
+    if (const char *ek = std::getenv("NSRGS_A_KEEP")) {   // experiment: the random-fraction policy
+      c->a_keep = (float)std::atof(ek);
+      c->keep_panels = 0;
+    }
+    if (const char *kp = std::getenv("NSRGS_KEEP_L2_FRAC"))   // experiment: kept share of L2
+      c->keep_panels = (int)(std::atof(kp) * (double)l2 / std::max(1.0, panel_bytes));
   }
   auto alloc = [&](void **p, size_t bytes) {
     cudaError_t e = cudaMalloc(p, bytes);
