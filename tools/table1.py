@@ -11,6 +11,7 @@ ROWS = [(1.0, 0.02, 4.38e-3, 0.154, 0.282), (1.0, 0.1, 2.19e-2, 0.158, 0.287), (
         (0.8, 0.02, 4.90e-3, 0.158, 0.292), (0.8, 0.1, 2.45e-2, 0.163, 0.302), (0.8, 0.2, 4.91e-2, 0.234, 0.423),
         (0.5, 0.02, 6.21e-3, 0.241, 0.420), (0.5, 0.1, 3.11e-2, 0.244, 0.422), (0.5, 0.2, 6.21e-2, 0.240, 0.434)]
 n, d = 500, 25
+TOL = float(os.environ.get("TABLE1_INIT_TOL", "1e-6"))
 st = torch.cuda.current_stream()
 for p, sigma, rel_paper, t_rgs_paper, t_gpm_paper in ROWS:
     out = {"p": p, "sigma": sigma, "rel_err_paper": rel_paper}
@@ -21,13 +22,16 @@ for p, sigma, rel_paper, t_rgs_paper, t_gpm_paper in ROWS:
         for rep in range(3):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(st)
-            s.init_spectral(0, 200, 1e-6, allow_unconverged=True)
+            sw = s.init_spectral(0, 200, TOL, allow_unconverged=True)
+            e_mid = torch.cuda.Event(enable_timing=True)
+            e_mid.record(st)
             it, tr = s.solve(alg, max_iter=100, eta=1.0 / (n * p), K=1, stop_tol=1e-8)
             e1.record(st)
             torch.cuda.synchronize()
             ms = e0.elapsed_time(e1)
-            best = ms if best is None else min(best, ms)
-        out[alg] = {"rel_err": s.alignment_error(Z)[0], "iters": it, "solve_ms_b200": round(best, 3),
-                    "solve_s_paper_cpu": tp}
+            if best is None or ms < best:
+                best, init_ms = ms, e0.elapsed_time(e_mid)
+        out[alg] = {"rel_err": s.alignment_error(Z)[0], "iters": it, "init_sweeps": sw, "init_ms": round(init_ms, 3),
+                    "solve_ms_b200": round(best, 3), "solve_s_paper_cpu": tp}
     print(json.dumps(out), flush=True)
     s.close()
