@@ -28,6 +28,8 @@
 // blocks broadcast from smem, X_j column k read coalesced from the (row-major) wide X layout.
 // Partials (objective / Gram terms): per-CTA slots, last CTA reduces in fixed order
 // (bitwise-deterministic; the node -> warp assignment is static).
+#include <cstdlib>
+
 #include "common.cuh"
 #include "epilogue.cuh"
 #include "kernels.h"
@@ -593,21 +595,23 @@ __global__ void __launch_bounds__(32 * BsrG4Cfg<D>::W) bsr_g4_kernel(const __gri
 // its slab (full), so arrivals never run ahead of the slot's phase; it waits at most for groups
 // below its own release point + S - 1 (chunks spanning more groups are processed in windows),
 // so the ring cannot deadlock.
-template <int D>
+// Two ring shapes (same 36 KB): 4 slots of 9 KB (G <= 64 at d = 5), the default for p >= 0.75,
+// and 8 slots of 4.5 KB (G <= 32: more groups of slack between the CTA's rows), opt-in.
+template <int D, int RS = 4>
 struct BsrSlabCfg {
   using B = BsrCfg<D>;
   static constexpr int W = 8;                  // consumer warps (rows) per CTA
   static constexpr int NW = W + 1;             // + producer warp
-  static constexpr int S = 4;                  // slab slots
-  static constexpr int SLAB = 2304;            // floats per slot (9 KB)
+  static constexpr int S = RS;                 // slab slots
+  static constexpr int SLAB = RS == 4 ? 2304 : 1152;   // floats per slot (9 KB / 4.5 KB)
   static constexpr int GMAX = SLAB / B::DSS;    // nodes per column group, at most
   static constexpr int SMEM = (S * SLAB + W * (2 * B::SAB + 5 * B::EP)) * 4 + NW * B::NPART * 8 + (2 * S + 2 * W) * 8 + 16;
 };
 
-template <int D, int MODE>
-__global__ void __launch_bounds__(32 * BsrSlabCfg<D>::NW) bsr_slab_kernel(const BsrParams bp, int lg2g) {
+template <int D, int MODE, int RS>
+__global__ void __launch_bounds__(32 * BsrSlabCfg<D, RS>::NW) bsr_slab_kernel(const BsrParams bp, int lg2g) {
   using B = BsrCfg<D>;
-  using C = BsrSlabCfg<D>;
+  using C = BsrSlabCfg<D, RS>;
   extern __shared__ float4 smem4[];
   float *smem = reinterpret_cast<float *>(smem4);
   const PanelParams &p = bp.e;
@@ -929,11 +933,11 @@ cudaError_t bsr_launch(const BsrParams &bp, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-template <int D, int MODE>
+template <int D, int MODE, int RS>
 cudaError_t bsr_slab_launch(const BsrParams &bp, int lg2g, cudaStream_t s) {
   if constexpr (D <= 6) {
-    using C = BsrSlabCfg<D>;
-    auto kern = bsr_slab_kernel<D, MODE>;
+    using C = BsrSlabCfg<D, RS>;
+    auto kern = bsr_slab_kernel<D, MODE, RS>;
     static bool attr = false;
     if (!attr) {
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
@@ -977,12 +981,21 @@ cudaError_t bsr_mode_switch(int mode, const BsrParams &bp, int lg2g, const CUten
       default: return bsr_g4_launch<D, kModeProduct>(bp, tmX, s);
     }
   }
-  if (lg2g >= 0) {
+  if (lg2g >= 0) {   // bits 0-7: log2 group size; bit 8: 8-slot ring
+    const int lg = lg2g & 0xff;
+    if (lg2g & 0x100) {
+      switch (mode) {
+        case kModeRgs: return bsr_slab_launch<D, kModeRgs, 8>(bp, lg, s);
+        case kModeObjective: return bsr_slab_launch<D, kModeObjective, 8>(bp, lg, s);
+        case kModeGpm: return bsr_slab_launch<D, kModeGpm, 8>(bp, lg, s);
+        default: return bsr_slab_launch<D, kModeProduct, 8>(bp, lg, s);
+      }
+    }
     switch (mode) {
-      case kModeRgs: return bsr_slab_launch<D, kModeRgs>(bp, lg2g, s);
-      case kModeObjective: return bsr_slab_launch<D, kModeObjective>(bp, lg2g, s);
-      case kModeGpm: return bsr_slab_launch<D, kModeGpm>(bp, lg2g, s);
-      default: return bsr_slab_launch<D, kModeProduct>(bp, lg2g, s);
+      case kModeRgs: return bsr_slab_launch<D, kModeRgs, 4>(bp, lg, s);
+      case kModeObjective: return bsr_slab_launch<D, kModeObjective, 4>(bp, lg, s);
+      case kModeGpm: return bsr_slab_launch<D, kModeGpm, 4>(bp, lg, s);
+      default: return bsr_slab_launch<D, kModeProduct, 4>(bp, lg, s);
     }
   }
   switch (mode) {
@@ -1006,27 +1019,33 @@ int bsr_grid(int d, int64_t n_local) {
   return (int)((n_local + w - 1) / w);
 }
 
-// log2 of the column-group size of the slab pass for sorted rows (d <= 6) observed with
-// probability ~p_eff: about 32 / p nodes per group (one chunk of observed blocks), capped by the
-// slot size; -1: use the per-block gather pass (bsr_kernel).  Measured (n 20000, d 5): the slab
-// pass wins at p = 1 (6.84 vs 7.77 ms per pass) and loses at p <= 0.5 (4.21 vs 3.97 ms at 0.5,
-// 1.76 vs 1.23 ms at 0.1: the CTA's rows advance in lockstep through the slab ring and two
-// 9-warp CTAs per SM hide less latency than four 4-warp ones), so it is chosen for p >= 0.75.
+// Pass selection for sorted rows (d <= 6) observed with probability ~p_eff.  Returns -1 for the
+// per-block gather pass (bsr_kernel), else (ring << 8) | log2 G for the slab pass: G ~ 32 / p
+// nodes per column group (about one 32-block chunk of observed blocks), capped by the slot size.
+// Measured at n 20000 (bsr_bench, one box): d 5 p 0.9: slab-4 6.73-6.85 ms, slab-8 6.89, gather
+// 7.7-8.8; d 5 p 0.5: slab-8 4.01, slab-4 4.25, gather 4.18-4.29; d 5 p 0.3: gather 2.57, slab-8
+// 2.83; d 6 p 0.5: gather 6.16, slab-8 7.04; d 4 p 0.5: gather 3.78, slab-8 4.11; d 5 p 0.1:
+// gather 1.23, slab-4 1.76; d 3 p 0.5: gather 1.86, slab-8 2.33 (the rows advance in lockstep
+// through the ring, and two 9-warp CTAs per SM hide less latency than four 4-warp ones).  So the
+// slab pass (4 slots) is the default for p >= 0.75 only; the 8-slot ring is opt-in.
 int bsr_slab_lg2g(int d, double p_eff) {
-  if (p_eff < 0.75) return -1;
+  const char *force = std::getenv("NSRGS_BSR_SLAB");   // "4" / "8": force that ring (experiments)
+  int ring = p_eff >= 0.75 ? 4 : 0;
+  if (force && (force[0] == '4' || force[0] == '8')) ring = force[0] - '0';
+  if (!ring) return -1;
   int gmax = 0;
   switch (d) {
-    case 2: gmax = BsrSlabCfg<2>::GMAX; break;
-    case 3: gmax = BsrSlabCfg<3>::GMAX; break;
-    case 4: gmax = BsrSlabCfg<4>::GMAX; break;
-    case 5: gmax = BsrSlabCfg<5>::GMAX; break;
-    case 6: gmax = BsrSlabCfg<6>::GMAX; break;
+    case 2: gmax = (ring == 4 ? BsrSlabCfg<2, 4>::GMAX : BsrSlabCfg<2, 8>::GMAX); break;
+    case 3: gmax = (ring == 4 ? BsrSlabCfg<3, 4>::GMAX : BsrSlabCfg<3, 8>::GMAX); break;
+    case 4: gmax = (ring == 4 ? BsrSlabCfg<4, 4>::GMAX : BsrSlabCfg<4, 8>::GMAX); break;
+    case 5: gmax = (ring == 4 ? BsrSlabCfg<5, 4>::GMAX : BsrSlabCfg<5, 8>::GMAX); break;
+    case 6: gmax = (ring == 4 ? BsrSlabCfg<6, 4>::GMAX : BsrSlabCfg<6, 8>::GMAX); break;
     default: return -1;
   }
   const double want = p_eff > 0.0 ? 32.0 / p_eff : 1e9;
   int lg = 3;
   while ((2 << lg) <= gmax && (double)(2 << lg) <= want) ++lg;
-  return lg;
+  return (ring == 8 ? 0x100 : 0) | lg;
 }
 
 cudaError_t bsr_dispatch(int d, int mode, const BsrParams *bp, int lg2g, const CUtensorMap *tmX, cudaStream_t s) {

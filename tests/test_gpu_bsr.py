@@ -106,19 +106,22 @@ def test_bsr_step_gpm_objective(nsrgs, n, d, sigma, p, K):
     s.close()
 
 
-@pytest.mark.parametrize("n,d,p", [(3000, 5, 0.9), (2000, 3, 0.8), (1000, 2, 1.0), (700, 6, 0.75), (500, 4, 1.0)])
-def test_bsr_slab_pass_equals_gather_pass(nsrgs, monkeypatch, n, d, p):
+@pytest.mark.parametrize("n,d,p,ring", [(3000, 5, 0.9, "1"), (2000, 3, 0.8, "1"), (1000, 2, 1.0, "1"),
+                                         (700, 6, 0.75, "1"), (500, 4, 1.0, "1"), (3000, 5, 0.5, "8"),
+                                         (900, 4, 0.35, "8"), (2000, 3, 0.5, "8"), (600, 6, 0.1, "8"),
+                                         (800, 5, 0.6, "4")])
+def test_bsr_slab_pass_equals_gather_pass(nsrgs, monkeypatch, n, d, p, ring):
     """The slab pass (sorted rows: column-group X slabs shared by the CTA's rows) and the
     per-block gather pass multiply the same blocks in the same per-lane order: identical X^{t+1};
     the objective partials differ only by the fp64 CTA grouping."""
     sigma, K = 0.4, 3
     X = oracle_iterate_near(inst.ground_truth(12, n, d), 0.2, 4).astype(np.float32)
     out = []
-    for slab in ("1", "0"):
+    for slab in (ring, "0"):   # "1": the default choice (the 4-slot ring at p >= 0.75), "4"/"8": forced ring
         monkeypatch.setenv("NSRGS_BSR_SLAB", slab)
         s = nsrgs.Solver(n, d)
         s.generate(12, sigma, want_Z=False, p=p, storage="bsr")
-        assert s.stats()["bsr_slab"] == (slab == "1")
+        assert s.stats()["bsr_slab"] == (slab != "0")
         s.set_X(X)
         f = s.step(1.0 / (n * p), K)
         out.append((s.get_X(), f))
@@ -138,6 +141,7 @@ def test_bsr_gather4_pass_equals_lsu_gather(nsrgs, monkeypatch, n, d, p):
     sigma, K = 0.4, 3
     X = oracle_iterate_near(inst.ground_truth(13, n, d), 0.2, 4).astype(np.float32)
     out = []
+    monkeypatch.setenv("NSRGS_BSR_SLAB", "0")   # the per-block gather family
     for g4 in ("1", "0"):
         monkeypatch.setenv("NSRGS_BSR_G4", g4)
         s = nsrgs.Solver(n, d)
