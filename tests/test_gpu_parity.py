@@ -278,6 +278,26 @@ def test_full_size_sampled_step(nsrgs, cfg):
     s.close()
 
 
+@pytest.mark.parametrize("cfg", ["c3", "c5"])
+def test_full_size_coop_run_equals_per_launch(nsrgs, monkeypatch, cfg):
+    """The launch configuration bench.py times (one cooperative launch for all T iterations,
+    in-kernel grid barrier) gives bitwise the X^T and objective trace of T per-iteration launches,
+    whose single steps are checked against the oracle at full size above."""
+    n, d, sigma, K = FULL[cfg]
+    Z = inst.ground_truth(0, n, d)
+    X = oracle_iterate_near(Z, 0.05, 3).astype(np.float32)
+    out = []
+    for no_coop in ("0", "1"):   # read at create: one context (and one A) at a time
+        monkeypatch.setenv("NSRGS_NO_COOP", no_coop)
+        s = nsrgs.Solver(n, d)
+        s.generate(0, sigma, want_Z=False)
+        s.set_X(X)
+        tr = s.run(3, 1.0 / n, K)
+        out.append((s.get_X(), tr))
+        s.close()
+    assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1])
+
+
 @pytest.mark.parametrize("cfg", ["c3", "c4"])
 def test_full_size_run_properties(nsrgs, cfg):
     n, d, sigma, K = FULL[cfg]
