@@ -9,6 +9,7 @@ namespace nsrgs {
 
 namespace {
 constexpr int kRedThreads = 256;
+constexpr int kChebRows = 64;   // rows per CTA of the Chebyshev combine (smem: 2 x 64 x 32 elements)
 
 template <typename T> __device__ __forceinline__ double block_sum(double v, double *sh) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -302,29 +303,32 @@ __global__ void scale_kernel(int64_t row0, int64_t rows, const double *MC, T *W,
 template <typename T>
 __global__ void cheb_combine_kernel(int d, int64_t row0, int64_t rows, double alpha, double beta, T *W,
                                     const T *Yprev, const T *Ycur, int64_t rows_local, int64_t tpr, double *part) {
-  const int64_t rl = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  // CTA = kChebRows rows: phase 1 forms this CTA's rows of Y_new (thread = row) and stages Y_new,
+  // Y_cur in smem; phase 2 forms the CTA's Gram partials entry-parallel (fixed row order)
+  __shared__ T sy[kChebRows * kMaxD], sc[kChebRows * kMaxD];
   const int DD = d * d;
-  double y[kMaxD], yc[kMaxD];
-  const bool valid = rl < rows;
-  if (valid) {
-    const int64_t r = row0 + rl;
+  const int64_t rbase = (int64_t)blockIdx.x * kChebRows;
+  const int nr = (int)min((int64_t)kChebRows, rows - rbase);
+  const int t = threadIdx.x;
+  if (t < nr) {
+    const int64_t r = row0 + rbase + t;
     for (int k = 0; k < d; ++k) {
       const int64_t ix = tile_index(r, k, d, rows_local, tpr);
       double v = alpha * (double)W[ix];
       if (beta != 0.0) v -= beta * (double)Yprev[ix];
       const T tv = (T)v;
       W[ix] = tv;
-      y[k] = (double)tv;
-      yc[k] = (double)Ycur[ix];
+      sy[t * d + k] = tv;
+      sc[t * d + k] = Ycur[ix];
     }
   }
-  // Gram partials per warp (slot = global warp index), entry by entry
-  const int64_t slot = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  for (int e = 0; e < 2 * DD; ++e) {
+  __syncthreads();
+  for (int e = t; e < 2 * DD; e += blockDim.x) {
     const int a = (e % DD) / d, b = (e % DD) % d;
-    double v = valid ? (e < DD ? y[a] : yc[a]) * y[b] : 0.0;
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if ((threadIdx.x & 31) == 0) part[slot * 2 * DD + e] = v;
+    const T *left = e < DD ? sy : sc;
+    double acc = 0.0;
+    for (int r = 0; r < nr; ++r) acc += (double)left[r * d + a] * (double)sy[r * d + b];
+    part[(int64_t)blockIdx.x * 2 * DD + e] = acc;
   }
 }
 
@@ -510,40 +514,56 @@ __global__ void gen_Y0_rt(int64_t N, int d, uint64_t seed, T *Y, int64_t rows_lo
   }
 }
 
+// One warp: right-looking Cholesky of the d x d Gram (the same subtraction order per entry as the
+// sequential left-looking form), column-parallel forward substitution for L^{-1}, then M = L^{-T}
+// and CM = Cm M entry-parallel.  (The single-thread version took 439 us at d = 25.)
 __global__ void chol_rt(int d, const double *res, double *MC, int *err) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  double L[kMaxD * kMaxD], Li[kMaxD * kMaxD];
-  for (int e = 0; e < d * d; ++e) L[e] = Li[e] = 0.0;
-  bool ok = true;
+  __shared__ double L[kMaxD][kMaxD + 1], Li[kMaxD][kMaxD + 1];
+  __shared__ int bad;
+  const int lane = threadIdx.x;
+  if (blockIdx.x != 0 || lane >= 32) return;
+  if (lane == 0) bad = 0;
+  for (int e = lane; e < kMaxD * kMaxD; e += 32) {
+    const int i = e / kMaxD, j = e % kMaxD;
+    L[i][j] = (i < d && j < d && j <= i) ? res[i * d + j] : 0.0;
+    Li[i][j] = 0.0;
+  }
+  __syncwarp();
   for (int j = 0; j < d; ++j) {
-    double s = res[j * d + j];
-    for (int k = 0; k < j; ++k) s -= L[j * d + k] * L[j * d + k];
-    if (!(s > 0.0)) { ok = false; s = 1.0; }
-    L[j * d + j] = sqrt(s);
-    for (int i = j + 1; i < d; ++i) {
-      double t = res[i * d + j];
-      for (int k = 0; k < j; ++k) t -= L[i * d + k] * L[j * d + k];
-      L[i * d + j] = t / L[j * d + j];
+    if (lane == 0) {
+      double s = L[j][j];
+      if (!(s > 0.0)) { bad = 1; s = 1.0; }
+      L[j][j] = sqrt(s);
+    }
+    __syncwarp();
+    const int i = lane;
+    if (i > j && i < d) L[i][j] /= L[j][j];
+    __syncwarp();
+    if (i > j && i < d)   // trailing update of row i: L[i][k] -= L[i][j] L[k][j], j < k <= i
+      for (int k = j + 1; k <= i; ++k) L[i][k] -= L[i][j] * L[k][j];
+    __syncwarp();
+  }
+  {
+    const int c = lane;   // column c of L^{-1}
+    if (c < d) {
+      Li[c][c] = 1.0 / L[c][c];
+      for (int i = c + 1; i < d; ++i) {
+        double t = 0.0;
+        for (int k = c; k < i; ++k) t += L[i][k] * Li[k][c];
+        Li[i][c] = -t / L[i][i];
+      }
     }
   }
-  for (int c = 0; c < d; ++c) {
-    Li[c * d + c] = 1.0 / L[c * d + c];
-    for (int i = c + 1; i < d; ++i) {
-      double t = 0.0;
-      for (int k = c; k < i; ++k) t += L[i * d + k] * Li[k * d + c];
-      Li[i * d + c] = -t / L[i * d + i];
-    }
-  }
-  for (int a = 0; a < d; ++a)
-    for (int b = 0; b < d; ++b) MC[a * d + b] = Li[b * d + a];
+  __syncwarp();
   const double *Cm = res + d * d;
-  for (int a = 0; a < d; ++a)
-    for (int b = 0; b < d; ++b) {
-      double t = 0.0;
-      for (int k = 0; k < d; ++k) t += Cm[a * d + k] * Li[b * d + k];
-      MC[d * d + a * d + b] = t;
-    }
-  if (!ok) atomicOr(err, kErrSingular);
+  for (int e = lane; e < d * d; e += 32) {
+    const int a2 = e / d, b2 = e % d;
+    MC[e] = Li[b2][a2];
+    double t = 0.0;
+    for (int k = 0; k < d; ++k) t += Cm[a2 * d + k] * Li[b2][k];
+    MC[d * d + e] = t;
+  }
+  if (lane == 0 && bad) atomicOr(err, kErrSingular);
 }
 
 template <typename T>
@@ -762,14 +782,14 @@ cudaError_t launch_cheb_combine(int dtype, int d, int64_t node0, int64_t n_local
                                 const void *Yprev, const void *Ycur, int64_t rows_local, int64_t tpr, double *part,
                                 int *nblocks, cudaStream_t s) {
   const int64_t rows = n_local * d, row0 = node0 * d;
-  const unsigned grid = nblk(rows, kRedThreads);
-  *nblocks = (int)grid * (kRedThreads / 32);   // partial slots (one per warp)
+  const unsigned grid = nblk(rows, kChebRows);
+  *nblocks = (int)grid;   // partial slots (one per CTA)
   if (dtype == 0)
-    cheb_combine_kernel<float><<<grid, kRedThreads, 0, s>>>(d, row0, rows, alpha, beta, (float *)W,
+    cheb_combine_kernel<float><<<grid, kChebRows, 0, s>>>(d, row0, rows, alpha, beta, (float *)W,
                                                                 (const float *)Yprev, (const float *)Ycur, rows_local,
                                                                 tpr, part);
   else
-    cheb_combine_kernel<double><<<grid, kRedThreads, 0, s>>>(d, row0, rows, alpha, beta, (double *)W,
+    cheb_combine_kernel<double><<<grid, kChebRows, 0, s>>>(d, row0, rows, alpha, beta, (double *)W,
                                                                  (const double *)Yprev, (const double *)Ycur,
                                                                  rows_local, tpr, part);
   return cudaGetLastError();

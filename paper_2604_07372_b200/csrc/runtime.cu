@@ -1064,7 +1064,7 @@ int nsrgs_init_spectral(nsrgs_ctx *c, uint64_t seed, int max_sweeps, double tol,
   double prev_chg = 1e300;
   int cheb_steps = 0, cheb_stall = 0;
   if (cheb_on && !c->yprev) CUDA_TRY(c, cudaMalloc(&c->yprev, c->esz * (size_t)c->plan.x_elems));
-  const int64_t ncs = ceil_div(c->plan.rows_local, 256) * 8;   // combine partial slots (per warp)
+  const int64_t ncs = ceil_div(c->plan.rows_local, 64);   // combine partial slots (per 64-row CTA)
   NSRGS_TRY(ensure_red(c, std::max<int64_t>(nbs, ncs * 2 * DD)));
   NSRGS_TRY(ensure_res(c, 1));
   for (sweeps = 1; sweeps <= max_sweeps; ++sweeps) {
