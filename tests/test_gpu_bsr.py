@@ -345,3 +345,31 @@ def test_bsr_tiny_instances(nsrgs, n, d, p):
     fo = ons.objective(A, X.astype(np.float64))
     assert abs(f - fo) <= 2e-6 * abs(fo) + 1e-9
     s.close()
+
+
+def test_bsr_error_paths(nsrgs):
+    """Block-sparse C-ABI contracts: F32 only, p in (0, 1], dense-only calls refuse while it is
+    active, get_A_bsr refuses a dense A, and a dense generate switches back."""
+    s = nsrgs.Solver(50, 3, nsrgs.F64)
+    with pytest.raises(nsrgs.NSRGSError) as e:
+        s.generate(1, 0.5, want_Z=False, p=0.5, storage="bsr")
+    assert e.value.name == "INVALID_ARG"
+    s.close()
+    s = nsrgs.Solver(50, 3)
+    for p in (0.0, 1.5, -0.1):
+        with pytest.raises(nsrgs.NSRGSError) as e:
+            s.generate(1, 0.5, want_Z=False, p=p, storage="bsr")
+        assert e.value.name == "INVALID_ARG"
+    s.generate(1, 0.5, want_Z=False)
+    with pytest.raises(nsrgs.NSRGSError) as e:
+        s.get_A_bsr()
+    assert e.value.name == "STATE"
+    s.generate(1, 0.5, want_Z=False, p=0.5, storage="bsr")
+    for call in (lambda: s.copy_A_rows(0, 3), lambda: s.set_symmetric(True)):
+        with pytest.raises(nsrgs.NSRGSError) as e:
+            call()
+        assert e.value.name == "STATE"
+    assert s.stats()["bsr"] == 1
+    s.generate(1, 0.5, want_Z=False)
+    assert s.stats()["bsr"] == 0 and s.copy_A_rows(0, 3).shape == (3, 150)
+    s.close()
