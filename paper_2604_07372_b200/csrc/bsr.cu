@@ -910,22 +910,20 @@ cudaError_t bsr_launch(const BsrParams &bp, cudaStream_t s) {
   if constexpr (D <= kMaxNarrowD) {
     using C = BsrCfg<D>;
     auto kern = bsr_kernel<D, MODE>;
-    static bool attr = false;
-    if (!attr) {
-      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    static bool attr[64] = {};
+    {
+      const cudaError_t e = set_smem_attr_once(reinterpret_cast<const void *>(kern), C::SMEM, attr);
       if (e != cudaSuccess) return e;
-      attr = true;
     }
     const unsigned grid = (unsigned)((bp.e.n_local + C::W - 1) / C::W);
     kern<<<grid, 32 * C::W, C::SMEM, s>>>(bp);
   } else {
     using C = BsrWideCfg<D>;
     auto kern = bsr_wide_kernel<D, MODE>;
-    static bool attr = false;
-    if (!attr) {
-      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    static bool attr[64] = {};
+    {
+      const cudaError_t e = set_smem_attr_once(reinterpret_cast<const void *>(kern), C::SMEM, attr);
       if (e != cudaSuccess) return e;
-      attr = true;
     }
     const unsigned grid = (unsigned)bp.e.n_local;   // one CTA per node row
     kern<<<grid, 32 * C::W, C::SMEM, s>>>(bp);
@@ -938,11 +936,10 @@ cudaError_t bsr_slab_launch(const BsrParams &bp, int lg2g, cudaStream_t s) {
   if constexpr (D <= 6) {
     using C = BsrSlabCfg<D, RS>;
     auto kern = bsr_slab_kernel<D, MODE, RS>;
-    static bool attr = false;
-    if (!attr) {
-      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    static bool attr[64] = {};
+    {
+      const cudaError_t e = set_smem_attr_once(reinterpret_cast<const void *>(kern), C::SMEM, attr);
       if (e != cudaSuccess) return e;
-      attr = true;
     }
     const unsigned grid = (unsigned)((bp.e.n_local + C::W - 1) / C::W);
     kern<<<grid, 32 * C::NW, C::SMEM, s>>>(bp, lg2g);
@@ -957,11 +954,10 @@ cudaError_t bsr_g4_launch(const BsrParams &bp, const CUtensorMap *tmX, cudaStrea
   if constexpr (D <= 6) {
     using C = BsrG4Cfg<D>;
     auto kern = bsr_g4_kernel<D, MODE>;
-    static bool attr = false;
-    if (!attr) {
-      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    static bool attr[64] = {};
+    {
+      const cudaError_t e = set_smem_attr_once(reinterpret_cast<const void *>(kern), C::SMEM, attr);
       if (e != cudaSuccess) return e;
-      attr = true;
     }
     const unsigned grid = (unsigned)((bp.e.n_local + C::W - 1) / C::W);
     kern<<<grid, 32 * C::W, C::SMEM, s>>>(*tmX, bp);

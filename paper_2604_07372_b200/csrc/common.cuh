@@ -86,6 +86,19 @@ struct BsrParams {
   const float *Xs;        // d <= 10: padded node-major copy of X^t (bsr_xs_stride(d) floats per node)
 };
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) is per device: remember it per (kernel, device)
+// (a process may drive contexts on several GPUs).  `done` is a kernel-specific static table.
+inline cudaError_t set_smem_attr_once(const void *kern, int bytes, bool (&done)[64]) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= 64) return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (done[dev]) return cudaSuccess;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done[dev] = true;
+  return e;
+}
+
 constexpr int kErrDivergence = 1;   // ||S||_F > 10 sqrt(d) or non-finite after NS
 constexpr int kErrSingular = 2;     // init polar did not converge / Cholesky failed
 constexpr int kErrNonfinite = 4;

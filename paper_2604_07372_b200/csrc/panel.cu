@@ -580,11 +580,10 @@ template <typename T, int D, int MODE>
 static cudaError_t launch_impl(const CUtensorMap *tm, const PanelParams &p, int grid, cudaStream_t s) {
   using C = PanelCfg<T, D>;
   auto kern = panel_kernel<T, D, MODE>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+  static bool attr_set[64] = {};
+  {
+    const cudaError_t e = set_smem_attr_once(reinterpret_cast<const void *>(kern), C::SMEM, attr_set);
     if (e != cudaSuccess) return e;
-    attr_set = true;
   }
   if (p.iters > 1) {   // all CTAs must be co-resident for the in-kernel grid barrier
     CUtensorMap tmc = *tm;

@@ -463,11 +463,10 @@ static SymShape sym_shape_impl() {
 template <int D>
 static cudaError_t sym_launch_impl(const CUtensorMap *tm, const SymParams &sp, int grid, int mode, cudaStream_t s) {
   using C = SymCfg<D>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(sym_block_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+  static bool attr[64] = {};
+  {
+    const cudaError_t e = set_smem_attr_once(reinterpret_cast<const void *>(sym_block_kernel<D>), C::SMEM, attr);
     if (e != cudaSuccess) return e;
-    attr = true;
   }
   sym_block_kernel<D><<<grid, kThreads, C::SMEM, s>>>(*tm, sp);
   cudaError_t e = cudaGetLastError();

@@ -179,11 +179,10 @@ template <int D, int MODE>
 static cudaError_t wide_launch(const CUtensorMap *tm, const PanelParams &p, int grid, cudaStream_t s) {
   using C = WideCfg<D>;
   auto kern = wide_kernel<D, MODE>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+  static bool attr[64] = {};
+  {
+    const cudaError_t e = set_smem_attr_once(reinterpret_cast<const void *>(kern), C::SMEM, attr);
     if (e != cudaSuccess) return e;
-    attr = true;
   }
   kern<<<grid, C::THREADS, C::SMEM, s>>>(*tm, p);
   return cudaGetLastError();
