@@ -25,7 +25,7 @@ struct PanelParams {
                         // are contiguous in column order (= the fixed combine order)
   int nunits;
   void *Bpart;          // split-unit partial B rows [slots][kWarps][EP] (EP = RT d padded to 16 B)
-  unsigned *ucnt;       // [panels][kWarps] unit arrivals per (split panel, warp); self-resetting
+  unsigned *ucnt;       // [panels][consumer warps] unit arrivals per (split panel, warp); self-resetting
   unsigned *ctl;        // [0] unit queue head (runs over iters x nunits), [1] (panel, warp)
                         // epilogues completed (X^{t+1} readiness), [2] CTAs exited; self-resetting
   unsigned long long *acc;   // [iters][npart][2] exact 128-bit fixed-point sums (lo, hi); self-zeroing

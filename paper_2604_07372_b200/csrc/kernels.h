@@ -11,6 +11,7 @@ enum PanelMode { kModeRgs = 0, kModeObjective = 1, kModeProduct = 2, kModeGpm = 
 
 struct PanelShape {
   int rows, nodes, stages, smem, npart, threads;
+  int nw;   // consumer warps (the (panel, warp) epilogue unit count per panel)
 };
 
 // panel.cu: shape query (shape_only) or launch of the fused A.X + epilogue kernel.

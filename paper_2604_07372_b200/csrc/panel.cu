@@ -599,7 +599,7 @@ static cudaError_t launch_impl(const CUtensorMap *tm, const PanelParams &p, int 
 template <typename T, int D>
 static PanelShape shape_impl() {
   using C = PanelCfg<T, D>;
-  return PanelShape{C::ROWS, C::NODES, C::STAGES, C::SMEM, C::NPART, kThreads};
+  return PanelShape{C::ROWS, C::NODES, C::STAGES, C::SMEM, C::NPART, kThreads, kWarps};
 }
 
 #define NSRGS_PANEL_CASE(T, D)                                                               \

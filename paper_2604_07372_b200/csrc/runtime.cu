@@ -166,7 +166,7 @@ struct nsrgs_ctx {
   int4 *units = nullptr;        // [nunits] (panel, t_begin, t_end, slot)
   int2 *pinfo = nullptr;        // [panels] (units covering the panel, first slot)
   int nunits = 0, nslots = 0, split_panels = 0;
-  unsigned *ucnt = nullptr;     // [panels][kWarps]
+  unsigned *ucnt = nullptr;     // [panels][consumer warps]
   unsigned *ctl = nullptr;      // [4] queue head, epilogues done, CTAs exited
   unsigned long long *acc = nullptr;   // [acc_cap][npart][2] fixed-point sums
   int acc_cap = 0;
@@ -245,7 +245,7 @@ int sync_and_check(nsrgs_ctx *c, int *flags_out = nullptr) {
     CUDA_TRY(c, cudaMemsetAsync(c->err, 0, sizeof(int), c->stream));
     if (flags & kErrTimeout) {   // a timed-out launch may leave the dense kernel's counters dirty
       if (c->ctl) CUDA_TRY(c, cudaMemsetAsync(c->ctl, 0, sizeof(unsigned) * 4, c->stream));
-      if (c->ucnt) CUDA_TRY(c, cudaMemsetAsync(c->ucnt, 0, sizeof(unsigned) * (size_t)c->panels * kWarps, c->stream));
+      if (c->ucnt) CUDA_TRY(c, cudaMemsetAsync(c->ucnt, 0, sizeof(unsigned) * (size_t)c->panels * c->shape.nw, c->stream));
       if (c->acc) CUDA_TRY(c, cudaMemsetAsync(c->acc, 0, sizeof(unsigned long long) * 2 * (size_t)c->acc_cap * c->shape.npart, c->stream));
       CUDA_TRY(c, cudaStreamSynchronize(c->stream));
     }
@@ -392,7 +392,7 @@ int launch_panel(nsrgs_ctx *c, int mode, const void *Xin, void *Xout, double *re
   if (p2p) {   // fused exchange (one iteration per launch): see PanelParams
     const size_t off = static_cast<char *>(Xout) - static_cast<char *>(c->xblock);
     p.p2p = 1;
-    p.xtarget = c->p2p_epoch * (unsigned)c->panels * (unsigned)kWarps;
+    p.xtarget = c->p2p_epoch * (unsigned)c->panels * (unsigned)c->shape.nw;
     p.xcnt = xcnt_of(c->xblock, c->xstride);
     for (int g = 0; g < c->world; ++g) {
       p.peer_X[g] = static_cast<char *>(c->peer_block[g]) + off;
@@ -800,7 +800,7 @@ int nsrgs_create(const nsrgs_desc *desc, nsrgs_ctx **out) {
             alloc((void **)&c->err, sizeof(int)) && alloc((void **)&c->ns_region, sizeof(unsigned));
   if (ok && c->d <= kMaxNarrowD) {
     ok = alloc((void **)&c->units, sizeof(int4) * units.size()) && alloc((void **)&c->pinfo, sizeof(int2) * pinfo.size()) &&
-         alloc((void **)&c->ucnt, sizeof(unsigned) * (size_t)c->panels * kWarps) &&
+         alloc((void **)&c->ucnt, sizeof(unsigned) * (size_t)c->panels * c->shape.nw) &&
          alloc((void **)&c->ctl, sizeof(unsigned) * 4) &&
          alloc(&c->Bpart, c->esz * (size_t)std::max(1, c->nslots) * (c->shape.rows * c->d + 4 * 8));   // per-warp rows padded to 16 B
     if (ok) ok = cudaMemcpyAsync(c->units, units.data(), sizeof(int4) * units.size(), cudaMemcpyHostToDevice, c->stream) == cudaSuccess &&
@@ -1170,7 +1170,7 @@ static int run_impl(nsrgs_ctx *c, int mode, int T, double eta, int K, double *tr
     // every peer's stores into this rank's buffers have landed before the call returns
     if (!c->emulated) {
       CUDA_TRY(c, launch_p2p_wait(xcnt_of(c->xblock, c->xstride), c->world,
-                                  c->p2p_epoch * (unsigned)c->panels * (unsigned)kWarps, c->err, c->stream));
+                                  c->p2p_epoch * (unsigned)c->panels * (unsigned)c->shape.nw, c->err, c->stream));
       c->kernel_launches++;
     }
   } else if (c->coop && !c->sym && !c->bsr && T > 1) {

@@ -196,7 +196,7 @@ cudaError_t wide_dispatch(int d, int mode, bool shape_only, PanelShape *shape, c
   case DV: {                                                                                       \
     using C = WideCfg<DV>;                                                                         \
     if (shape_only) {                                                                              \
-      *shape = PanelShape{C::ROWS, C::W, C::STAGES, C::SMEM, C::NPART, C::THREADS};                \
+      *shape = PanelShape{C::ROWS, C::W, C::STAGES, C::SMEM, C::NPART, C::THREADS, C::W};          \
       return cudaSuccess;                                                                          \
     }                                                                                              \
     if (mode == kModeRgs) return wide_launch<DV, kModeRgs>(tm, *p, grid, s);                       \
