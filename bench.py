@@ -451,12 +451,15 @@ def main():
     ap.add_argument("--symmetric", action="store_true", help="symmetric half-storage pass (d <= 6, 1 GPU)")
     ap.add_argument("--no-sym-variant", action="store_true", help="skip the extra symmetric-variant measurement")
     ap.add_argument("--no-read-probe", action="store_true", help="skip the in-run read-stream peak probe")
+    ap.add_argument("--sigma", type=float, default=None, help="noise level override (c2 lists 0.5, 2 and 8)")
     ap.add_argument("--bsr-p", type=float, default=0.5, help="observation probability of the block-sparse variant")
     ap.add_argument("--no-bsr-variant", action="store_true", help="skip the block-sparse (p < 1) variant")
     args = ap.parse_args()
     if args.config is None:
         args.config = "c3"
-    cfg = CONFIGS[args.config]
+    cfg = dict(CONFIGS[args.config])
+    if args.sigma is not None:
+        cfg["sigma"] = args.sigma
     if args.impl == "reference":
         run_reference(args, cfg)
     else:
