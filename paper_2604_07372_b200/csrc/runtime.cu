@@ -117,6 +117,7 @@ struct nsrgs_ctx {
   bool own_A = false, have_A = false;
   CUtensorMap tmA;
   CUtensorMap tmA_sym;   // symmetric pass: same A, its own panel height
+  bool wide_mma = false; // d > 10: 3xTF32 tensor-core pass (A tensor map with the 128-byte swizzle)
   double a_fro2 = 0.0;
   // iterate
   void *X[2] = {nullptr, nullptr};   // both inside xblock (one IPC-shareable allocation)
@@ -377,8 +378,10 @@ int build_tmap(nsrgs_ctx *c, CUtensorMap *out = nullptr, int rows = 0) {
                            (cuuint64_t)(c->lda * c->esz)};
   cuuint32_t box[3] = {(cuuint32_t)col_tile(c->d), 1u, (cuuint32_t)rows};
   cuuint32_t estr[3] = {1u, 1u, 1u};
+  const bool swz = out == &c->tmA && c->wide_mma;   // the tensor-core wide pass reads swizzled tiles
   CUresult r = encode(out, c->dtype == NSRGS_F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64,
-                      3, c->A, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                      3, c->A, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                      swz ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return set_err(c, NSRGS_ERR_CUDA, "cuTensorMapEncodeTiled failed (CUresult %d)", (int)r);
   return NSRGS_OK;
@@ -469,7 +472,7 @@ int launch_panel(nsrgs_ctx *c, int mode, const void *Xin, void *Xout, double *re
     CUDA_TRY(c, sym_dispatch(c->d, mode, false, nullptr, &c->tmA_sym, &sp, c->sym_grid, c->stream));
     c->kernel_launches++;
   } else if (c->d > kMaxNarrowD) {
-    CUDA_TRY(c, wide_dispatch(c->d, mode, false, nullptr, &c->tmA, &p, c->grid, c->stream));
+    CUDA_TRY(c, wide_dispatch(c->d, mode, false, nullptr, &c->tmA, &p, c->grid, c->stream, c->wide_mma));
   } else {
     CUDA_TRY(c, panel_dispatch(c->dtype, c->d, mode, false, nullptr, &c->tmA, &p, c->grid, c->stream));
   }
@@ -747,7 +750,13 @@ int nsrgs_create(const nsrgs_desc *desc, nsrgs_ctx **out) {
   cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, c->device);
   if (c->d > kMaxNarrowD) {
     if (c->dtype != NSRGS_F32) return bail(NSRGS_ERR_INVALID_ARG, "d > 10 supports F32 only");
-    wide_dispatch(c->d, 0, true, &c->shape, nullptr, nullptr, 0, nullptr);
+    {
+      // opt-in: 3xTF32 tensor cores measured only ~7 % faster at the Table 1 size (0.756 vs
+      // 0.815 ms per pass; the wide pass is not FMA-bound there) with ~8x the fp32 product error
+      const char *wm = std::getenv("NSRGS_WIDE_MMA");
+      c->wide_mma = c->dtype == NSRGS_F32 && wm && wm[0] == '1';
+    }
+    wide_dispatch(c->d, 0, true, &c->shape, nullptr, nullptr, 0, nullptr, c->wide_mma);
   } else {
     panel_dispatch(c->dtype, c->d, 0, true, &c->shape, nullptr, nullptr, 0, nullptr);
   }

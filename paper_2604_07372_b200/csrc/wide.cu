@@ -17,7 +17,7 @@
 
 namespace nsrgs {
 
-template <int D>
+template <int D, bool MMA = false>
 struct WideCfg {
   static constexpr int W = 4;                          // consumer warps = nodes per panel
   static constexpr int THREADS = 32 * (W + 1);
@@ -25,7 +25,9 @@ struct WideCfg {
   static constexpr int CW = kWideColTile;
   static constexpr int A_BYTES = ROWS * CW * 4;
   static constexpr int X_BYTES = CW * D * 4;
-  static constexpr int STAGE_BYTES = A_BYTES + X_BYTES;   // = 128 (ROWS + D): TMA-aligned
+  // = 128 (ROWS + D): TMA-aligned; the tensor-core variant reads A through the 128-byte TMA
+  // swizzle, whose pattern needs 1024-byte aligned stages
+  static constexpr int STAGE_BYTES = MMA ? (A_BYTES + X_BYTES + 1023) / 1024 * 1024 : A_BYTES + X_BYTES;
   static constexpr int DD = D * D, E = DD, DDL = (DD + 31) / 32;
   static constexpr int NPART = 2 * DD + 2;
   static constexpr int SCR = W * 5 * E * 4;
@@ -49,10 +51,30 @@ __device__ __forceinline__ uint64_t wffma2(uint64_t a, uint64_t b, uint64_t c) {
   return d;
 }
 
-template <int D, int MODE>
-__global__ void __launch_bounds__(WideCfg<D>::THREADS, 1)
+// ---- tensor-core path (3xTF32 on mma.sync m16n8k8): fp32 x = hi + lo with hi = tf32(x),
+// lo = tf32(x - hi); A X ~ A_lo X_hi + A_hi X_lo + A_hi X_hi (the dropped A_lo X_lo is ~2^-22
+// relative), accumulated in fp32.
+__device__ __forceinline__ void split_tf32(float x, uint32_t &hi, uint32_t &lo) {
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hi) : "f"(x));
+  const float r = x - __uint_as_float(hi);
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(lo) : "f"(r));
+}
+__device__ __forceinline__ void mma_tf32(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+               "{%0, %1, %2, %3};"
+               : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+               : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+// element (r, c) of a 128-byte-swizzled [rows][32] fp32 TMA tile (1024-byte aligned base)
+__device__ __forceinline__ float lds_sw128(const uint8_t *base, int r, int c) {
+  const uint32_t off = (uint32_t)r * 128u + ((((uint32_t)(c >> 2) ^ (uint32_t)(r & 7)) << 4) | ((uint32_t)(c & 3) << 2));
+  return *reinterpret_cast<const float *>(base + off);
+}
+
+template <int D, int MODE, bool MMA>
+__global__ void __launch_bounds__(WideCfg<D, MMA>::THREADS, 1)
     wide_kernel(const __grid_constant__ CUtensorMap tmA, const PanelParams p) {
-  using C = WideCfg<D>;
+  using C = WideCfg<D, MMA>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = smem_raw + (((smem_u32(smem_raw) + 1023u) & ~1023u) - smem_u32(smem_raw));
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + C::STAGES * C::STAGE_BYTES);
@@ -87,7 +109,7 @@ __global__ void __launch_bounds__(WideCfg<D>::THREADS, 1)
         const int tt = g * tpr + jt;
         mbar_wait(&empty[stage], phase ^ 1u);
         uint8_t *sb = smem + stage * C::STAGE_BYTES;
-        mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
+        mbar_arrive_expect_tx(&full[stage], C::A_BYTES + C::X_BYTES);   // STAGE_BYTES may include alignment padding
         tma_load_3d(sb, &tmA, &full[stage], jt * C::CW, g, panel * C::ROWS, pol_a);
         bulk_load(sb + C::A_BYTES, Xg + (int64_t)tt * C::CW * D, C::X_BYTES, &full[stage], pol_x);
         if (++stage == C::STAGES) { stage = 0; phase ^= 1u; }
@@ -97,6 +119,69 @@ __global__ void __launch_bounds__(WideCfg<D>::THREADS, 1)
   }
 
   // ------------------------------------------------------------------ consumer warp = one node
+  float *sX = scr + warp * 5 * C::E, *sG = sX + C::E, *sH = sG + C::E, *sS = sH + C::E, *sM = sS + C::E;
+  if constexpr (MMA) {
+    // tensor cores: B_i[a][k] = sum_c A[a][c] X[c][k] as m16 (node rows) x n8 (components) x k8
+    // (columns) tiles; A fragments from the swizzled tile (conflict-free), X fragments from the
+    // row-major [32][d] slab; rows / components past d are computed on padding and dropped
+    constexpr int MT = (D + 15) / 16, NT = (D + 7) / 8;
+    float acc[MT][NT][4];
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[mt][nt][e] = 0.f;
+    const int g = lane >> 2, tq = lane & 3;
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int t = 0; t < p.total_tiles; ++t) {
+      mbar_wait(&full[stage], phase);
+      const uint8_t *Ab = smem + stage * C::STAGE_BYTES;
+      const float *Xs = reinterpret_cast<const float *>(smem + stage * C::STAGE_BYTES + C::A_BYTES);
+#pragma unroll
+      for (int k0 = 0; k0 < C::CW; k0 += 8) {
+        uint32_t bh[NT][2], bl[NT][2];
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          const int n = nt * 8 + g;
+          const float x0 = n < D ? Xs[(k0 + tq) * D + n] : 0.f;
+          const float x1 = n < D ? Xs[(k0 + tq + 4) * D + n] : 0.f;
+          split_tf32(x0, bh[nt][0], bl[nt][0]);
+          split_tf32(x1, bh[nt][1], bl[nt][1]);
+        }
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+          const int r0 = warp * D + mt * 16 + g;
+          uint32_t ah[4], al[4];
+          split_tf32(lds_sw128(Ab, r0, k0 + tq), ah[0], al[0]);
+          split_tf32(lds_sw128(Ab, r0 + 8, k0 + tq), ah[1], al[1]);
+          split_tf32(lds_sw128(Ab, r0, k0 + tq + 4), ah[2], al[2]);
+          split_tf32(lds_sw128(Ab, r0 + 8, k0 + tq + 4), ah[3], al[3]);
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) {
+            mma_tf32(acc[mt][nt], al, bh[nt][0], bh[nt][1]);
+            mma_tf32(acc[mt][nt], ah, bl[nt][0], bl[nt][1]);
+            mma_tf32(acc[mt][nt], ah, bh[nt][0], bh[nt][1]);
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[stage]);
+      if (++stage == C::STAGES) { stage = 0; phase ^= 1u; }
+    }
+    // C fragment (row g / g + 8, columns 2 tq, 2 tq + 1) -> B_i entries (a, k) inside d x d
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int a = mt * 16 + g + (e >> 1) * 8, k = nt * 8 + 2 * tq + (e & 1);
+          if (a < D && k < D) sG[a * D + k] = acc[mt][nt][e];
+        }
+    __syncwarp();
+  } else {
   const int kk = lane < D ? lane : D - 1;
   uint64_t acc2[D];   // (even-column, odd-column) partial sums of row r, component `lane`
 #pragma unroll
@@ -123,7 +208,6 @@ __global__ void __launch_bounds__(WideCfg<D>::THREADS, 1)
     if (++stage == C::STAGES) { stage = 0; phase ^= 1u; }
   }
 
-  float *sX = scr + warp * 5 * C::E, *sG = sX + C::E, *sH = sG + C::E, *sS = sH + C::E, *sM = sS + C::E;
 #pragma unroll
   for (int r = 0; r < D; ++r) {
     float lo, hi;
@@ -131,6 +215,7 @@ __global__ void __launch_bounds__(WideCfg<D>::THREADS, 1)
     if (lane < D) sG[r * D + lane] = lo + hi;   // entry (a = r, b = lane) of B_i
   }
   __syncwarp();
+  }
   const int64_t node = (int64_t)panel * C::W + warp;
   const int nvalid = node < p.n_local ? 1 : 0;
   double g1s[C::DDL], g2s[C::DDL], so = 0.0, xs = 0.0;
@@ -175,10 +260,10 @@ __global__ void __launch_bounds__(WideCfg<D>::THREADS, 1)
   }
 }
 
-template <int D, int MODE>
+template <int D, int MODE, bool MMA>
 static cudaError_t wide_launch(const CUtensorMap *tm, const PanelParams &p, int grid, cudaStream_t s) {
-  using C = WideCfg<D>;
-  auto kern = wide_kernel<D, MODE>;
+  using C = WideCfg<D, MMA>;
+  auto kern = wide_kernel<D, MODE, MMA>;
   static bool attr[64] = {};
   {
     const cudaError_t e = set_smem_attr_once(reinterpret_cast<const void *>(kern), C::SMEM, attr);
@@ -188,21 +273,32 @@ static cudaError_t wide_launch(const CUtensorMap *tm, const PanelParams &p, int 
   return cudaGetLastError();
 }
 
+template <int D, bool MMA>
+static cudaError_t wide_mode(int mode, const CUtensorMap *tm, const PanelParams &p, int grid, cudaStream_t s) {
+  if (mode == kModeRgs) return wide_launch<D, kModeRgs, MMA>(tm, p, grid, s);
+  if (mode == kModeObjective) return wide_launch<D, kModeObjective, MMA>(tm, p, grid, s);
+  if (mode == kModeGpm) return wide_launch<D, kModeGpm, MMA>(tm, p, grid, s);
+  return wide_launch<D, kModeProduct, MMA>(tm, p, grid, s);
+}
+
 bool wide_supported(int d) { return d == 12 || d == 16 || d == 20 || d == 24 || d == 25 || d == 32; }
 
+// mma: the 3xTF32 tensor-core variant (the caller's tensor map must then use the 128-byte swizzle)
 cudaError_t wide_dispatch(int d, int mode, bool shape_only, PanelShape *shape, const CUtensorMap *tm,
-                          const PanelParams *p, int grid, cudaStream_t s) {
+                          const PanelParams *p, int grid, cudaStream_t s, bool mma) {
 #define NSRGS_WIDE_CASE(DV)                                                                        \
   case DV: {                                                                                       \
-    using C = WideCfg<DV>;                                                                         \
     if (shape_only) {                                                                              \
-      *shape = PanelShape{C::ROWS, C::W, C::STAGES, C::SMEM, C::NPART, C::THREADS, C::W};          \
+      if (mma) {                                                                                   \
+        using C = WideCfg<DV, true>;                                                               \
+        *shape = PanelShape{C::ROWS, C::W, C::STAGES, C::SMEM, C::NPART, C::THREADS, C::W};        \
+      } else {                                                                                     \
+        using C = WideCfg<DV, false>;                                                              \
+        *shape = PanelShape{C::ROWS, C::W, C::STAGES, C::SMEM, C::NPART, C::THREADS, C::W};        \
+      }                                                                                            \
       return cudaSuccess;                                                                          \
     }                                                                                              \
-    if (mode == kModeRgs) return wide_launch<DV, kModeRgs>(tm, *p, grid, s);                       \
-    if (mode == kModeObjective) return wide_launch<DV, kModeObjective>(tm, *p, grid, s);           \
-    if (mode == kModeGpm) return wide_launch<DV, kModeGpm>(tm, *p, grid, s);                       \
-    return wide_launch<DV, kModeProduct>(tm, *p, grid, s);                                         \
+    return mma ? wide_mode<DV, true>(mode, tm, *p, grid, s) : wide_mode<DV, false>(mode, tm, *p, grid, s); \
   }
   switch (d) {
     NSRGS_WIDE_CASE(12)

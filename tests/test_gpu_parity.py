@@ -544,6 +544,30 @@ def _table1_rows():
     return [tuple(float(t) for t in l.split()) for l in open(path) if l.strip() and not l.startswith("#")]
 
 
+@pytest.mark.parametrize("n,d,sigma,K", [(60, 12, 0.5, 3), (50, 25, 0.1, 1), (23, 32, 0.2, 2)])
+def test_wide_tensor_core_variant(nsrgs, monkeypatch, n, d, sigma, K):
+    """Opt-in 3xTF32 mma.sync wide pass (NSRGS_WIDE_MMA=1, 128-byte swizzled A tiles): one step
+    and GPM against the fp64 oracle.  Tolerance 5e-6 on the iterate: each product carries ~2^-21
+    relative error (the dropped A_lo X_lo term and the tf32 rounding of the lo parts), ~8x fp32's,
+    plus the tensor cores' fp32 accumulation.  The fused objective is a difference of terms ~4x
+    larger than F (expansion R15), so its bound is 1e-4 (measured 3e-5 at d = 25)."""
+    monkeypatch.setenv("NSRGS_WIDE_MMA", "1")
+    s = nsrgs.Solver(n, d)
+    s.generate(4, sigma, want_Z=False)
+    Z = inst.ground_truth(4, n, d)
+    A = inst.measurement_matrix(4, Z, sigma)
+    X = oracle_iterate_near(Z, 0.1, 2).astype(np.float32)
+    s.set_X(X)
+    f = s.step(1.0 / n, K)
+    Xo, _, _ = ons.step(A, X.astype(np.float64), 1.0 / n, K)
+    assert rel_fro(s.get_X(), Xo) <= 5e-6
+    assert abs(f - ons.objective(A, X.astype(np.float64))) <= 1e-4 * f
+    s.set_X(X)
+    s.gpm_run(1)
+    assert rel_fro(s.get_X(), ons.gpm_step(A, X.astype(np.float64))) <= 5e-6
+    s.close()
+
+
 def test_table1_on_b200(nsrgs):
     """PAPER.md Table 1 (all nine cells, :345-359) with the paper's protocol on the GPU:
     spectral init, T_s = 1, mu = 1/(np), stop at R^t < 1e-8 / MaxIter 100, NS-RGS and GPM."""
