@@ -23,7 +23,7 @@ cudaError_t launch_p2p_wait(const unsigned *xcnt, int world, unsigned target, in
 // wide.cu: d > 10 (one node per warp, lane = component).
 bool wide_supported(int d);
 cudaError_t wide_dispatch(int d, int mode, bool shape_only, PanelShape *shape, const CUtensorMap *tm,
-                          const PanelParams *p, int grid, cudaStream_t s, int mma);
+                          const PanelParams *p, int grid, cudaStream_t s, bool mma);
 
 // sym.cu: symmetric half-storage pass (fp32, world == 1, d in [2, 6]).
 struct SymShape {

@@ -117,8 +117,7 @@ struct nsrgs_ctx {
   bool own_A = false, have_A = false;
   CUtensorMap tmA;
   CUtensorMap tmA_sym;   // symmetric pass: same A, its own panel height
-  int wide_mma = 0;      // d > 10 pass: 0 CUDA cores, 1 3xTF32 mma.sync, 2 3xTF32 tcgen05
-                         // (1 and 2 read A through the 128-byte TMA swizzle)
+  bool wide_mma = false; // d > 10: 3xTF32 tensor-core pass (A tensor map with the 128-byte swizzle)
   double a_fro2 = 0.0;
   // iterate
   void *X[2] = {nullptr, nullptr};   // both inside xblock (one IPC-shareable allocation)
@@ -379,7 +378,7 @@ int build_tmap(nsrgs_ctx *c, CUtensorMap *out = nullptr, int rows = 0) {
                            (cuuint64_t)(c->lda * c->esz)};
   cuuint32_t box[3] = {(cuuint32_t)col_tile(c->d), 1u, (cuuint32_t)rows};
   cuuint32_t estr[3] = {1u, 1u, 1u};
-  const bool swz = out == &c->tmA && c->wide_mma != 0;   // the tensor-core wide pass reads swizzled tiles
+  const bool swz = out == &c->tmA && c->wide_mma;   // the tensor-core wide pass reads swizzled tiles
   CUresult r = encode(out, c->dtype == NSRGS_F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64,
                       3, c->A, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                       swz ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -755,7 +754,7 @@ int nsrgs_create(const nsrgs_desc *desc, nsrgs_ctx **out) {
       // opt-in: 3xTF32 tensor cores measured only ~7 % faster at the Table 1 size (0.756 vs
       // 0.815 ms per pass; the wide pass is not FMA-bound there) with ~8x the fp32 product error
       const char *wm = std::getenv("NSRGS_WIDE_MMA");
-      c->wide_mma = (c->dtype == NSRGS_F32 && wm && (wm[0] == '1' || wm[0] == '2')) ? wm[0] - '0' : 0;
+      c->wide_mma = c->dtype == NSRGS_F32 && wm && wm[0] == '1';
     }
     wide_dispatch(c->d, 0, true, &c->shape, nullptr, nullptr, 0, nullptr, c->wide_mma);
   } else {

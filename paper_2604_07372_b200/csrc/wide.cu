@@ -17,11 +17,10 @@
 
 namespace nsrgs {
 
-// MMA: 0 CUDA cores (default), 1 3xTF32 on mma.sync, 2 3xTF32 on tcgen05 (TMEM accumulator)
-template <int D, int MMA = 0>
+template <int D, bool MMA = false>
 struct WideCfg {
   static constexpr int W = 4;                          // consumer warps = nodes per panel
-  static constexpr int THREADS = 32 * (W + (MMA == 2 ? 2 : 1));   // + TMA producer (+ MMA issuer)
+  static constexpr int THREADS = 32 * (W + 1);
   static constexpr int ROWS = W * D;
   static constexpr int CW = kWideColTile;
   static constexpr int A_BYTES = ROWS * CW * 4;
@@ -33,19 +32,11 @@ struct WideCfg {
   static constexpr int NPART = 2 * DD + 2;
   static constexpr int SCR = W * 5 * E * 4;
   static constexpr int RED = W * NPART * 8;
-  // tcgen05 variant: double-buffered split tiles (A_hi, A_lo: 128 rows x 128 B; X^T_hi, X^T_lo:
-  // 32 components x 128 B, K-major, 128-byte swizzle); the epilogue scratch (scr, red) aliases the
-  // stage ring + split area, which are idle once the accumulator is complete
-  static constexpr int SPLIT_BUF = 2 * 16384 + 2 * 4096;
-  static constexpr int SPLIT = MMA == 2 ? 2 * SPLIT_BUF : 0;
-  static constexpr int ALIAS = SCR + RED + 64;
-  static constexpr int FIXED = MMA == 2 ? 1024 + 256 + SPLIT : 1024 + 128 + SCR + RED + 64;
+  static constexpr int FIXED = 1024 + 128 + SCR + RED + 64;
   static constexpr int BUDGET = 222 * 1024;
   static constexpr int STAGES_RAW = (BUDGET - FIXED) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_RAW > 6 ? 6 : STAGES_RAW;
   static_assert(STAGES >= 2, "ring");
-  static_assert(MMA != 2 || STAGES * STAGE_BYTES + SPLIT >= ALIAS, "epilogue scratch alias");
-  static_assert(MMA != 2 || ROWS <= 128, "one M = 128 tile per panel");
   static constexpr int SMEM = FIXED + STAGES * STAGE_BYTES;
 };
 
@@ -80,44 +71,15 @@ __device__ __forceinline__ float lds_sw128(const uint8_t *base, int r, int c) {
   return *reinterpret_cast<const float *>(base + off);
 }
 
-// ---- tcgen05 (5th-generation tensor core) helpers; encodings pinned by tools/micro/umma_tf32.cu
-// smem matrix descriptor: K-major, 128-byte swizzle, SBO = 1024 B between 8-row groups, sm_100 version
-__device__ __forceinline__ uint64_t umma_sdesc(uint32_t saddr) {
-  return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
-         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
-}
-// instruction descriptor: D f32, A/B tf32, both K-major, N = 32, M = 128
-constexpr uint32_t kUmmaIdescTf32 = (1u << 4) | (2u << 7) | (2u << 10) | ((32u >> 3) << 17) | ((128u >> 4) << 24);
-__device__ __forceinline__ void umma_tf32(uint32_t tmem, uint64_t da, uint64_t db, uint32_t accumulate) {
-  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-               "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}"
-               ::"r"(tmem), "l"(da), "l"(db), "r"(kUmmaIdescTf32), "r"(accumulate));
-}
-__device__ __forceinline__ void umma_commit(uint64_t *bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
-               : "memory");
-}
-__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-__device__ __forceinline__ float tf32_rna(float x) {
-  uint32_t h;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(x));
-  return __uint_as_float(h);
-}
-
-template <int D, int MODE, int MMA>
+template <int D, int MODE, bool MMA>
 __global__ void __launch_bounds__(WideCfg<D, MMA>::THREADS, 1)
     wide_kernel(const __grid_constant__ CUtensorMap tmA, const PanelParams p) {
   using C = WideCfg<D, MMA>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = smem_raw + (((smem_u32(smem_raw) + 1023u) & ~1023u) - smem_u32(smem_raw));
-  uint64_t *full = reinterpret_cast<uint64_t *>(smem + C::STAGES * C::STAGE_BYTES + C::SPLIT);
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + C::STAGES * C::STAGE_BYTES);
   uint64_t *empty = full + 8;
-  uint64_t *split_full = empty + 8, *split_free = split_full + 2, *acc_full = split_free + 2;
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(acc_full + 1);
-  float *scr = MMA == 2 ? reinterpret_cast<float *>(smem)   // aliases the (then idle) ring, see WideCfg
-                        : reinterpret_cast<float *>(smem + C::STAGES * C::STAGE_BYTES + 128);
+  float *scr = reinterpret_cast<float *>(smem + C::STAGES * C::STAGE_BYTES + 128);
   double *red = reinterpret_cast<double *>(reinterpret_cast<uint8_t *>(scr) + C::SCR);
   int *flag = reinterpret_cast<int *>(red + C::W * C::NPART);
 
@@ -127,35 +89,9 @@ __global__ void __launch_bounds__(WideCfg<D, MMA>::THREADS, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], C::W);
     }
-    if constexpr (MMA == 2) {
-      for (int b = 0; b < 2; ++b) { mbar_init(&split_full[b], C::W); mbar_init(&split_free[b], 1); }
-      mbar_init(acc_full, 1);
-    }
     fence_mbar_init();
   }
-  if constexpr (MMA == 2) {
-    // zero the split tiles' padding rows once (A rows >= ROWS, X^T components >= D): never rewritten
-    uint8_t *split = smem + C::STAGES * C::STAGE_BYTES;
-    for (int b = 0; b < 2; ++b) {
-      uint8_t *AH = split + b * C::SPLIT_BUF;
-      for (int i = threadIdx.x; i < (128 - C::ROWS) * 32; i += C::THREADS) {
-        reinterpret_cast<float *>(AH + C::ROWS * 128)[i] = 0.f;
-        reinterpret_cast<float *>(AH + 16384 + C::ROWS * 128)[i] = 0.f;
-      }
-      for (int i = threadIdx.x; i < (32 - D) * 32; i += C::THREADS) {
-        reinterpret_cast<float *>(AH + 32768 + D * 128)[i] = 0.f;
-        reinterpret_cast<float *>(AH + 32768 + 4096 + D * 128)[i] = 0.f;
-      }
-    }
-    fence_proxy_async_smem();
-    if ((threadIdx.x >> 5) == 0) {
-      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 32;" ::"r"(smem_u32(tmem_slot)));
-      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-    }
-    tc_fence_before();
-  }
   __syncthreads();
-  if constexpr (MMA == 2) tc_fence_after();
   const float *Xg = static_cast<const float *>(p.X);
   const int panel = blockIdx.x;
   const int tpr = (int)p.tiles_per_rank;
@@ -181,100 +117,10 @@ __global__ void __launch_bounds__(WideCfg<D, MMA>::THREADS, 1)
     }
     return;
   }
-  if constexpr (MMA == 2) {
-    if (warp == C::W + 1) {   // ------------------------------------------ tcgen05 issuer (one lane)
-      if (lane == 0) {
-        const uint32_t tmem = *tmem_slot;
-        const uint32_t split = smem_u32(smem + C::STAGES * C::STAGE_BYTES);
-        for (int t = 0; t < p.total_tiles; ++t) {
-          const int b = t & 1;
-          mbar_wait(&split_full[b], (uint32_t)(t >> 1) & 1u);
-          tc_fence_after();
-          const uint32_t AH = split + b * C::SPLIT_BUF, AL = AH + 16384, XH = AL + 16384, XL = XH + 4096;
-#pragma unroll
-          for (int ks = 0; ks < C::CW / 8; ++ks) {   // B += A_lo X_hi + A_hi X_lo + A_hi X_hi per K = 8
-            const uint64_t ah = umma_sdesc(AH + ks * 32), al = umma_sdesc(AL + ks * 32);
-            const uint64_t xh = umma_sdesc(XH + ks * 32), xl = umma_sdesc(XL + ks * 32);
-            umma_tf32(tmem, al, xh, (t | ks) != 0);
-            umma_tf32(tmem, ah, xl, 1u);
-            umma_tf32(tmem, ah, xh, 1u);
-          }
-          umma_commit(&split_free[b]);
-        }
-        umma_commit(acc_full);
-      }
-      return;
-    }
-  }
 
   // ------------------------------------------------------------------ consumer warp = one node
   float *sX = scr + warp * 5 * C::E, *sG = sX + C::E, *sH = sG + C::E, *sS = sH + C::E, *sM = sS + C::E;
-  if constexpr (MMA == 2) {
-    // split producer: A -> (A_hi, A_lo) chunk by chunk in the TMA tile's own swizzled layout, the
-    // X slab -> K-major swizzled (X^T_hi, X^T_lo); the stage is released as soon as it is split
-    uint8_t *split = smem + C::STAGES * C::STAGE_BYTES;
-    const int tid = threadIdx.x, kc = tid & 31;
-    int stage = 0;
-    uint32_t phase = 0;
-    for (int t = 0; t < p.total_tiles; ++t) {
-      const int b = t & 1;
-      uint8_t *AH = split + b * C::SPLIT_BUF, *AL = AH + 16384, *XH = AL + 16384, *XL = XH + 4096;
-      mbar_wait(&full[stage], phase);
-      mbar_wait(&split_free[b], ((uint32_t)(t >> 1) & 1u) ^ 1u);
-      const uint8_t *sb = smem + stage * C::STAGE_BYTES;
-      if (tid < C::ROWS) {
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const uint32_t off = (uint32_t)tid * 128u + ((uint32_t)((j + tid) & 7) << 4);   // rotated: no conflicts
-          const float4 v = *reinterpret_cast<const float4 *>(sb + off);
-          float4 h, l;
-          h.x = tf32_rna(v.x); l.x = tf32_rna(v.x - h.x);
-          h.y = tf32_rna(v.y); l.y = tf32_rna(v.y - h.y);
-          h.z = tf32_rna(v.z); l.z = tf32_rna(v.z - h.z);
-          h.w = tf32_rna(v.w); l.w = tf32_rna(v.w - h.w);
-          *reinterpret_cast<float4 *>(AH + off) = h;
-          *reinterpret_cast<float4 *>(AL + off) = l;
-        }
-      }
-      const float *Xs = reinterpret_cast<const float *>(sb + C::A_BYTES);
-      for (int n = tid >> 5; n < D; n += C::W) {
-        const float x = Xs[kc * D + n];
-        const float h = tf32_rna(x), l = tf32_rna(x - h);
-        const uint32_t off = (uint32_t)n * 128u + ((uint32_t)((kc >> 2) ^ (n & 7)) << 4) + (uint32_t)(kc & 3) * 4u;
-        *reinterpret_cast<float *>(XH + off) = h;
-        *reinterpret_cast<float *>(XL + off) = l;
-      }
-      fence_proxy_async_smem();
-      __syncwarp();
-      if (lane == 0) { mbar_arrive(&split_full[b]); mbar_arrive(&empty[stage]); }
-      if (++stage == C::STAGES) { stage = 0; phase ^= 1u; }
-    }
-    // accumulator: TMEM lane r = panel row r, column k = component; warp w reads lanes 32w..32w+31
-    mbar_wait(acc_full, 0);
-    tc_fence_after();
-    uint32_t v[32];
-    asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 "
-                 "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-                 "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-                   "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
-                   "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
-                   "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
-                   "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-                 : "r"(*tmem_slot + ((uint32_t)(warp * 32) << 16)));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-    const int r = warp * 32 + lane;
-    if (r < C::ROWS) {
-      const int wn = r / D, a = r - wn * D;
-      float *g = scr + wn * 5 * C::E + C::E + a * D;
-#pragma unroll
-      for (int k = 0; k < D; ++k) g[k] = __uint_as_float(v[k]);
-    }
-    tc_fence_before();
-    named_bar_sync(2, C::W * 32);
-    tc_fence_after();
-    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 32;" ::"r"(*tmem_slot));
-  } else if constexpr (MMA == 1) {
+  if constexpr (MMA) {
     // tensor cores: B_i[a][k] = sum_c A[a][c] X[c][k] as m16 (node rows) x n8 (components) x k8
     // (columns) tiles; A fragments from the swizzled tile (conflict-free), X fragments from the
     // row-major [32][d] slab; rows / components past d are computed on padding and dropped
@@ -414,7 +260,7 @@ __global__ void __launch_bounds__(WideCfg<D, MMA>::THREADS, 1)
   }
 }
 
-template <int D, int MODE, int MMA>
+template <int D, int MODE, bool MMA>
 static cudaError_t wide_launch(const CUtensorMap *tm, const PanelParams &p, int grid, cudaStream_t s) {
   using C = WideCfg<D, MMA>;
   auto kern = wide_kernel<D, MODE, MMA>;
@@ -427,7 +273,7 @@ static cudaError_t wide_launch(const CUtensorMap *tm, const PanelParams &p, int 
   return cudaGetLastError();
 }
 
-template <int D, int MMA>
+template <int D, bool MMA>
 static cudaError_t wide_mode(int mode, const CUtensorMap *tm, const PanelParams &p, int grid, cudaStream_t s) {
   if (mode == kModeRgs) return wide_launch<D, kModeRgs, MMA>(tm, p, grid, s);
   if (mode == kModeObjective) return wide_launch<D, kModeObjective, MMA>(tm, p, grid, s);
@@ -437,27 +283,22 @@ static cudaError_t wide_mode(int mode, const CUtensorMap *tm, const PanelParams 
 
 bool wide_supported(int d) { return d == 12 || d == 16 || d == 20 || d == 24 || d == 25 || d == 32; }
 
-// mma: 0 CUDA cores; 1 3xTF32 on mma.sync; 2 3xTF32 on tcgen05 (1 and 2 read A through the
-// 128-byte TMA swizzle: the caller's tensor map must use it)
+// mma: the 3xTF32 tensor-core variant (the caller's tensor map must then use the 128-byte swizzle)
 cudaError_t wide_dispatch(int d, int mode, bool shape_only, PanelShape *shape, const CUtensorMap *tm,
-                          const PanelParams *p, int grid, cudaStream_t s, int mma) {
+                          const PanelParams *p, int grid, cudaStream_t s, bool mma) {
 #define NSRGS_WIDE_CASE(DV)                                                                        \
   case DV: {                                                                                       \
     if (shape_only) {                                                                              \
-      if (mma == 2) {                                                                              \
-        using C = WideCfg<DV, 2>;                                                                  \
-        *shape = PanelShape{C::ROWS, C::W, C::STAGES, C::SMEM, C::NPART, C::THREADS, C::W};        \
-      } else if (mma == 1) {                                                                       \
-        using C = WideCfg<DV, 1>;                                                                  \
+      if (mma) {                                                                                   \
+        using C = WideCfg<DV, true>;                                                               \
         *shape = PanelShape{C::ROWS, C::W, C::STAGES, C::SMEM, C::NPART, C::THREADS, C::W};        \
       } else {                                                                                     \
-        using C = WideCfg<DV, 0>;                                                                  \
+        using C = WideCfg<DV, false>;                                                              \
         *shape = PanelShape{C::ROWS, C::W, C::STAGES, C::SMEM, C::NPART, C::THREADS, C::W};        \
       }                                                                                            \
       return cudaSuccess;                                                                          \
     }                                                                                              \
-    return mma == 2 ? wide_mode<DV, 2>(mode, tm, *p, grid, s)                                      \
-         : mma == 1 ? wide_mode<DV, 1>(mode, tm, *p, grid, s) : wide_mode<DV, 0>(mode, tm, *p, grid, s); \
+    return mma ? wide_mode<DV, true>(mode, tm, *p, grid, s) : wide_mode<DV, false>(mode, tm, *p, grid, s); \
   }
   switch (d) {
     NSRGS_WIDE_CASE(12)

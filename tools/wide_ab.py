@@ -1,4 +1,4 @@
-"""A/B of the wide-pass variants (NSRGS_WIDE_MMA = 0 broadcast, 1 3xTF32 mma.sync, 2 3xTF32 tcgen05) on one box:
+"""A/B of the wide-pass variants (NSRGS_WIDE_MMA = 0 broadcast, 1 3xTF32) on one box:
 mean panel pass over 20 iterations after spectral init.  Usage: python tools/wide_ab.py"""
 import os, subprocess, sys
 if len(sys.argv) > 1:
@@ -14,5 +14,5 @@ if len(sys.argv) > 1:
     print(f"variant={os.environ.get('NSRGS_WIDE_MMA', '0')} d={d} n={n} pass {ms*1e3:.1f} us  {4*N*N/ms/1e6:.0f} GB/s", flush=True)
     sys.exit(0)
 for n, d in [(500, 25), (2000, 25), (4000, 25), (7000, 25), (1000, 16), (8000, 16)]:
-    for v in ("0", "1", "2"):
+    for v in ("0", "1"):
         subprocess.run([sys.executable, __file__, str(n), str(d)], env={**os.environ, "NSRGS_WIDE_MMA": v}, timeout=300)
