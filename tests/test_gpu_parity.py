@@ -550,7 +550,10 @@ def test_wide_tensor_core_variant(nsrgs, monkeypatch, n, d, sigma, K):
     and GPM against the fp64 oracle.  Tolerance 5e-6 on the iterate: each product carries ~2^-21
     relative error (the dropped A_lo X_lo term and the tf32 rounding of the lo parts), ~8x fp32's,
     plus the tensor cores' fp32 accumulation.  The fused objective is a difference of terms ~4x
-    larger than F (expansion R15), so its bound is 1e-4 (measured 3e-5 at d = 25)."""
+    larger than F (expansion R15), so its bound is 1e-4 (measured 3e-5 at d = 25).  These bounds
+    hold at these small n only: the tensor core's fp32 accumulation is not round-to-nearest, so
+    the step error grows linearly with N (3.1e-5 at n 700, d 25, tools/wide_err.py) —
+    the reason the variant is opt-in."""
     monkeypatch.setenv("NSRGS_WIDE_MMA", "1")
     s = nsrgs.Solver(n, d)
     s.generate(4, sigma, want_Z=False)
