@@ -117,7 +117,8 @@ struct nsrgs_ctx {
   bool own_A = false, have_A = false;
   CUtensorMap tmA;
   CUtensorMap tmA_sym;   // symmetric pass: same A, its own panel height
-  bool wide_mma = false; // d > 10: 3xTF32 tensor-core pass (A tensor map with the 128-byte swizzle)
+  bool wide_mma = false; // d > 10: 3xTF32 tensor-core pass (default; A tensor map with the 128-byte
+                         // swizzle); NSRGS_WIDE_MMA=0 selects the CUDA-core pass
   double a_fro2 = 0.0;
   // iterate
   void *X[2] = {nullptr, nullptr};   // both inside xblock (one IPC-shareable allocation)
@@ -754,7 +755,9 @@ int nsrgs_create(const nsrgs_desc *desc, nsrgs_ctx **out) {
       // opt-in: 3xTF32 tensor cores measured only ~7 % faster at the Table 1 size (0.756 vs
       // 0.815 ms per pass; the wide pass is not FMA-bound there) with ~8x the fp32 product error
       const char *wm = std::getenv("NSRGS_WIDE_MMA");
-      c->wide_mma = c->dtype == NSRGS_F32 && wm && wm[0] == '1';
+      // 3xTF32 tensor-core pass by default (accumulator drained per tile: ≤ 3.1e-7 per step vs
+      // 8.4e-7 on CUDA cores, 1.07-1.9x faster; profiles/r01c_wide_variants.txt); =0 CUDA cores
+      c->wide_mma = c->dtype == NSRGS_F32 && !(wm && wm[0] == '0');
     }
     wide_dispatch(c->d, 0, true, &c->shape, nullptr, nullptr, 0, nullptr, c->wide_mma);
   } else {

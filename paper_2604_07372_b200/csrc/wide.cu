@@ -125,13 +125,16 @@ __global__ void __launch_bounds__(WideCfg<D, MMA>::THREADS, 1)
     // (columns) tiles; A fragments from the swizzled tile (conflict-free), X fragments from the
     // row-major [32][d] slab; rows / components past d are computed on padding and dropped
     constexpr int MT = (D + 15) / 16, NT = (D + 7) / 8;
-    float acc[MT][NT][4];
+    // acc: the tensor core's accumulator, restarted every tile (32 columns = 12 MMAs): its fp32
+    // accumulation does not round to nearest, so a chain over all N columns drifts (error ∝ N);
+    // tot: the running sum in CUDA-core fp32 (round to nearest), one FADD per entry per tile
+    float acc[MT][NT][4], tot[MT][NT][4];
 #pragma unroll
     for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-        for (int e = 0; e < 4; ++e) acc[mt][nt][e] = 0.f;
+        for (int e = 0; e < 4; ++e) { acc[mt][nt][e] = 0.f; tot[mt][nt][e] = 0.f; }
     const int g = lane >> 2, tq = lane & 3;
     int stage = 0;
     uint32_t phase = 0;
@@ -166,6 +169,12 @@ __global__ void __launch_bounds__(WideCfg<D, MMA>::THREADS, 1)
           }
         }
       }
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) { tot[mt][nt][e] += acc[mt][nt][e]; acc[mt][nt][e] = 0.f; }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[stage]);
       if (++stage == C::STAGES) { stage = 0; phase ^= 1u; }
@@ -178,7 +187,7 @@ __global__ void __launch_bounds__(WideCfg<D, MMA>::THREADS, 1)
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const int a = mt * 16 + g + (e >> 1) * 8, k = nt * 8 + 2 * tq + (e & 1);
-          if (a < D && k < D) sG[a * D + k] = acc[mt][nt][e];
+          if (a < D && k < D) sG[a * D + k] = tot[mt][nt][e];
         }
     __syncwarp();
   } else {
