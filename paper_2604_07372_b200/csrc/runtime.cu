@@ -752,8 +752,6 @@ int nsrgs_create(const nsrgs_desc *desc, nsrgs_ctx **out) {
   if (c->d > kMaxNarrowD) {
     if (c->dtype != NSRGS_F32) return bail(NSRGS_ERR_INVALID_ARG, "d > 10 supports F32 only");
     {
-      // opt-in: 3xTF32 tensor cores measured only ~7 % faster at the Table 1 size (0.756 vs
-      // 0.815 ms per pass; the wide pass is not FMA-bound there) with ~8x the fp32 product error
       const char *wm = std::getenv("NSRGS_WIDE_MMA");
       // 3xTF32 tensor-core pass by default (accumulator drained per tile: ≤ 3.1e-7 per step vs
       // 8.4e-7 on CUDA cores, 1.07-1.9x faster; profiles/r01c_wide_variants.txt); =0 CUDA cores
