@@ -1443,6 +1443,7 @@ int nsrgs_get_stats(nsrgs_ctx *c, nsrgs_stats_t *o) {
   o->bsr_nnzb = c->bsr ? c->bsr_nnzb : 0;
   o->bsr_slab = (c->bsr && c->bsr_lg2g >= 0) ? 1 : 0;
   o->bsr_g4 = (c->bsr && c->bsr_g4) ? 1 : 0;
+  o->wide_tc = (c->d > kMaxNarrowD && !c->bsr && c->wide_mma) ? 1 : 0;
   o->p2p = c->p2p ? 1 : 0;
   return NSRGS_OK;
 }

@@ -47,7 +47,8 @@ class Stats(ct.Structure):
                 ("smem_bytes", ct.c_int64), ("panel_ms_total", ct.c_double), ("panel_launches", ct.c_int64),
                 ("kernel_launches", ct.c_int64), ("ns_region_max", ct.c_double), ("a_fro2", ct.c_double),
                 ("symmetric", ct.c_int32), ("a_bytes_per_pass", ct.c_int64), ("p2p", ct.c_int32),
-                ("bsr", ct.c_int32), ("bsr_nnzb", ct.c_int64), ("bsr_slab", ct.c_int32), ("bsr_g4", ct.c_int32)]
+                ("bsr", ct.c_int32), ("bsr_nnzb", ct.c_int64), ("bsr_slab", ct.c_int32), ("bsr_g4", ct.c_int32),
+                ("wide_tc", ct.c_int32)]
 
 
 _P = ct.c_void_p

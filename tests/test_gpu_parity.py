@@ -518,6 +518,7 @@ def test_masked_end_to_end_and_symmetric(nsrgs):
 def test_wide_generator_step_gpm(nsrgs, n, d, sigma, K):
     s = nsrgs.Solver(n, d)
     Zg = s.generate(4, sigma)
+    assert s.stats()["wide_tc"] == 1                # the default wide pass is the tensor-core one
     Z = inst.ground_truth(4, n, d)
     assert np.max(np.abs(Zg.astype(np.float64) - Z)) <= 2e-7
     A = inst.measurement_matrix(4, Z, sigma)
@@ -557,6 +558,7 @@ def test_wide_pass_variants(nsrgs, monkeypatch, variant, n, d, sigma, K):
     monkeypatch.setenv("NSRGS_WIDE_MMA", variant)
     s = nsrgs.Solver(n, d)
     s.generate(4, sigma, want_Z=False)
+    assert s.stats()["wide_tc"] == (variant == "1")
     Z = inst.ground_truth(4, n, d)
     A = inst.measurement_matrix(4, Z, sigma)
     X = oracle_iterate_near(Z, 0.1, 2).astype(np.float32)
