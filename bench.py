@@ -248,7 +248,7 @@ def run_gpu(args, cfg):
     Xpin = torch.empty((n, d, d), dtype=torch.float32).pin_memory()
 
     def solve(e2e=False):
-        sw = s.init_spectral(0, INIT_MAX_SWEEPS, INIT_TOL, allow_unconverged=True)
+        sw = s.init_spectral(0, INIT_MAX_SWEEPS, INIT_TOL)
         tr = s.run(T, eta, K, trace=True)
         if e2e:
             s.get_X(Xpin)                                # D2H of the result (pinned)
@@ -303,7 +303,7 @@ def run_gpu(args, cfg):
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
     barrier()
     ev[0].record(stream)
-    s.init_spectral(0, INIT_MAX_SWEEPS, INIT_TOL, allow_unconverged=True)
+    s.init_spectral(0, INIT_MAX_SWEEPS, INIT_TOL)
     ev[1].record(stream)
     s.run(T, eta, K, trace=True)
     ev[2].record(stream)
@@ -313,7 +313,7 @@ def run_gpu(args, cfg):
     phases = {"init_ms": ev[0].elapsed_time(ev[1]), "iterations_ms": ev[1].elapsed_time(ev[2]),
               "metrics_ms": ev[2].elapsed_time(ev[3])}
     phases["iterations_per_sec_run_only"] = T / (phases["iterations_ms"] / 1e3)
-    s.init_spectral(0, INIT_MAX_SWEEPS, INIT_TOL, allow_unconverged=True)
+    s.init_spectral(0, INIT_MAX_SWEEPS, INIT_TOL)
     rgs_ms = per_iter_ms(lambda k: s.run(k, eta, K, trace=False))
     gpm_ms = per_iter_ms(lambda k: s.gpm_run(k, trace=False))
 
@@ -358,7 +358,7 @@ def run_gpu(args, cfg):
         Zb = torch.from_numpy(sb.generate(0, cfg["sigma"], p=pb, storage="bsr")).to(f"cuda:{local}")
 
         def solve_b():
-            sb.init_spectral(0, INIT_MAX_SWEEPS, INIT_TOL, allow_unconverged=True)
+            sb.init_spectral(0, INIT_MAX_SWEEPS, INIT_TOL)
             sb.run(T, 1.0 / (n * pb), K, trace=True)
             return sb.alignment_error(Zb)
 

@@ -61,7 +61,7 @@ typedef enum { NSRGS_F32 = 0, NSRGS_F64 = 1 } nsrgs_dtype;
 /* Context description. */
 typedef struct {
   int64_t n;                    /* number of nodes (group elements), n >= 2                     */
-  int32_t d;                    /* block size; supported: 2..10 and 12,16,20,24,25,32 (F32), 2..6 (F64) */
+  int32_t d;                    /* block size; supported: 2..16, 20, 24, 25, 32 (F32), 2..6 (F64) */
   int32_t dtype;                /* nsrgs_dtype: storage + arithmetic type of A, X (fp64 partials) */
   int32_t rank, world;          /* world >= 1, 0 <= rank < world, n % world == 0; for world > 1
                                    also (n/world)*d*sizeof(dtype) % 16 == 0 (TMA row-segment
@@ -148,7 +148,10 @@ int nsrgs_generate_observed(nsrgs_ctx *ctx, uint64_t seed, double sigma, double 
  * F32 contexts, every supported d, any world.  nsrgs_set_symmetric and nsrgs_copy_A_rows
  * return NSRGS_ERR_STATE while block-sparse storage is active; a dense generate / attach
  * switches back.  nsrgs_get_A_bsr copies the arrays to host (each pointer nullable;
- * *nnzb_out receives nnzb). */
+ * *nnzb_out receives nnzb).  nsrgs_attach_A_bsr checks the structure on the device before
+ * using it (rowptr[0] = 0, non-decreasing, rowptr[n_local] = nnzb, every col in [0, n)) and
+ * returns NSRGS_ERR_INVALID_ARG otherwise, leaving the previous A in place; the values and
+ * the column order within a row are not checked. */
 int nsrgs_generate_observed_bsr(nsrgs_ctx *ctx, uint64_t seed, double sigma, double p, void *Z_out_host);
 int nsrgs_attach_A_bsr(nsrgs_ctx *ctx, const int64_t *rowptr_dev, const int32_t *col_dev, const void *vals_dev,
                        int64_t nnzb);
@@ -162,8 +165,13 @@ int nsrgs_copy_A_rows(nsrgs_ctx *ctx, int64_t row0, int64_t nrows, void *out_hos
  * by subspace iteration Y <- A Y (the same panel A.X kernel as nsrgs_step) with Cholesky-QR,
  * Y_0 Gaussian from Philox counter (r,0,q,3), stopped when ||Y_new - Y_old(Y_old^T Y_new)||_F
  * < tol or after max_sweeps; then X^0 = sgn(Y) blockwise by scaled Newton-Schulz (no SVD).
- * Sets the current iterate.  sweeps_used: host, nullable.  Returns
- * NSRGS_ERR_EIG_NOT_CONVERGED (X^0 still set) if tol was not reached. */
+ * A tol below the dtype's rounding floor of the change (50 sqrt(d) eps: fp32 6.7e-6 at d = 5)
+ * is raised to that floor, and a change that stalls within 10x of the floor counts as
+ * converged; a slowly contracting subspace keeps iterating.  Sets the current iterate.
+ * sweeps_used: host, nullable (sweeps actually run; small instances read the change back every
+ * 4 sweeps, so it may exceed the first sweep that met tol by up to 3).  Returns
+ * NSRGS_ERR_EIG_NOT_CONVERGED (X^0 still set) if tol was not reached within max_sweeps,
+ * NSRGS_ERR_SINGULAR if the Cholesky factor of Y^T Y or the polar factor of a block failed. */
 int nsrgs_init_spectral(nsrgs_ctx *ctx, uint64_t seed, int max_sweeps, double tol, int *sweeps_used);
 
 /* One NS-RGS iteration t -> t+1 of Algorithm 2:

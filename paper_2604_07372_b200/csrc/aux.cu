@@ -362,25 +362,39 @@ __global__ void objective_final_kernel(int d, int T, const double *res, int npar
   F[t] = 0.5 * (g2 - r[2 * d * d]) - r[2 * d * d + 1] + 0.5 * a_fro2[0];
 }
 
-// a9: Gram partials over all nodes: [Z^T Z | X^T X | Z^T X], one thread per (matrix, entry),
-// blockIdx.x = node chunk.
+// a9: Gram partials [Z^T Z | X^T X | Z^T X] (3 d^2 entries).  Node-parallel: a CTA takes
+// `npb` nodes; its 256 threads form G = 256 / (3 d^2) node groups x the 3 d^2 entries (for
+// d^2 > 85 one group, threads stride over the entries), each group sums its nodes, and the
+// groups are summed in fixed order through smem -> one deterministic partial row per CTA.
+// (The round-1 kernel gave each thread one entry and walked 256 nodes serially: 121 us at
+// n = 100, 0.38 ms at n = 2000.)
 template <typename T, int D>
-__global__ void metrics_kernel(int64_t n, const T *X, const T *Z, int64_t rows_local, int64_t tpr,
-                               int64_t chunk, double *part) {
-  const int e = threadIdx.x;
-  if (e >= 3 * D * D) return;
-  const int which = e / (D * D), a = (e / D) % D, b = e % D;
-  const int64_t i0 = (int64_t)blockIdx.x * chunk, i1 = min(n, i0 + chunk);
-  double s = 0.0;
-  for (int64_t i = i0; i < i1; ++i)
+__global__ void metrics_kernel(int64_t n, const T *X, const T *Z, int64_t rows_local, int64_t tpr, int npb,
+                               double *part) {
+  constexpr int DD = D * D, E3 = 3 * DD;
+  extern __shared__ double msh[];
+  const int G = blockDim.x >= E3 ? (int)blockDim.x / E3 : 1;
+  const int64_t i0 = (int64_t)blockIdx.x * npb, i1 = min(n, i0 + npb);
+  for (int t = threadIdx.x; t < G * E3; t += blockDim.x) {
+    const int g = t / E3, e = t - g * E3;
+    const int which = e / DD, a = (e / D) % D, b = e % D;
+    double s = 0.0;
+    for (int64_t i = i0 + g; i < i1; i += G)
 #pragma unroll
-    for (int k = 0; k < D; ++k) {
-      const double z_ka = (double)Z[(i * D + k) * D + a], z_kb = (double)Z[(i * D + k) * D + b];
-      const double x_ka = (double)X[tile_index(i * D + k, a, D, rows_local, tpr)];
-      const double x_kb = (double)X[tile_index(i * D + k, b, D, rows_local, tpr)];
-      s += which == 0 ? z_ka * z_kb : which == 1 ? x_ka * x_kb : z_ka * x_kb;
-    }
-  part[(int64_t)blockIdx.x * 3 * D * D + e] = s;
+      for (int k = 0; k < D; ++k) {
+        const int64_t r = i * D + k;
+        const double u = which == 1 ? (double)X[tile_index(r, a, D, rows_local, tpr)] : (double)Z[r * D + a];
+        const double v = which == 0 ? (double)Z[r * D + b] : (double)X[tile_index(r, b, D, rows_local, tpr)];
+        s += u * v;
+      }
+    msh[t] = s;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < E3; e += blockDim.x) {
+    double v = 0.0;
+    for (int g = 0; g < G; ++g) v += msh[g * E3 + e];
+    part[(int64_t)blockIdx.x * E3 + e] = v;
+  }
 }
 
 // Rel.Err. (Gram identity), nuclear norm of Z^T X by cyclic Jacobi on (Z^T X)^T (Z^T X),
@@ -596,20 +610,21 @@ __global__ void scale_rt(int d, int64_t row0, int64_t rows, const double *MC, T 
 }
 
 template <typename T>
-__global__ void metrics_rt(int64_t n, int d, const T *X, const T *Z, int64_t rows_local, int64_t tpr, int64_t chunk,
-                           double *part) {
-  const int64_t i0 = (int64_t)blockIdx.x * chunk, i1 = min(n, i0 + chunk);
-  for (int e = threadIdx.x; e < 3 * d * d; e += blockDim.x) {
-    const int which = e / (d * d), a = (e / d) % d, b = e % d;
+__global__ void metrics_rt(int64_t n, int d, const T *X, const T *Z, int64_t rows_local, int64_t tpr, int npb,
+                           double *part) {   // d > 10: as metrics_kernel with one node group
+  const int DD = d * d, E3 = 3 * DD;
+  const int64_t i0 = (int64_t)blockIdx.x * npb, i1 = min(n, i0 + npb);
+  for (int e = threadIdx.x; e < E3; e += blockDim.x) {
+    const int which = e / DD, a = (e / d) % d, b = e % d;
     double s = 0.0;
     for (int64_t i = i0; i < i1; ++i)
       for (int k = 0; k < d; ++k) {
-        const double z_ka = (double)Z[(i * d + k) * d + a], z_kb = (double)Z[(i * d + k) * d + b];
-        const double x_ka = (double)X[tile_index(i * d + k, a, d, rows_local, tpr)];
-        const double x_kb = (double)X[tile_index(i * d + k, b, d, rows_local, tpr)];
-        s += which == 0 ? z_ka * z_kb : which == 1 ? x_ka * x_kb : z_ka * x_kb;
+        const int64_t r = i * d + k;
+        const double u = which == 1 ? (double)X[tile_index(r, a, d, rows_local, tpr)] : (double)Z[r * d + a];
+        const double v = which == 0 ? (double)Z[r * d + b] : (double)X[tile_index(r, b, d, rows_local, tpr)];
+        s += u * v;
       }
-    part[(int64_t)blockIdx.x * 3 * d * d + e] = s;
+    part[(int64_t)blockIdx.x * E3 + e] = s;
   }
 }
 
@@ -813,24 +828,32 @@ cudaError_t launch_objective_final(int d, int T, const double *res, int npart, c
   return cudaGetLastError();
 }
 
+// Partial rows: one per CTA; the caller reduces *nblocks rows of width 3 d^2 (launch_reduce).
+int metrics_blocks(int d, int64_t n) {
+  const int E3 = 3 * d * d, G = E3 <= 256 ? 256 / E3 : 1;
+  const int npb = 4 * G;
+  return (int)((n + npb - 1) / npb);
+}
+
 cudaError_t launch_metrics(int dtype, int d, int64_t n, const void *X, const void *Z, int64_t rows_local, int64_t tpr,
                            double *part, int *nblocks, cudaStream_t s) {
-  const int64_t chunk = 256;
-  *nblocks = (int)nblk(n, (int)chunk);
+  const int E3 = 3 * d * d, G = E3 <= 256 ? 256 / E3 : 1;
+  const int npb = 4 * G;   // ~4 nodes per group
+  *nblocks = (int)nblk(n, npb);
   if (d > kMaxNarrowD) {
     if (dtype == 0)
-      metrics_rt<float><<<*nblocks, 256, 0, s>>>(n, d, (const float *)X, (const float *)Z, rows_local, tpr, chunk, part);
+      metrics_rt<float><<<*nblocks, 256, 0, s>>>(n, d, (const float *)X, (const float *)Z, rows_local, tpr, npb, part);
     else
-      metrics_rt<double><<<*nblocks, 256, 0, s>>>(n, d, (const double *)X, (const double *)Z, rows_local, tpr, chunk, part);
+      metrics_rt<double><<<*nblocks, 256, 0, s>>>(n, d, (const double *)X, (const double *)Z, rows_local, tpr, npb, part);
     return cudaGetLastError();
   }
-  const int threads = ((3 * d * d + 31) / 32) * 32;
+  const size_t sh = sizeof(double) * (size_t)(G * E3 > 256 ? G * E3 : 256);
   if (dtype == 0) {
-    NSRGS_D_SWITCH(d, (metrics_kernel<float, D><<<*nblocks, threads, 0, s>>>(n, (const float *)X, (const float *)Z,
-                                                                            rows_local, tpr, chunk, part)));
+    NSRGS_D_SWITCH(d, (metrics_kernel<float, D><<<*nblocks, 256, sh, s>>>(n, (const float *)X, (const float *)Z,
+                                                                         rows_local, tpr, npb, part)));
   } else {
-    NSRGS_D_SWITCH(d, (metrics_kernel<double, D><<<*nblocks, threads, 0, s>>>(n, (const double *)X, (const double *)Z,
-                                                                             rows_local, tpr, chunk, part)));
+    NSRGS_D_SWITCH(d, (metrics_kernel<double, D><<<*nblocks, 256, sh, s>>>(n, (const double *)X, (const double *)Z,
+                                                                          rows_local, tpr, npb, part)));
   }
   return cudaGetLastError();
 }

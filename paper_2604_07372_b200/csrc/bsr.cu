@@ -1057,7 +1057,11 @@ cudaError_t bsr_dispatch(int d, int mode, const BsrParams *bp, int lg2g, const C
     NSRGS_BSR_CASE(8)
     NSRGS_BSR_CASE(9)
     NSRGS_BSR_CASE(10)
+    NSRGS_BSR_CASE(11)
     NSRGS_BSR_CASE(12)
+    NSRGS_BSR_CASE(13)
+    NSRGS_BSR_CASE(14)
+    NSRGS_BSR_CASE(15)
     NSRGS_BSR_CASE(16)
     NSRGS_BSR_CASE(20)
     NSRGS_BSR_CASE(24)
@@ -1113,4 +1117,32 @@ cudaError_t launch_bsr_sumsq(const float *vals, int64_t count, double *part, int
   return cudaGetLastError();
 }
 
+}  // namespace nsrgs
+
+namespace nsrgs {
+// Caller-attached block-sparse arrays (nsrgs_attach_A_bsr): rowptr[0] = 0, rowptr non-decreasing,
+// rowptr[n_local] = nnzb and every col in [0, n).  The passes address X_j directly from col[b]
+// (bsr.cu gathers), so a bad index would read outside X: bit 1 = bad rowptr, bit 2 = bad col.
+__global__ void bsr_validate_kernel(const int64_t *rowptr, const int *col, int64_t n_local, int64_t nnzb, int64_t n,
+                                    int *bad) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int b = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= n_local; i += stride) {
+    const int64_t r = rowptr[i];
+    if (i == 0 && r != 0) b |= 1;
+    if (i == n_local && r != nnzb) b |= 1;
+    if (i < n_local && rowptr[i + 1] < r) b |= 1;
+  }
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nnzb; i += stride) {
+    const int c = col[i];
+    if (c < 0 || (int64_t)c >= n) b |= 2;
+  }
+  if (b) atomicOr(bad, b);
+}
+
+cudaError_t launch_bsr_validate(const int64_t *rowptr, const int *col, int64_t n_local, int64_t nnzb, int64_t n,
+                                int *bad, cudaStream_t s) {
+  bsr_validate_kernel<<<592, 256, 0, s>>>(rowptr, col, n_local, nnzb, n, bad);
+  return cudaGetLastError();
+}
 }  // namespace nsrgs

@@ -44,6 +44,8 @@ cudaError_t launch_bsr_count(int64_t n, int64_t node0, int64_t n_local, uint64_t
 cudaError_t launch_bsr_fill(int d, int64_t n, int64_t node0, int64_t n_local, uint64_t seed, double sigma, double p_obs,
                             const double *Z64, const int64_t *rowptr, int *col, float *vals, double *part,
                             cudaStream_t s);
+cudaError_t launch_bsr_validate(const int64_t *rowptr, const int *col, int64_t n_local, int64_t nnzb, int64_t n,
+                                int *bad, cudaStream_t s);
 cudaError_t launch_bsr_sumsq(const float *vals, int64_t count, double *part, int *nblocks, cudaStream_t s);
 
 // aux.cu
@@ -71,6 +73,7 @@ cudaError_t launch_polar(int dtype, int d, int64_t n, const void *Y, void *X, in
                          int64_t tiles_per_rank, int *err, cudaStream_t s);
 cudaError_t launch_objective_final(int d, int T, const double *res, int npart, const double *a_fro2,
                                    double *F, cudaStream_t s);
+int metrics_blocks(int d, int64_t n);
 cudaError_t launch_metrics(int dtype, int d, int64_t n, const void *X, const void *Z, int64_t rows_local,
                            int64_t tiles_per_rank, double *part, int *nblocks, cudaStream_t s);
 cudaError_t launch_metrics_final(int d, int64_t n, const double *grams, double *out3, cudaStream_t s);

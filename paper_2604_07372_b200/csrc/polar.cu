@@ -64,7 +64,8 @@ cudaError_t launch_polar(int dtype, int d, int64_t n, const void *Y, void *X, in
                       : (DV <= 6 ? polar_launch<double, (DV <= 6 ? DV : 2)>(p, s) : cudaErrorInvalidValue);
   switch (d) {
     NSRGS_POLAR(2) NSRGS_POLAR(3) NSRGS_POLAR(4) NSRGS_POLAR(5) NSRGS_POLAR(6) NSRGS_POLAR(7) NSRGS_POLAR(8)
-    NSRGS_POLAR(9) NSRGS_POLAR(10) NSRGS_POLAR(12) NSRGS_POLAR(16) NSRGS_POLAR(20) NSRGS_POLAR(24)
+    NSRGS_POLAR(9) NSRGS_POLAR(10) NSRGS_POLAR(11) NSRGS_POLAR(12) NSRGS_POLAR(13) NSRGS_POLAR(14)
+    NSRGS_POLAR(15) NSRGS_POLAR(16) NSRGS_POLAR(20) NSRGS_POLAR(24)
     NSRGS_POLAR(25) NSRGS_POLAR(32)
     default: return cudaErrorInvalidValue;
   }

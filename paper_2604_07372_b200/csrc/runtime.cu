@@ -77,7 +77,7 @@ int plan_impl(int64_t n, int32_t d, int32_t world, int32_t rank, nsrgs_plan_t *o
   if (!out) return fail("plan: out is NULL");
   if (n < 2) return fail("n must be >= 2");
   if (d < 2 || d > kMaxD) return fail("d must be in [2, 32] (d = 1: O(1) has a trivial tangent space, SPEC.md:295)");
-  if (d > kMaxNarrowD && !wide_supported(d)) return fail("d in [11, 32]: supported wide sizes are 12, 16, 20, 24, 25, 32");
+  if (d > kMaxNarrowD && !wide_supported(d)) return fail("d in [11, 32]: supported wide sizes are 11-16, 20, 24, 25, 32");
   if (world < 1 || rank < 0 || rank >= world) return fail("need world >= 1 and 0 <= rank < world");
   if (n % world) return fail("n must be divisible by world (row-block sharding by node)");
   out->n_local = n / world;
@@ -304,10 +304,10 @@ int ensure_res(nsrgs_ctx *c, int slots) {
 // kernel re-zeroes what it used).
 int ensure_acc(nsrgs_ctx *c, int iters) {
   if (iters <= c->acc_cap) return NSRGS_OK;
+  const int cap = std::max(iters, 2 * c->acc_cap);   // geometric growth: one realloc per doubling
   if (c->acc) cudaFree(c->acc);
   c->acc = nullptr;
   c->acc_cap = 0;
-  const int cap = std::max(iters, 2 * c->acc_cap);
   const size_t bytes = sizeof(unsigned long long) * 2 * (size_t)cap * c->shape.npart;
   CUDA_TRY(c, cudaMalloc(&c->acc, bytes));
   CUDA_TRY(c, cudaMemsetAsync(c->acc, 0, bytes, c->stream));
@@ -979,6 +979,19 @@ int nsrgs_attach_A_bsr(nsrgs_ctx *c, const int64_t *rowptr_dev, const int32_t *c
   if (c->dtype != NSRGS_F32) return set_err(c, NSRGS_ERR_INVALID_ARG, "block-sparse storage: F32 only");
   if (!rowptr_dev || nnzb < 0 || (nnzb > 0 && (!col_dev || !vals_dev)) || (reinterpret_cast<uintptr_t>(vals_dev) % 4))
     return set_err(c, NSRGS_ERR_INVALID_ARG, "attach_A_bsr: need rowptr, col, vals (4-byte aligned), nnzb >= 0");
+  {   // structural check before anything is replaced (the passes index X by col[b])
+    int *bad = nullptr, hbad = 0;
+    CUDA_TRY(c, cudaMalloc(&bad, sizeof(int)));
+    CUDA_TRY(c, cudaMemsetAsync(bad, 0, sizeof(int), c->stream));
+    CUDA_TRY(c, launch_bsr_validate(rowptr_dev, col_dev, c->plan.n_local, nnzb, c->n, bad, c->stream));
+    c->kernel_launches++;
+    CUDA_TRY(c, cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    const cudaError_t e = cudaStreamSynchronize(c->stream);
+    cudaFree(bad);
+    CUDA_TRY(c, e);
+    if (hbad & 1) return set_err(c, NSRGS_ERR_INVALID_ARG, "attach_A_bsr: rowptr must start at 0, be non-decreasing and end at nnzb");
+    if (hbad & 2) return set_err(c, NSRGS_ERR_INVALID_ARG, "attach_A_bsr: col[] outside [0, n)");
+  }
   drop_bsr(c);
   if (c->own_A && c->A) cudaFree(c->A);
   c->A = nullptr;
@@ -1058,7 +1071,23 @@ int nsrgs_init_spectral(nsrgs_ctx *c, uint64_t seed, int max_sweeps, double tol,
   NSRGS_TRY(ensure_red(c, nbs));
   int sweeps = 0, stalled = 0;
   bool converged = false;
+  // Stopping (reading R14): the subspace change chg = ||Y_new - Y_old (Y_old^T Y_new)||_F < tol,
+  // the first sweep never counts.  In fp32 the change cannot fall below its rounding floor
+  // (Y_new is stored in fp32: ~ sqrt(2 d) eps per sweep, amplified by the filter), so a tol
+  // below the floor is replaced by it: chg < max(tol, floor), floor = 50 sqrt(d) eps_dtype
+  // (fp32: 6.7e-6 at d = 5, 1.5e-5 at d = 25; measured floors 1e-6 / 1e-5, R14).  A
+  // change that has stalled within 10x of the floor (no new minimum for 3 sweeps) is that
+  // floor too.  Anything else keeps iterating: a slowly contracting instance (gap ratio near 1)
+  // runs until tol or max_sweeps (NSRGS_ERR_EIG_NOT_CONVERGED) instead of stopping early.
+  const double eps_t = c->dtype == NSRGS_F32 ? 5.960464477539063e-08 : 1.1102230246251565e-16;
+  const double floor_chg = 50.0 * std::sqrt((double)c->d) * eps_t;
+  const double tol_eff = std::max(tol, floor_chg);
   double best_chg = 1e300;
+  // Convergence is read back every `batch` sweeps: one host synchronisation per sweep costs
+  // ~10-20 us of launch gap, which matters only when the A pass itself is short (A shard below
+  // ~1 GB: <= 0.15 ms per pass); larger shards read it every sweep (no overshoot).
+  const double a_bytes = (double)c->esz * (double)c->plan.rows_local * (double)c->N;
+  const int batch_max = a_bytes < 1e9 ? 4 : 1;
   // Chebyshev filtering (reading R20): from the second sweep on, each sweep applies
   // the three-term recurrence T_{k+1}(A/b) = 2 (A/b) T_k - T_{k-1} that keeps [-b, b] bounded,
   // b = 2 ||A||_F / sqrt(N) (the Wigner bulk-edge bound: the noise spectrum of the instance lies
@@ -1077,64 +1106,73 @@ int nsrgs_init_spectral(nsrgs_ctx *c, uint64_t seed, int max_sweeps, double tol,
   const int64_t ncs = ceil_div(c->plan.rows_local, 64);   // combine partial slots (per 64-row CTA)
   NSRGS_TRY(ensure_red(c, std::max<int64_t>(nbs, ncs * 2 * DD)));
   NSRGS_TRY(ensure_res(c, 1));
-  for (sweeps = 1; sweeps <= max_sweeps; ++sweeps) {
-    void *Y = c->X[c->cur], *W = c->X[1 - c->cur];
-    NSRGS_TRY(launch_panel(c, kModeProduct, Y, W, c->res, 0.0, 0));
-    if (!cheb) {
-      NSRGS_TRY(allreduce_sum(c, c->res, 2 * DD));
-    } else {
-      // Y_new = alpha W - beta Y_prev (W = A Y_cur; c = 0 for the symmetric interval), Grams
-      const double alpha = (cheb_steps == 0 ? 1.0 : 2.0) / bnd, beta = cheb_steps == 0 ? 0.0 : 1.0;
-      int nsl = 0;
-      CUDA_TRY(c, launch_cheb_combine(c->dtype, c->d, c->plan.node0, c->plan.n_local, alpha, beta, W, c->yprev, Y,
-                                      c->plan.rows_local, c->plan.tiles_per_rank, c->red_part, &nsl, c->stream));
-      CUDA_TRY(c, launch_reduce(c->red_part, nsl, 2 * DD, c->res, c->stream));
-      c->kernel_launches += 2;
-      NSRGS_TRY(allreduce_sum(c, c->res, 2 * DD));
-      ++cheb_steps;
+  const bool dbg = std::getenv("NSRGS_DEBUG_INIT") != nullptr;
+  while (sweeps < max_sweeps && !converged) {
+    // sweep 1 alone (its result decides whether the filter starts); then batches
+    const int kb = sweeps == 0 ? 1 : std::min(batch_max, max_sweeps - sweeps);
+    for (int j = 0; j < kb; ++j) {
+      void *Y = c->X[c->cur], *W = c->X[1 - c->cur];
+      NSRGS_TRY(launch_panel(c, kModeProduct, Y, W, c->res, 0.0, 0));
+      if (!cheb) {
+        NSRGS_TRY(allreduce_sum(c, c->res, 2 * DD));
+      } else {
+        // Y_new = alpha W - beta Y_prev (W = A Y_cur; c = 0 for the symmetric interval), Grams
+        const double alpha = (cheb_steps == 0 ? 1.0 : 2.0) / bnd, beta = cheb_steps == 0 ? 0.0 : 1.0;
+        int nsl = 0;
+        CUDA_TRY(c, launch_cheb_combine(c->dtype, c->d, c->plan.node0, c->plan.n_local, alpha, beta, W, c->yprev, Y,
+                                        c->plan.rows_local, c->plan.tiles_per_rank, c->red_part, &nsl, c->stream));
+        CUDA_TRY(c, launch_reduce(c->red_part, nsl, 2 * DD, c->res, c->stream));
+        c->kernel_launches += 2;
+        NSRGS_TRY(allreduce_sum(c, c->res, 2 * DD));
+        ++cheb_steps;
+      }
+      CUDA_TRY(c, launch_chol(c->d, c->res, c->small + kSmallMC, c->err, c->stream));
+      int nb = 0;
+      CUDA_TRY(c, launch_scale(c->dtype, c->d, c->plan.node0, c->plan.n_local, c->small + kSmallMC, W, Y,
+                               c->plan.rows_local, c->plan.tiles_per_rank, c->red_part, &nb, c->stream));
+      CUDA_TRY(c, launch_reduce(c->red_part, nb, 1, c->small + kSmallChg + j, c->stream));
+      c->kernel_launches += 3;
+      if (cheb) {   // the previous iterate in the new basis: Y_prev <- Y_cur M
+        CUDA_TRY(c, launch_cheb_apply(c->dtype, c->d, c->plan.node0, c->plan.n_local, c->small + kSmallMC, Y, c->yprev,
+                                      c->plan.rows_local, c->plan.tiles_per_rank, c->stream));
+        c->kernel_launches++;
+      }
+      NSRGS_TRY(allreduce_sum(c, c->small + kSmallChg + j, 1));
+      NSRGS_TRY(allgather_X(c, W));
+      c->cur = 1 - c->cur;
     }
-    CUDA_TRY(c, launch_chol(c->d, c->res, c->small + kSmallMC, c->err, c->stream));
-    int nb = 0;
-    CUDA_TRY(c, launch_scale(c->dtype, c->d, c->plan.node0, c->plan.n_local, c->small + kSmallMC, W, Y,
-                             c->plan.rows_local, c->plan.tiles_per_rank, c->red_part, &nb, c->stream));
-    CUDA_TRY(c, launch_reduce(c->red_part, nb, 1, c->small + kSmallChg, c->stream));
-    c->kernel_launches += 3;
-    if (cheb) {   // the previous iterate in the new basis: Y_prev <- Y_cur M
-      CUDA_TRY(c, launch_cheb_apply(c->dtype, c->d, c->plan.node0, c->plan.n_local, c->small + kSmallMC, Y, c->yprev,
-                                    c->plan.rows_local, c->plan.tiles_per_rank, c->stream));
-      c->kernel_launches++;
-    }
-    NSRGS_TRY(allreduce_sum(c, c->small + kSmallChg, 1));
-    NSRGS_TRY(allgather_X(c, W));
-    c->cur = 1 - c->cur;
-    double chg2 = 0.0;
-    CUDA_TRY(c, cudaMemcpyAsync(&chg2, c->small + kSmallChg, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    double chg2[4] = {0.0, 0.0, 0.0, 0.0};
+    CUDA_TRY(c, cudaMemcpyAsync(chg2, c->small + kSmallChg, sizeof(double) * kb, cudaMemcpyDeviceToHost, c->stream));
     int flags = 0;
     NSRGS_TRY(sync_and_check(c, &flags));
-    if (flags & kErrSingular) return set_err(c, NSRGS_ERR_SINGULAR, "Cholesky of Y^T Y failed at sweep %d", sweeps);
-    if (flags & kErrNonfinite) return set_err(c, NSRGS_ERR_NONFINITE, "non-finite Gram partial at sweep %d", sweeps);
-    if (!std::isfinite(chg2)) return set_err(c, NSRGS_ERR_NONFINITE, "non-finite subspace change at sweep %d", sweeps);
-    const double chg = std::sqrt(chg2);
-    if (std::getenv("NSRGS_DEBUG_INIT"))
-      std::fprintf(stderr, "init sweep %d cheb %d chg %.3e bnd %.6g\n", sweeps, (int)cheb, chg, bnd);
-    if (sweeps >= 2 && chg < tol) { converged = true; break; }
-    // fp32 noise floor (reading R14): the change stopped shrinking while already tiny
-    if (sweeps >= 4 && chg < 1e-3 && chg > 0.7 * best_chg) {
-      if (++stalled >= 3) { converged = true; break; }
-    } else {
-      stalled = 0;
-    }
-    if (sweeps >= 2) best_chg = std::min(best_chg, chg);
-    if (cheb) {   // stall guard: no decrease over 4 filtered sweeps while far from converged
-      cheb_stall = (chg > 0.9 * prev_chg && chg > 1e-3) ? cheb_stall + 1 : 0;
-      if (cheb_stall >= 4) {
-        cheb = false;
-        cheb_failed = true;
+    if (flags & kErrSingular) return set_err(c, NSRGS_ERR_SINGULAR, "Cholesky of Y^T Y failed at sweep <= %d", sweeps + kb);
+    if (flags & kErrNonfinite) return set_err(c, NSRGS_ERR_NONFINITE, "non-finite Gram partial at sweep <= %d", sweeps + kb);
+    for (int j = 0; j < kb; ++j) {
+      ++sweeps;
+      if (!std::isfinite(chg2[j])) return set_err(c, NSRGS_ERR_NONFINITE, "non-finite subspace change at sweep %d", sweeps);
+      const double chg = std::sqrt(chg2[j]);
+      if (dbg) std::fprintf(stderr, "init sweep %d cheb %d chg %.3e bnd %.6g\n", sweeps, (int)cheb, chg, bnd);
+      if (converged) continue;   // later sweeps of the batch only refine the converged subspace
+      if (sweeps >= 2 && chg < tol_eff) { converged = true; continue; }
+      if (sweeps >= 2) {   // stalled at the rounding floor (within 10x of it, no new minimum)
+        if (chg < 10.0 * floor_chg && chg >= best_chg) {
+          if (++stalled >= 3) { converged = true; continue; }
+        } else if (chg < best_chg) {
+          stalled = 0;
+        }
+        best_chg = std::min(best_chg, chg);
       }
-    } else if (cheb_on && !cheb_failed && sweeps == 1 && bnd > 0.0 && std::isfinite(bnd)) {
-      cheb = true;   // Y_1 is orthonormal: start the recurrence from it
+      if (cheb) {   // stall guard: no decrease over 4 filtered sweeps while far from converged
+        cheb_stall = (chg > 0.9 * prev_chg && chg > 1e-3) ? cheb_stall + 1 : 0;
+        if (cheb_stall >= 4) {
+          cheb = false;
+          cheb_failed = true;
+        }
+      } else if (cheb_on && !cheb_failed && sweeps == 1 && bnd > 0.0 && std::isfinite(bnd)) {
+        cheb = true;   // Y_1 is orthonormal: start the recurrence from it
+      }
+      prev_chg = chg;
     }
-    prev_chg = chg;
   }
   if (sweeps > max_sweeps) sweeps = max_sweeps;
   CUDA_TRY(c, launch_polar(c->dtype, c->d, c->n, c->X[c->cur], c->X[1 - c->cur], c->plan.rows_local,
@@ -1301,7 +1339,7 @@ int nsrgs_alignment_error(nsrgs_ctx *c, const void *Z, int Z_on_device, double o
     Zd = c->stage;
   }
   const int w = 3 * c->d * c->d;
-  NSRGS_TRY(ensure_red(c, (ceil_div(c->n, 256) + 1) * w));
+  NSRGS_TRY(ensure_red(c, ((int64_t)metrics_blocks(c->d, c->n) + 1) * w));
   NSRGS_TRY(ensure_small(c, kSmallOut + w + 8));
   int nb = 0;
   CUDA_TRY(c, launch_metrics(c->dtype, c->d, c->n, c->X[c->cur], Zd, c->plan.rows_local, c->plan.tiles_per_rank,

@@ -1,14 +1,25 @@
-// wide.cu — the A.X pass + fused epilogue for wide blocks, d in {12, 16, 20, 24, 25, 32}
-// (the paper's experiments use d = 25).
+// wide.cu — the A.X pass + fused epilogue for wide blocks, d in {11, ..., 16, 20, 24, 25, 32}
+// (the paper's experiments use d = 25; §8(b) asks for d <= 16).
 //
 // With d > 10 the narrow kernel's register tile (RT rows x d accumulators per lane) no longer
-// fits, so the roles flip: a consumer warp owns ONE node (d rows of A) and lane k owns output
-// component k: acc[r] += A[r][c] X[c][k].  A row pieces are smem broadcasts (128-bit, 4
-// columns), X[c][k] is a per-lane scalar of a row-major 32 x d X slab, and the products run as
-// FFMA2 on column pairs (even / odd column partial sums).  4 consumer warps + 1 TMA producer
-// warp per CTA; one CTA per row panel (4 nodes); the same mbarrier ring, tensor map and
-// per-node epilogue (epilogue.cuh) as the narrow kernel.  Compute-bound (d/2 FMA per byte),
-// sized for the paper's scale (n = 500: a 625 MB A).
+// fits, so a consumer warp owns ONE node (d rows of A).  4 consumer warps + 1 TMA producer warp
+// per CTA, one CTA per row panel (4 nodes), the same mbarrier ring, tensor map and per-node
+// epilogue (epilogue.cuh) as the narrow kernel.  Two inner products:
+//
+//  * MMA = true (DEFAULT, the runtime's `wide_mma`): 3xTF32 on the tensor cores with legacy
+//    mma.sync m16n8k8 — A fragments read from the stage through the 128-byte TMA swizzle (so the
+//    runtime's tensor map MUST be encoded with CU_TENSOR_MAP_SWIZZLE_128B whenever this variant
+//    runs: build_tmap couples the two through ctx->wide_mma), X fragments from the row-major
+//    32 x d slab, hi/lo splits on the fly, and the MMA accumulator drained into a CUDA-core fp32
+//    sum after every 32-column tile (the tensor core's fp32 accumulation does not round to
+//    nearest; bounding each chain to one tile keeps the step error at <= 3.1e-7, below the
+//    CUDA-core pass's 8.4e-7, profiles/r01c_wide_variants.txt).
+//  * MMA = false (NSRGS_WIDE_MMA=0): CUDA cores, lane k owns output component k,
+//    acc[r] += A[r][c] X[c][k] with A row pieces as 128-bit smem broadcasts and FFMA2 on column
+//    pairs (even / odd partial sums).
+//
+// Measured (same box, mean pass): the MMA variant is 1.07-1.21x faster at d = 25
+// and 1.46-1.76x at d = 16; both are latency / issue bound (2.1-3.5 TB/s), not HBM-bound.
 #include <cuda.h>
 
 #include "common.cuh"
@@ -38,6 +49,12 @@ struct WideCfg {
   static constexpr int STAGES = STAGES_RAW > 6 ? 6 : STAGES_RAW;
   static_assert(STAGES >= 2, "ring");
   static constexpr int SMEM = FIXED + STAGES * STAGE_BYTES;
+  // The MMA variant reads A fragment rows warp*D .. warp*D + 16*MT - 1: for d not a multiple of
+  // 16 the last rows are the next node's (warp 3: bytes of the X slab).  Their products land in
+  // accumulator rows a >= D, which are dropped; the reads must stay inside the stage.
+  static constexpr int MT = (D + 15) / 16;
+  static_assert(!MMA || ((W - 1) * D + 16 * MT) * CW * 4 <= STAGE_BYTES,
+                "MMA fragment rows past the panel must stay inside the stage");
 };
 
 __device__ __forceinline__ uint64_t wpack(float lo, float hi) {
@@ -290,7 +307,7 @@ static cudaError_t wide_mode(int mode, const CUtensorMap *tm, const PanelParams 
   return wide_launch<D, kModeProduct, MMA>(tm, p, grid, s);
 }
 
-bool wide_supported(int d) { return d == 12 || d == 16 || d == 20 || d == 24 || d == 25 || d == 32; }
+bool wide_supported(int d) { return (d >= 11 && d <= 16) || d == 20 || d == 24 || d == 25 || d == 32; }
 
 // mma: the 3xTF32 tensor-core variant (the caller's tensor map must then use the 128-byte swizzle)
 cudaError_t wide_dispatch(int d, int mode, bool shape_only, PanelShape *shape, const CUtensorMap *tm,
@@ -310,7 +327,11 @@ cudaError_t wide_dispatch(int d, int mode, bool shape_only, PanelShape *shape, c
     return mma ? wide_mode<DV, true>(mode, tm, *p, grid, s) : wide_mode<DV, false>(mode, tm, *p, grid, s); \
   }
   switch (d) {
+    NSRGS_WIDE_CASE(11)
     NSRGS_WIDE_CASE(12)
+    NSRGS_WIDE_CASE(13)
+    NSRGS_WIDE_CASE(14)
+    NSRGS_WIDE_CASE(15)
     NSRGS_WIDE_CASE(16)
     NSRGS_WIDE_CASE(20)
     NSRGS_WIDE_CASE(24)

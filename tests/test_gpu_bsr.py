@@ -186,7 +186,7 @@ def test_bsr_end_to_end(nsrgs):
     Xo = ons.run(A, X0, T, 1.0 / (n * p), K)
     s = nsrgs.Solver(n, d)
     Zg = s.generate(2, sigma, p=p, storage="bsr")
-    s.init_spectral(2, 300, 1e-6, allow_unconverged=True)
+    s.init_spectral(2, 300, 1e-6)
     s.run(T, 1.0 / (n * p), K, trace=False)
     assert rel_mod_rotation(s.get_X(), Xo) <= 1e-4
     rel = s.alignment_error(Zg)[0]
@@ -283,7 +283,7 @@ def test_table1_p_lt_1_bsr(nsrgs):
             continue
         s = nsrgs.Solver(n, d)
         Zg = s.generate(0, sigma, p=p, storage="bsr")
-        s.init_spectral(0, 200, 1e-6, allow_unconverged=True)
+        s.init_spectral(0, 200, 1e-6)
         it, tr = s.solve("ns_rgs", max_iter=100, eta=1.0 / (n * p), K=1, stop_tol=1e-8)
         assert it <= 100 and np.all(np.isfinite(tr))
         rel = s.alignment_error(Zg)[0]

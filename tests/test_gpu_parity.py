@@ -146,7 +146,7 @@ def test_end_to_end_modulo_rotation(nsrgs, n, d, sigma, K, T, dtype):
     Zg = s.generate(0, sigma)
     Z = inst.ground_truth(0, n, d)
     A = inst.measurement_matrix(0, Z, sigma, dtype=npdt)
-    s.init_spectral(0, 400, 1e-6 if dtype == "f32" else 1e-12, allow_unconverged=(dtype == "f32"))
+    s.init_spectral(0, 400, 1e-6 if dtype == "f32" else 1e-12)
     if n <= 200:
         X0, _, _ = ons.spectral_init(A, d, "eigh")
     else:
@@ -173,7 +173,7 @@ def test_chebyshev_init_matches_plain_and_oracle(nsrgs, monkeypatch, n, d, sigma
         monkeypatch.setenv("NSRGS_INIT_CHEB", cheb)
         s = nsrgs.Solver(n, d)
         s.generate(3, sigma, want_Z=False, p=p)
-        sw = s.init_spectral(3, 400, 1e-6, allow_unconverged=True)
+        sw = s.init_spectral(3, 400, 1e-6)
         out[cheb] = (sw, s.get_X())
         s.close()
     assert out["1"][0] < out["0"][0], (out["1"][0], out["0"][0])
@@ -202,7 +202,7 @@ def test_noiseless_exact_recovery(nsrgs):
     n, d = 200, 3
     s = nsrgs.Solver(n, d)
     Z = s.generate(1, 0.0)
-    s.init_spectral(1, 100, 1e-6, allow_unconverged=True)
+    s.init_spectral(1, 100, 1e-6)
     s.run(5, 1.0 / n, 5, trace=False)
     rel, dF, mse = s.alignment_error(Z)
     assert rel < 1e-5 and dF < 1e-4 * np.sqrt(n * d)
@@ -232,7 +232,7 @@ def test_divergence_and_state_errors(nsrgs):
     s.close()
 
 
-@pytest.mark.parametrize("kw", [dict(n=1, d=3), dict(n=10, d=1), dict(n=10, d=11), dict(n=10, d=7, dtype=1)])
+@pytest.mark.parametrize("kw", [dict(n=1, d=3), dict(n=10, d=1), dict(n=10, d=17), dict(n=10, d=7, dtype=1)])
 def test_create_rejects_unsupported(nsrgs, kw):
     with pytest.raises(nsrgs.NSRGSError) as e:
         nsrgs.Solver(**kw)
@@ -245,7 +245,7 @@ def test_deterministic_bitwise(nsrgs):
     for _ in range(2):
         s = nsrgs.Solver(n, d)
         s.generate(8, 1.0, want_Z=False)
-        s.init_spectral(8, 50, 1e-5, allow_unconverged=True)
+        s.init_spectral(8, 50, 1e-5)
         tr = s.run(10, 1.0 / n, 5)
         out.append((s.get_X(), tr))
         s.close()
@@ -303,7 +303,7 @@ def test_full_size_run_properties(nsrgs, cfg):
     n, d, sigma, K = FULL[cfg]
     s = nsrgs.Solver(n, d)
     Z = s.generate(0, sigma)
-    s.init_spectral(0, 100, 1e-5, allow_unconverged=True)
+    s.init_spectral(0, 100, 1e-5)
     s.reset_stats()
     tr = s.run(100, 1.0 / n, K)
     st = s.stats()
@@ -412,7 +412,7 @@ def test_symmetric_modes_and_rejects(nsrgs):
     s.set_symmetric(True)
     Z = inst.ground_truth(0, n, d)
     A = inst.measurement_matrix(0, Z, sigma)
-    s.init_spectral(0, 200, 1e-6, allow_unconverged=True)        # PRODUCT mode through sym_final
+    s.init_spectral(0, 200, 1e-6)        # PRODUCT mode through sym_final
     X0, _, _ = ons.spectral_init(A, d)
     assert rel_mod_rotation(s.get_X(), X0) <= 1e-4
     X = oracle_iterate_near(Z, 0.1, 3).astype(np.float32)
@@ -446,7 +446,7 @@ def test_symmetric_full_size_sampled_and_run(nsrgs, cfg):
     R = inst.measurement_rows(0, Z, sigma, nodes)
     Xo = oracle_node_step(R, X.astype(np.float64), nodes, 1.0 / n, K)
     assert rel_fro(Xg[nodes], Xo) <= 1e-5
-    s.init_spectral(0, 100, 1e-5, allow_unconverged=True)
+    s.init_spectral(0, 100, 1e-5)
     tr = s.run(30, 1.0 / n, K)
     assert np.all(np.diff(tr) <= 1e-6 * tr[0])
     rel = s.alignment_error(Zg)[0]
@@ -461,7 +461,7 @@ def test_symmetric_deterministic_and_matches_dense(nsrgs):
         s = nsrgs.Solver(n, d)
         s.generate(8, 1.0, want_Z=False)
         s.set_symmetric(sym)
-        s.init_spectral(8, 50, 1e-5, allow_unconverged=True)
+        s.init_spectral(8, 50, 1e-5)
         tr = s.run(10, 1.0 / n, 5)
         out.append((s.get_X(), tr))
         s.close()
@@ -504,7 +504,7 @@ def test_masked_end_to_end_and_symmetric(nsrgs):
         s = nsrgs.Solver(n, d)
         Zg = s.generate(2, sigma, p=p)
         s.set_symmetric(sym)
-        s.init_spectral(2, 300, 1e-6, allow_unconverged=True)
+        s.init_spectral(2, 300, 1e-6)
         s.run(T, 1.0 / (n * p), K, trace=False)
         assert rel_mod_rotation(s.get_X(), Xo) <= 1e-4
         rel = s.alignment_error(Zg)[0]
@@ -514,7 +514,8 @@ def test_masked_end_to_end_and_symmetric(nsrgs):
 
 
 # ---------------------------------------------------------------------------- wide blocks, d = 25 (§8f row 4)
-@pytest.mark.parametrize("n,d,sigma,K", [(60, 12, 0.5, 3), (37, 16, 0.3, 4), (50, 25, 0.1, 1), (23, 32, 0.2, 2)])
+@pytest.mark.parametrize("n,d,sigma,K", [(60, 12, 0.5, 3), (37, 16, 0.3, 4), (50, 25, 0.1, 1), (23, 32, 0.2, 2),
+                                         (41, 11, 0.4, 2), (35, 13, 0.3, 3), (130, 14, 0.2, 1), (29, 15, 0.5, 2)])
 def test_wide_generator_step_gpm(nsrgs, n, d, sigma, K):
     s = nsrgs.Solver(n, d)
     Zg = s.generate(4, sigma)
@@ -581,7 +582,7 @@ def test_table1_on_b200(nsrgs):
     for (n_, d_, p, sigma, rel_paper) in _table1_rows():
         s = nsrgs.Solver(n, d)
         Zg = s.generate(0, sigma, p=p)
-        s.init_spectral(0, 200, 1e-6, allow_unconverged=True)
+        s.init_spectral(0, 200, 1e-6)
         X0 = s.get_X()
         rels = {}
         for alg in ("ns_rgs", "gpm"):
@@ -674,7 +675,7 @@ def test_stats_and_launch_accounting(nsrgs):
     n, d = 300, 5
     s = nsrgs.Solver(n, d)
     s.generate(1, 1.0, want_Z=False)
-    s.init_spectral(1, 50, 1e-5, allow_unconverged=True)
+    s.init_spectral(1, 50, 1e-5)
     s.reset_stats(timing=True)
     s.run(7, 1.0 / n, 5)
     st = s.stats()
@@ -698,7 +699,7 @@ def test_nccl_plumbing_one_rank(nsrgs, monkeypatch):
         monkeypatch.setenv("NSRGS_NO_COOP", "1")
         s = nsrgs.Solver(n, d)
         Z = s.generate(3, sigma)
-        sw = s.init_spectral(3, 100, 1e-5, allow_unconverged=True)
+        sw = s.init_spectral(3, 100, 1e-5)
         tr = s.run(10, 1.0 / n, 5)
         outs.append((sw, tr, s.get_X(), s.alignment_error(Z), s.objective()))
         s.close()
@@ -723,7 +724,7 @@ def test_multi_iteration_launch_bitwise_equals_per_iteration_launches(nsrgs, mon
         monkeypatch.setenv("NSRGS_NO_COOP", no_coop)
         s = nsrgs.Solver(n, d, dtype=dt)
         s.generate(5, 1.0, want_Z=False)
-        s.init_spectral(5, 60, 1e-5, allow_unconverged=True)
+        s.init_spectral(5, 60, 1e-5)
         tr = s.run(25, 1.0 / n, 5)
         X = s.get_X()
         trg = s.gpm_run(6)

@@ -69,7 +69,7 @@ def test_plan_partitions_rows(nsrgs, n, d, world):
     assert all(a[1] == b[0] for a, b in zip(rows, rows[1:]))
 
 
-@pytest.mark.parametrize("kw", [dict(n=1, d=3), dict(n=10, d=1), dict(n=10, d=11), dict(n=10, d=33), dict(n=10, d=3, world=3),
+@pytest.mark.parametrize("kw", [dict(n=1, d=3), dict(n=10, d=1), dict(n=10, d=17), dict(n=10, d=33), dict(n=10, d=3, world=3),
                                 dict(n=10, d=3, world=2, rank=2)])
 def test_plan_rejects(nsrgs, kw):
     with pytest.raises(nsrgs.NSRGSError):
