@@ -194,13 +194,23 @@ int nsrgs_gpm_run(nsrgs_ctx *ctx, int T, double *objective_trace);
 /* The paper's experimental protocol (§4.1): iterate `algorithm` from the
  * current X^0 until R^t = (F(X^t) - F(X^{t+1}))/F(X^{t+1}) < stop_tol or max_iter iterations.
  * On return X = X^{t_stop}; *iters_used = t_stop; objective_trace (host, nullable, length
- * max_iter + 1) receives F(X^0..X^{t_stop}).  eta, K are used by NSRGS_ALG_NSRGS only. */
+ * max_iter + 1) receives F(X^0..X^{t_stop}).  eta, K are used by NSRGS_ALG_NSRGS only.
+ * F32 contexts evaluate F with nsrgs_objective_fp64's pass (one extra A pass per iteration) so
+ * that the stop is decided by the iteration rather than by fp32 rounding of F; F64 contexts use
+ * the fp64 partials fused into the iteration's own pass. */
 typedef enum { NSRGS_ALG_NSRGS = 0, NSRGS_ALG_GPM = 1 } nsrgs_algorithm;
 int nsrgs_solve(nsrgs_ctx *ctx, int algorithm, int max_iter, double eta, int K, double stop_tol, int *iters_used,
                 double *objective_trace);
 
 /* F(X) of the current iterate (PAPER.md:70-72 Eq. def:f); one A pass. */
 int nsrgs_objective(nsrgs_ctx *ctx, double *F_out);
+
+/* F(X) of the current iterate with every product A_rc (X_r . X_c) formed and summed in fp64
+ * (F32 contexts; dense or block-sparse A): exact to ~1e-16 relative for the stored fp32 iterate,
+ * where nsrgs_objective's fp32-accumulated <X, A X> carries ~1e-7 relative error.  One extra A
+ * pass (fp64 FMA bound for d >= 10).  This is the evaluator nsrgs_solve uses for the stopping
+ * rule on F32 contexts.  INVALID_ARG for F64 contexts (use nsrgs_objective). */
+int nsrgs_objective_fp64(nsrgs_ctx *ctx, double *F_out);
 
 /* Recovery metrics of the current iterate against ground truth Z (n*d*d elements of dtype,
  * host if Z_on_device == 0 else device): out[0] = Rel.Err. = ||ZZ^T - XX^T||_F/||ZZ^T||_F

@@ -48,6 +48,22 @@ cudaError_t launch_bsr_validate(const int64_t *rowptr, const int *col, int64_t n
                                 int *bad, cudaStream_t s);
 cudaError_t launch_bsr_sumsq(const float *vals, int64_t count, double *part, int *nblocks, cudaStream_t s);
 
+// objective64.cu: F(X) with fp64 accumulation of <X, A X> (the nsrgs_solve stopping rule).
+struct Obj64Args {
+  const float *A;              // dense shard (NULL when block-sparse)
+  int64_t lda;
+  const int64_t *bsr_rowptr;   // block-sparse shard (NULL when dense)
+  const int *bsr_col;
+  const float *bsr_vals;
+  int64_t n, n_local, node0;
+  const float *Xs;             // row-major n d x d stack of X (all nodes)
+  double *part_x;              // [grid_x] <X_loc, (A X)_loc> partials
+  double *part_g;              // [grid_g][2 d^2 + 2] Gram partials
+  int grid_x, grid_g, sm_count;
+};
+void obj64_grids(int64_t n_local, int d, bool bsr, int sm_count, int *grid_x, int *grid_g);
+cudaError_t launch_obj64(int d, const Obj64Args &a, cudaStream_t s);
+
 // aux.cu
 cudaError_t launch_gen_Z(int dtype, int d, int64_t n, uint64_t seed, double *Z64, void *Zt, cudaStream_t s);
 cudaError_t launch_gen_A(int dtype, int d, int64_t n, int64_t node0, int64_t n_local, uint64_t seed,

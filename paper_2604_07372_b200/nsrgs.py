@@ -72,6 +72,7 @@ _SIGS = {
     "nsrgs_step": ([_P, ct.c_double, ct.c_int, ct.POINTER(ct.c_double)], ct.c_int),
     "nsrgs_run": ([_P, ct.c_int, ct.c_double, ct.c_int, ct.POINTER(ct.c_double)], ct.c_int),
     "nsrgs_objective": ([_P, ct.POINTER(ct.c_double)], ct.c_int),
+    "nsrgs_objective_fp64": ([_P, ct.POINTER(ct.c_double)], ct.c_int),
     "nsrgs_gpm_run": ([_P, ct.c_int, ct.POINTER(ct.c_double)], ct.c_int),
     "nsrgs_solve": ([_P, ct.c_int, ct.c_int, ct.c_double, ct.c_int, ct.c_double, ct.POINTER(ct.c_int),
                      ct.POINTER(ct.c_double)], ct.c_int),
@@ -279,6 +280,12 @@ class Solver:
     def objective(self) -> float:
         f = ct.c_double(0.0)
         self._check(_lib.nsrgs_objective(self._h, ct.byref(f)))
+        return f.value
+
+    def objective_fp64(self) -> float:
+        """F(X) with fp64-accumulated <X, A X> (F32 contexts; the solve stopping-rule evaluator)."""
+        f = ct.c_double(0.0)
+        self._check(_lib.nsrgs_objective_fp64(self._h, ct.byref(f)))
         return f.value
 
     def alignment_error(self, Z):

@@ -49,7 +49,7 @@ def test_init_singular_polar_block(nsrgs):
     """Node 0 disconnected (its block row and column of A zero): the top-d eigenvectors of A
     have Y_0 = 0 exactly (row 0 of A Y is zero every sweep), so sgn(Y_0) does not exist
     (PAPER.md:141 needs a full-rank block) -> NSRGS_ERR_SINGULAR from the init polar."""
-    n, d = 30, 3
+    n, d = 32, 3                                   # n d * 4 bytes: 16-byte aligned rows
     Z = inst.ground_truth(5, n, d)
     A = inst.measurement_matrix(5, Z, 0.05)
     A[:d, :] = 0.0
