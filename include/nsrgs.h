@@ -274,6 +274,19 @@ int nsrgs_debug_timestamps(nsrgs_ctx *ctx, int max_iters, unsigned long long *ou
  * all-gather fallback if any rank cannot map a peer; NSRGS_P2P=0 forces the fallback). */
 int nsrgs_debug_link_peers(nsrgs_ctx **ctxs, int world);
 
+/* Test-only: join `world` rank contexts created in ONE process with NSRGS_EMULATE_RANKS=1 into
+ * an in-process rank group whose collectives exchange real data (the multi-GPU collectives of
+ * nsrgs_generate, nsrgs_init_spectral, nsrgs_run / nsrgs_step / nsrgs_gpm_run / nsrgs_solve,
+ * nsrgs_objective(_fp64) on one GPU): the all-reduce of fp64 partials sums every rank's buffer
+ * in rank order, the X all-gather copies the other ranks' slices.  Each rank's calls must be
+ * issued from its own host thread (every call is collective, as with NCCL); collectives are
+ * host-synchronised, so no kernel waits for another rank.  A rank that does not reach a
+ * collective within 120 s fails it (and every later one) with NSRGS_ERR_NCCL.  ctxs[r] must be
+ * rank r of the same (n, d, dtype, device), not linked by nsrgs_debug_link_peers (the fused P2P
+ * exchange needs concurrently running ranks, i.e. one GPU per rank).  Returns INVALID_ARG
+ * otherwise.  The group lives until its last context is destroyed. */
+int nsrgs_debug_group(nsrgs_ctx **ctxs, int world);
+
 #ifdef __cplusplus
 }
 #endif

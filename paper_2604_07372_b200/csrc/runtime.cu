@@ -11,7 +11,10 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <condition_variable>
+#include <mutex>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -103,6 +106,53 @@ void pack_host_t(int64_t n, int d, const nsrgs_plan_t &pl, T *stack, T *tiled, b
 }
 }  // namespace
 
+// ------------------------------------------------------------------------------ in-process rank group
+// nsrgs_debug_group (test-only): `world` emulated rank contexts of ONE process on one GPU, each
+// driven by its own host thread, whose collectives exchange real data.  A collective is two
+// host barriers: every rank publishes its buffer after its stream has drained; each rank then
+// reads all ranks' buffers (all-reduce: one kernel summing them in rank order, so every rank
+// gets the same bits; all-gather: device-to-device copies of the other ranks' slices); the
+// second barrier keeps every buffer unchanged until all ranks have read it.  No kernel ever
+// waits for another rank's kernel (B200_PROFILING.md: such ranks must not share a GPU).
+struct RankGroup {
+  int world = 0, refs = 0;
+  std::mutex m;
+  std::condition_variable cv;
+  int arrived = 0;
+  unsigned long long gen = 0;
+  bool broken = false;                  // a rank timed out: every later barrier fails at once
+  void *ptr[kMaxWorld] = {};
+  bool barrier() {
+    std::unique_lock<std::mutex> lk(m);
+    if (broken) return false;
+    const unsigned long long g0 = gen;
+    if (++arrived == world) {
+      arrived = 0;
+      ++gen;
+      cv.notify_all();
+      return true;
+    }
+    const bool ok = cv.wait_for(lk, std::chrono::seconds(120), [&] { return gen != g0 || broken; });
+    if (!ok || broken) {
+      broken = true;
+      cv.notify_all();
+      return false;
+    }
+    return true;
+  }
+};
+std::mutex g_group_mu;   // RankGroup reference counts
+
+struct GroupPtrs { const double *p[kMaxWorld]; };
+
+__global__ void group_sum_kernel(GroupPtrs g, int world, int64_t count, double *out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int r = 0; r < world; ++r) acc += g.p[r][i];   // rank order: identical on every rank
+    out[i] = acc;
+  }
+}
+
 // ------------------------------------------------------------------------------ context
 struct nsrgs_ctx {
   int64_t n = 0, N = 0;
@@ -185,6 +235,9 @@ struct nsrgs_ctx {
   ncclComm_t comm = nullptr;
   bool emulated = false;   // test-only: world > 1 without a communicator (collectives are no-ops)
   bool forced_nccl = false; // test-only: world == 1 with a 1-rank NCCL communicator
+  RankGroup *group = nullptr;   // test-only: in-process rank group (nsrgs_debug_group)
+  double *group_tmp = nullptr;  // all-reduce result before it replaces the caller's buffer
+  int64_t group_cap = 0;
   unsigned long long *ts = nullptr;   // debug phase timestamps (nsrgs_debug_timestamps)
   // stats / timing
   bool timing = false;
@@ -267,13 +320,60 @@ int sync_and_check(nsrgs_ctx *c, int *flags_out = nullptr) {
   return NSRGS_OK;
 }
 
+int group_barrier(nsrgs_ctx *c) {
+  if (!c->group->barrier())
+    return set_err(c, NSRGS_ERR_NCCL, "rank group: a rank did not reach the collective within 120 s");
+  return NSRGS_OK;
+}
+
+// In-process rank group: sum of every rank's `buf` in rank order (see RankGroup).
+int group_allreduce(nsrgs_ctx *c, double *buf, size_t count) {
+  if ((int64_t)count > c->group_cap) {
+    if (c->group_tmp) cudaFree(c->group_tmp);
+    c->group_tmp = nullptr;
+    c->group_cap = 0;
+    CUDA_TRY(c, cudaMalloc(&c->group_tmp, sizeof(double) * count));
+    c->group_cap = (int64_t)count;
+  }
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  c->group->ptr[c->rank] = buf;
+  NSRGS_TRY(group_barrier(c));
+  GroupPtrs g{};
+  for (int r = 0; r < c->world; ++r) g.p[r] = static_cast<const double *>(c->group->ptr[r]);
+  const int blocks = (int)std::min<int64_t>(1024, ((int64_t)count + 255) / 256);
+  group_sum_kernel<<<blocks, 256, 0, c->stream>>>(g, c->world, (int64_t)count, c->group_tmp);
+  CUDA_TRY(c, cudaGetLastError());
+  c->kernel_launches++;
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  NSRGS_TRY(group_barrier(c));
+  CUDA_TRY(c, cudaMemcpyAsync(buf, c->group_tmp, sizeof(double) * count, cudaMemcpyDeviceToDevice, c->stream));
+  return NSRGS_OK;
+}
+
+// In-process rank group: copy every other rank's slice of its X buffer into ours.
+int group_allgather(nsrgs_ctx *c, void *buf) {
+  const size_t bytes = (size_t)c->plan.x_slice_elems * c->esz;
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  c->group->ptr[c->rank] = buf;
+  NSRGS_TRY(group_barrier(c));
+  for (int r = 0; r < c->world; ++r)
+    if (r != c->rank)
+      CUDA_TRY(c, cudaMemcpyAsync(static_cast<char *>(buf) + r * bytes, static_cast<const char *>(c->group->ptr[r]) + r * bytes,
+                                  bytes, cudaMemcpyDeviceToDevice, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return group_barrier(c);
+}
+
 int allreduce_sum(nsrgs_ctx *c, double *buf, size_t count) {
-  if ((c->world == 1 && !c->forced_nccl) || count == 0 || c->emulated) return NSRGS_OK;
+  if (count == 0) return NSRGS_OK;
+  if (c->group) return group_allreduce(c, buf, count);
+  if ((c->world == 1 && !c->forced_nccl) || c->emulated) return NSRGS_OK;
   NCCL_TRY(c, g_nccl.AllReduce(buf, buf, count, ncclFloat64, ncclSum, c->comm, c->stream));
   return NSRGS_OK;
 }
 
 int allgather_X(nsrgs_ctx *c, void *buf) {
+  if (c->group) return group_allgather(c, buf);
   if ((c->world == 1 && !c->forced_nccl) || c->emulated) return NSRGS_OK;
   const size_t cnt = (size_t)c->plan.x_slice_elems;
   char *base = static_cast<char *>(buf);
@@ -729,6 +829,12 @@ int nsrgs_destroy(nsrgs_ctx *c) {
   for (auto e : c->ev) cudaEventDestroy(e);
   for (int g = 0; g < kMaxWorld; ++g)
     if (c->peer_opened[g]) cudaIpcCloseMemHandle(c->peer_block[g]);
+  if (c->group) {
+    std::lock_guard<std::mutex> lk(g_group_mu);
+    if (--c->group->refs == 0) delete c->group;
+    c->group = nullptr;
+  }
+  if (c->group_tmp) cudaFree(c->group_tmp);
   void *bufs[] = {c->units, c->pinfo, c->ucnt, c->ctl, c->acc, c->ts, c->xblock, c->stage, c->cta_part, c->counters, c->Bpart, c->res, c->red_part, c->small,
                   c->err, c->ns_region, c->rowpart, c->colpart, c->blocks, c->sym_cnt, c->sym_part,
                   c->bsr_xs, c->bsr_part, c->bsr_cnt, c->yprev};
@@ -1125,7 +1231,8 @@ int nsrgs_init_spectral(nsrgs_ctx *c, uint64_t seed, int max_sweeps, double tol,
   // ~10-20 us of launch gap, which matters only when the A pass itself is short (A shard below
   // ~1 GB: <= 0.15 ms per pass); larger shards read it every sweep (no overshoot).
   const double a_bytes = (double)c->esz * (double)c->plan.rows_local * (double)c->N;
-  const int batch_max = a_bytes < 1e9 ? 4 : 1;
+  int batch_max = a_bytes < 1e9 ? 4 : 1;
+  if (const char *eb = std::getenv("NSRGS_INIT_BATCH")) batch_max = std::min(4, std::max(1, std::atoi(eb)));   // tests
   // Chebyshev filtering (reading R20): from the second sweep on, each sweep applies
   // the three-term recurrence T_{k+1}(A/b) = 2 (A/b) T_k - T_{k-1} that keeps [-b, b] bounded,
   // b = 2 ||A||_F / sqrt(N) (the Wigner bulk-edge bound: the noise spectrum of the instance lies
@@ -1520,9 +1627,10 @@ int nsrgs_debug_link_peers(nsrgs_ctx **ctxs, int world) {
   if (!ctxs || world < 2 || world > kMaxWorld) return NSRGS_ERR_INVALID_ARG;
   for (int r = 0; r < world; ++r) {
     nsrgs_ctx *c = ctxs[r];
-    if (!c || !c->emulated || c->world != world || c->rank != r || c->n != ctxs[0]->n || c->d != ctxs[0]->d ||
-        c->dtype != ctxs[0]->dtype || c->d > kMaxNarrowD || c->device != ctxs[0]->device)
-      return c ? set_err(c, NSRGS_ERR_INVALID_ARG, "link_peers: need emulated ranks 0..world-1 of one instance, d <= 10")
+    if (!c || !c->emulated || c->group || c->world != world || c->rank != r || c->n != ctxs[0]->n ||
+        c->d != ctxs[0]->d || c->dtype != ctxs[0]->dtype || c->d > kMaxNarrowD || c->device != ctxs[0]->device)
+      return c ? set_err(c, NSRGS_ERR_INVALID_ARG,
+                         "link_peers: need emulated, ungrouped ranks 0..world-1 of one instance, d <= 10")
                : NSRGS_ERR_INVALID_ARG;
   }
   for (int r = 0; r < world; ++r) {
@@ -1533,6 +1641,27 @@ int nsrgs_debug_link_peers(nsrgs_ctx **ctxs, int world) {
     CUDA_TRY(c, cudaMemset(xcnt_of(c->xblock, c->xstride), 0, sizeof(unsigned) * kMaxWorld));
     c->p2p = true;
     c->p2p_epoch = 0;
+  }
+  return NSRGS_OK;
+}
+
+int nsrgs_debug_group(nsrgs_ctx **ctxs, int world) {
+  if (!ctxs || world < 2 || world > kMaxWorld) return NSRGS_ERR_INVALID_ARG;
+  for (int r = 0; r < world; ++r) {
+    nsrgs_ctx *c = ctxs[r];
+    if (!c || !c->emulated || c->group || c->p2p || c->world != world || c->rank != r || c->n != ctxs[0]->n ||
+        c->d != ctxs[0]->d || c->dtype != ctxs[0]->dtype || c->device != ctxs[0]->device)
+      return c ? set_err(c, NSRGS_ERR_INVALID_ARG,
+                         "debug_group: need emulated, unlinked ranks 0..world-1 of one instance on one device")
+               : NSRGS_ERR_INVALID_ARG;
+  }
+  RankGroup *g = new RankGroup();
+  g->world = world;
+  g->refs = world;
+  for (int r = 0; r < world; ++r) {
+    NSRGS_TRY(enter(ctxs[r]));
+    NSRGS_TRY(sync_and_check(ctxs[r]));
+    ctxs[r]->group = g;
   }
   return NSRGS_OK;
 }

@@ -83,6 +83,7 @@ _SIGS = {
     "nsrgs_set_symmetric": ([_P, ct.c_int], ct.c_int),
     "nsrgs_debug_timestamps": ([_P, ct.c_int, _P], ct.c_int),
     "nsrgs_debug_link_peers": ([_P, ct.c_int], ct.c_int),
+    "nsrgs_debug_group": ([_P, ct.c_int], ct.c_int),
     "nsrgs_reset_stats": ([_P, ct.c_int], ct.c_int),
 }
 for _name, (_args, _res) in _SIGS.items():
@@ -105,6 +106,15 @@ def link_peers(solvers) -> None:
     """Test-only (NSRGS_EMULATE_RANKS=1): fused P2P exchange between rank contexts of one process."""
     arr = (_P * len(solvers))(*[s._h.value for s in solvers])
     rc = _lib.nsrgs_debug_link_peers(arr, len(solvers))
+    if rc != 0:
+        raise NSRGSError(rc, (_lib.nsrgs_last_error(solvers[0]._h) or b"").decode())
+
+
+def link_group(solvers) -> None:
+    """Test-only (NSRGS_EMULATE_RANKS=1): in-process rank group with real collectives; drive
+    each rank's calls from its own thread (see nsrgs_debug_group)."""
+    arr = (_P * len(solvers))(*[s._h.value for s in solvers])
+    rc = _lib.nsrgs_debug_group(arr, len(solvers))
     if rc != 0:
         raise NSRGSError(rc, (_lib.nsrgs_last_error(solvers[0]._h) or b"").decode())
 
