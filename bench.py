@@ -109,29 +109,63 @@ def _dist_env():
 
 
 # ------------------------------------------------------------------------------------ oracle
-def _oracle_sample(cfg, nodes_sample, budget_s):
-    """Time oracle.nsrgs.step_rows (Algorithm 2 restricted to a panel of nodes) on this host.
-    Returns (it/s scaled to the whole problem, seconds per sample pass, passes, threads)."""
-    from threadpoolctl import threadpool_info
+def _oracle_worker(cfg, node0, m, warm, passes_fixed, budget_s, barrier, q):
+    """One host process of the CPU baseline: oracle.nsrgs.step_rows (Algorithm 2 restricted to a
+    panel of m nodes, the oracle's arithmetic unchanged) on its own panel, 1 BLAS thread."""
+    from threadpoolctl import threadpool_limits
 
     from oracle import instance as inst
     from oracle import nsrgs as ons
 
-    n, d = cfg["n"], cfg["d"]
-    Z = inst.ground_truth(0, n, d)
-    nodes = np.arange(nodes_sample)
-    R = inst.measurement_rows(0, Z, cfg["sigma"], nodes)       # fp32-rounded A rows, fp64 (untimed)
-    X = Z.copy()
-    passes, t0 = 0, time.perf_counter()
-    while True:
-        ons.step_rows(R, X, nodes, 1.0 / n, cfg["K"])
-        passes += 1
-        el = time.perf_counter() - t0
-        if el >= budget_s or passes >= 10000:
-            break
-    per = el / passes
-    threads = max([p.get("num_threads", 1) for p in threadpool_info()] or [1])
-    return (nodes_sample / n) / per, per, passes, threads
+    with threadpool_limits(limits=1):
+        n, d = cfg["n"], cfg["d"]
+        Z = inst.ground_truth(0, n, d)
+        nodes = np.arange(node0, node0 + m)
+        R = inst.measurement_rows(0, Z, cfg["sigma"], nodes)   # fp32-rounded A rows, fp64 (untimed)
+        for _ in range(warm):
+            ons.step_rows(R, Z, nodes, 1.0 / n, cfg["K"])
+        barrier.wait()
+        passes, t0 = 0, time.perf_counter()
+        while True:
+            ons.step_rows(R, Z, nodes, 1.0 / n, cfg["K"])
+            passes += 1
+            el = time.perf_counter() - t0
+            if (passes_fixed and passes >= passes_fixed) or (not passes_fixed and (el >= budget_s or passes >= 100000)):
+                break
+    q.put((m, passes, el))
+
+
+def _host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def _oracle_pool(cfg, nodes_per_worker, warm=1, passes_fixed=0, budget_s=10.0, workers=None):
+    """The oracle on all host cores: one spawned process per core, each timing step_rows on its
+    own panel of nodes (the sample) after a common barrier.  Returns (it/s scaled to the whole
+    problem, workers, max seconds per pass, sample description)."""
+    import multiprocessing as mp
+
+    n = cfg["n"]
+    W = workers or max(1, min(_host_cores(), 64, n // max(1, nodes_per_worker)))
+    m = max(1, min(nodes_per_worker, n // W))
+    ctx = mp.get_context("spawn")
+    barrier, q = ctx.Barrier(W), ctx.Queue()
+    procs = [ctx.Process(target=_oracle_worker, args=(cfg, w * m, m, warm, passes_fixed, budget_s, barrier, q))
+             for w in range(W)]
+    for p in procs:
+        p.start()
+    res = [q.get() for _ in range(W)]
+    for p in procs:
+        p.join()
+    nodes_per_s = sum(mm * ps / el for mm, ps, el in res)
+    per_pass = max(el / ps for _, ps, el in res)
+    sample = (f"oracle.nsrgs.step_rows in {W} processes (1 BLAS thread each) x {m} nodes = {W * m} of {n} nodes "
+              f"({W * m * cfg['d']} of {n * cfg['d']} A rows, fp64), each on its own panel; "
+              f"it/s = (sum over processes of nodes x passes / seconds) / {n}")
+    return nodes_per_s / n, W, per_pass, sample
 
 
 def _oracle_single_thread(cfg, nodes_sample, passes=3):
@@ -155,55 +189,34 @@ def _oracle_single_thread(cfg, nodes_sample, passes=3):
 
 
 def _read_stream_gbs(torch, device, stream, gib=8, reps=5):
-    """In-run read-stream peak: best of `reps` fp32 sums over a buffer far larger
-    than L2 (torch's reduction kernel, a plain HBM read stream), CUDA events on `stream`."""
-    n = gib * (1 << 30) // 4
-    buf = torch.ones(n, dtype=torch.float32, device=device)
-    best = None
-    with torch.cuda.stream(stream):
-        buf.sum()
-        for _ in range(reps):
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            buf.sum()
-            e1.record(stream)
-            e1.synchronize()
-            ms = e0.elapsed_time(e1)
-            best = ms if best is None else min(best, ms)
+    """In-run HBM read-stream ceiling: the library's TMA read probe
+    (nsrgs_probe_read_stream: the dense pass's access pattern — one CTA per SM, 32 KB bulk
+    copies into a shared-memory ring — with the arithmetic removed) over a buffer far larger
+    than L2; best of `reps`, CUDA events on `stream`."""
+    from paper_2604_07372_b200 import nsrgs
+
+    buf = torch.ones(gib * (1 << 30) // 4, dtype=torch.float32, device=device)
+    torch.cuda.synchronize()
+    g = nsrgs.probe_read_stream(buf, stream, reps)
     del buf
     torch.cuda.empty_cache()
-    return 4.0 * n / (best / 1e3) / 1e9
+    return g
 
 
-def run_reference(args, cfg):
-    world, rank, _ = _dist_env()
+def run_reference(args, cfg, world):
+    """--impl reference: the fp64 oracle as it stands, on all host cores (process per core, each
+    on its own node panel), `warmup` untimed passes then `steps` timed passes; rank 0 only."""
+    _, rank, _ = _dist_env()
     if rank != 0:
         return
     n = cfg["n"]
-    m = max(1, min(n, args.sample_nodes))
-    from oracle import instance as inst
-    from oracle import nsrgs as ons
-    from threadpoolctl import threadpool_info
-
-    Z = inst.ground_truth(0, n, cfg["d"])
-    nodes = np.arange(m)
-    R = inst.measurement_rows(0, Z, cfg["sigma"], nodes)
-    for _ in range(args.warmup):
-        ons.step_rows(R, Z, nodes, 1.0 / n, cfg["K"])
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        ons.step_rows(R, Z, nodes, 1.0 / n, cfg["K"])
-    el = time.perf_counter() - t0
-    per = el / args.steps
-    value = (m / n) / per
-    threads = max([p.get("num_threads", 1) for p in threadpool_info()] or [1])
-    sample = (f"oracle.nsrgs.step_rows on {m} of {n} nodes ({m * cfg['d']} of {n * cfg['d']} A rows, fp64), "
-              f"one sample per step; it/s = ({m}/{n}) / seconds per sample")
+    value, W, per, sample = _oracle_pool(cfg, args.nodes_per_core, warm=max(1, args.warmup), passes_fixed=args.steps)
     line = {"metric": METRIC, "value": value, "unit": "it/s", "impl": "reference", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": per * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": _config_dict(args, cfg, world),
-            "cpu_baseline": {"value": value, "unit": "it/s", "cores": threads, "kind": "oracle", "sample": sample},
+            "cpu_baseline": {"value": value, "unit": "it/s", "cores": W, "kind": "oracle", "sample": sample,
+                             "host_cores": _host_cores(), "blas_threads_per_process": 1},
             "e2e": {"value": value, "unit": "it/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -219,6 +232,51 @@ def _config_dict(args, cfg, world):
 
 
 # ------------------------------------------------------------------------------------ GPU arm
+def _side_config(nsrgs, torch, make_solver, name, cfg, steps, warmup, barrier, stream, world, local):
+    """Whole-solve it/s and the panel pass's roofline for another BASELINE config on the same
+    GPUs (spectral init + T iterations + metrics per step, as the headline)."""
+    n, d, T, K = cfg["n"], cfg["d"], cfg["T"], cfg["K"]
+    s = make_solver(n, d)
+    Zd = torch.from_numpy(s.generate(0, cfg["sigma"])).to(f"cuda:{local}")
+
+    def solve():
+        sw = s.init_spectral(0, INIT_MAX_SWEEPS, INIT_TOL)
+        s.run(T, 1.0 / n, K, trace=True)
+        return sw, s.alignment_error(Zd)
+
+    for _ in range(warmup):
+        solve()
+    s.reset_stats(timing=True)
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        sw, met = solve()
+    e1.record(stream)
+    barrier()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    st = s.stats()
+    s.close()
+    N = n * d
+    rows_local = N // world
+    avg = st["panel_ms_total"] / max(1, st["panel_launches"])
+    bytes_launch = 4 * rows_local * N + 4 * N * d + 4 * rows_local * d
+    peak = _peaks()[0]
+    return {"config": name, "n": n, "d": d, "T": T, "K": K, "sigma": cfg["sigma"], "n_gpus": world,
+            "value": T * steps / (ms / 1e3), "unit": "it/s", "ms_per_step": ms / steps, "init_sweeps": sw,
+            "avg_pass_ms": avg, "bytes_per_launch": bytes_launch, "achieved_gbs": bytes_launch / (avg / 1e3) / 1e9,
+            "frac_of_peak": bytes_launch / (avg / 1e3) / 1e9 / peak,
+            "aggregate_gbs": world * bytes_launch / (avg / 1e3) / 1e9, "rel_err": met[0],
+            "rel_err_first_order": cfg["sigma"] * np.sqrt((d - 1) / n), "x_exchange": (
+                ("fused P2P NVLink stores from the epilogue" if st.get("p2p") else "NCCL all-gather")
+                if world > 1 else "none (1 GPU)")}
+
+
 def run_gpu(args, cfg):
     import torch
     import torch.distributed as dist
@@ -229,17 +287,22 @@ def run_gpu(args, cfg):
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        idt = torch.zeros(128, dtype=torch.uint8, device="cuda")
-        if rank == 0:
-            idt.copy_(torch.frombuffer(bytearray(nsrgs.get_nccl_unique_id()), dtype=torch.uint8))
-        dist.broadcast(idt, 0)
-        nid = bytes(idt.cpu().numpy().tobytes())
-    else:
-        nid = None
+
+    def make_solver(n_, d_):
+        """One context per (config, rank); world > 1: a fresh NCCL unique id broadcast from rank 0."""
+        nid_ = None
+        if world > 1:
+            idt = torch.zeros(128, dtype=torch.uint8, device="cuda")
+            if rank == 0:
+                idt.copy_(torch.frombuffer(bytearray(nsrgs.get_nccl_unique_id()), dtype=torch.uint8))
+            dist.broadcast(idt, 0)
+            nid_ = bytes(idt.cpu().numpy().tobytes())
+        return nsrgs.Solver(n_, d_, nsrgs.F32, rank=rank, world=world, device=local, nccl_id=nid_, stream=stream)
+
     n, d, T, K = cfg["n"], cfg["d"], cfg["T"], cfg["K"]
     eta = 1.0 / n
     stream = torch.cuda.Stream()
-    s = nsrgs.Solver(n, d, nsrgs.F32, rank=rank, world=world, device=local, nccl_id=nid, stream=stream)
+    s = make_solver(n, d)
     Zh = s.generate(0, cfg["sigma"])                     # A shard generated on the device, resident
     if args.symmetric:
         s.set_symmetric(True)
@@ -384,19 +447,30 @@ def run_gpu(args, cfg):
                        "kernel": "bsr_kernel (warp per node row: bulk-copied A chunks, gathered X_j records, "
                                  "fused epilogue)"}
         sb.close()
+    s.close()
+    # the other dense BASELINE configs on the same GPUs (driver-visible): c4 (d = 10, FMA
+    # co-limited) and the largest, c5 (160 GB; the north star's scaling config)
+    side = {}
+    for name in args.side_configs.split(",") if args.side_configs else []:
+        if name == args.config:
+            continue
+        c = CONFIGS[name]
+        if 4 * (c["n"] * c["d"]) ** 2 / world > 170e9:     # shard must fit one B200's 180 GB
+            continue
+        side[name] = _side_config(nsrgs, torch, make_solver, name, c, max(1, args.side_steps), 1, barrier,
+                                  stream, world, local)
+    read_peak = _read_stream_gbs(torch, f"cuda:{local}", stream) if not args.no_read_probe else None
     if rank != 0:
-        s.close()
+        if world > 1:
+            dist.destroy_process_group()
         return
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        v, per, passes_c, threads = _oracle_sample(cfg, args.sample_nodes, args.cpu_budget)
-        cpu = {"value": v, "unit": "it/s", "cores": threads, "kind": "oracle",
-               "sample": f"oracle.nsrgs.step_rows on {args.sample_nodes} of {n} nodes "
-                         f"({args.sample_nodes * d} of {N} A rows, fp64), {passes_c} passes in "
-                         f"{passes_c * per:.1f} s; it/s = ({args.sample_nodes}/{n}) / s_per_pass",
-               "single_thread_value": _oracle_single_thread(cfg, args.sample_nodes)}
+        v, W, per, sample = _oracle_pool(cfg, args.nodes_per_core, warm=1, budget_s=args.cpu_budget)
+        cpu = {"value": v, "unit": "it/s", "cores": W, "kind": "oracle", "sample": sample + f", {args.cpu_budget:.0f} s",
+               "host_cores": _host_cores(), "blas_threads_per_process": 1,
+               "single_thread_value": _oracle_single_thread(cfg, args.nodes_per_core)}
     traffic = _traffic(args.config)
-    read_peak = _read_stream_gbs(torch, f"cuda:{local}", stream) if not args.no_read_probe else None
     line = {
         "metric": METRIC, "value": value, "unit": "it/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
@@ -432,10 +506,31 @@ def run_gpu(args, cfg):
         line["symmetric_variant"] = sym_variant
     if bsr_variant:
         line["bsr_variant"] = bsr_variant
+    for name, v in side.items():
+        line[f"{name}_line"] = v
     print(json.dumps(line), flush=True)
-    s.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+def _launch_ranks(argv, gpus):
+    """--gpus N > 1 without a torchrun environment: start N ranks on this node (one per GPU) with
+    torch.distributed.run on 127.0.0.1, or fail with a clear message if fewer GPUs are visible."""
+    import socket
+
+    import torch
+
+    ng = torch.cuda.device_count()
+    if ng < gpus:
+        print(f"bench.py: --gpus {gpus} needs {gpus} visible GPUs on this node, found {ng}; "
+              f"nothing was timed", file=sys.stderr, flush=True)
+        sys.exit(2)
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *argv]
+    sys.exit(subprocess.call(cmd))
 
 
 def main():
@@ -443,9 +538,9 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default=None, help="c1..c5 (default: c3 at 1-4 GPUs, c5 at 8)")
+    ap.add_argument("--config", default="c3", help="c1..c5 (headline: c3 at every N, strong scaling)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--sample-nodes", type=int, default=50)
+    ap.add_argument("--nodes-per-core", type=int, default=8, help="oracle sample: nodes per host process")
     ap.add_argument("--cpu-budget", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--symmetric", action="store_true", help="symmetric half-storage pass (d <= 6, 1 GPU)")
@@ -454,16 +549,23 @@ def main():
     ap.add_argument("--sigma", type=float, default=None, help="noise level override (c2 lists 0.5, 2 and 8)")
     ap.add_argument("--bsr-p", type=float, default=0.5, help="observation probability of the block-sparse variant")
     ap.add_argument("--no-bsr-variant", action="store_true", help="skip the block-sparse (p < 1) variant")
+    ap.add_argument("--side-configs", default="c4,c5",
+                    help="other dense configs measured on the same GPUs after the headline ('' = none)")
+    ap.add_argument("--side-steps", type=int, default=2)
     args = ap.parse_args()
-    if args.config is None:
-        args.config = "c3"
     cfg = dict(CONFIGS[args.config])
     if args.sigma is not None:
         cfg["sigma"] = args.sigma
+    env_world = os.environ.get("WORLD_SIZE")
+    if env_world is not None and int(env_world) != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={env_world}", file=sys.stderr, flush=True)
+        sys.exit(2)
     if args.impl == "reference":
-        run_reference(args, cfg)
-    else:
-        run_gpu(args, cfg)
+        run_reference(args, cfg, int(env_world) if env_world else args.gpus)
+        return
+    if args.gpus > 1 and env_world is None:
+        _launch_ranks(sys.argv[1:], args.gpus)
+    run_gpu(args, cfg)
 
 
 if __name__ == "__main__":

@@ -263,6 +263,14 @@ int nsrgs_reset_stats(nsrgs_ctx *ctx, int enable_panel_timing);
  * unused slots 0); max_iters == 0 copies it to out_host (host, may be NULL) and disarms. */
 int nsrgs_debug_timestamps(nsrgs_ctx *ctx, int max_iters, unsigned long long *out_host);
 
+/* Measurement: HBM read-stream ceiling of this GPU (bench.py's roofline denominator).  Streams
+ * `bytes` (>= 32 KB; far larger than L2 for a DRAM figure) of the 16-byte-aligned DEVICE buffer
+ * buf_dev with the dense pass's access pattern (one CTA per SM, 32 KB cp.async.bulk copies into
+ * a 6-stage shared-memory ring, nothing written back), once to warm up and then `reps` times on
+ * `cuda_stream` (NULL: legacy default stream) of the current device; *best_gbs = bytes read per
+ * second of the fastest rep (1e9 B/s).  INVALID_ARG for bad arguments, CUDA / OOM on failure. */
+int nsrgs_probe_read_stream(const void *buf_dev, int64_t bytes, void *cuda_stream, int reps, double *best_gbs);
+
 /* Test-only: link `world` rank contexts created in ONE process with NSRGS_EMULATE_RANKS=1 (no
  * communicator) so that the fused P2P X exchange runs between them on one GPU: each rank's
  * epilogue stores X^{t+1} into every linked rank's buffer and bumps its arrival counters.  The

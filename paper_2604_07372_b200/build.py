@@ -15,7 +15,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 OUT = os.path.join(PKG, "libnsrgs.so")
 BUILD = os.path.join(PKG, "_build")
-SOURCES = ["panel.cu", "sym.cu", "wide.cu", "bsr.cu", "polar.cu", "aux.cu", "objective64.cu", "runtime.cu"]
+SOURCES = ["panel.cu", "sym.cu", "wide.cu", "bsr.cu", "polar.cu", "aux.cu", "objective64.cu", "probe.cu", "runtime.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "--expt-relaxed-constexpr",
          "-I" + os.path.join(ROOT, "include"), "-I" + CSRC]
@@ -35,16 +35,28 @@ def _stale(obj: str, deps) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
+def _includes(path: str, seen=None) -> set:
+    """Quoted #include files of `path`, recursively (the object's header dependencies)."""
+    seen = set() if seen is None else seen
+    with open(path) as f:
+        for line in f:
+            line = line.strip()
+            if line.startswith("#include") and '"' in line:
+                dep = os.path.normpath(os.path.join(os.path.dirname(path), line.split('"')[1]))
+                if dep not in seen and os.path.exists(dep):
+                    seen.add(dep)
+                    _includes(dep, seen)
+    return seen
+
+
 def build(verbose: bool = False, force: bool = False, ptxas_v: bool = False) -> str:
     nvcc = _nvcc()
     os.makedirs(BUILD, exist_ok=True)
-    headers = [os.path.join(CSRC, h) for h in os.listdir(CSRC) if h.endswith((".cuh", ".h"))]
-    headers.append(os.path.join(ROOT, "include", "nsrgs.h"))
     jobs = []
     for src in SOURCES:
         s = os.path.join(CSRC, src)
         o = os.path.join(BUILD, src + ".o")
-        if force or _stale(o, [s] + headers):
+        if force or _stale(o, [s] + sorted(_includes(s))):
             cmd = [nvcc, *ARCH, *FLAGS, "-c", s, "-o", o]
             if ptxas_v:
                 cmd += ["-Xptxas", "-v"]

@@ -84,6 +84,7 @@ _SIGS = {
     "nsrgs_debug_timestamps": ([_P, ct.c_int, _P], ct.c_int),
     "nsrgs_debug_link_peers": ([_P, ct.c_int], ct.c_int),
     "nsrgs_debug_group": ([_P, ct.c_int], ct.c_int),
+    "nsrgs_probe_read_stream": ([_P, ct.c_int64, _P, ct.c_int, ct.POINTER(ct.c_double)], ct.c_int),
     "nsrgs_reset_stats": ([_P, ct.c_int], ct.c_int),
 }
 for _name, (_args, _res) in _SIGS.items():
@@ -117,6 +118,16 @@ def link_group(solvers) -> None:
     rc = _lib.nsrgs_debug_group(arr, len(solvers))
     if rc != 0:
         raise NSRGSError(rc, (_lib.nsrgs_last_error(solvers[0]._h) or b"").decode())
+
+
+def probe_read_stream(buf, stream, reps: int = 5) -> float:
+    """HBM read-stream ceiling (GB/s) over the device tensor `buf` (nsrgs_probe_read_stream)."""
+    g = ct.c_double(0.0)
+    rc = _lib.nsrgs_probe_read_stream(buf.data_ptr(), buf.numel() * buf.element_size(), _P(stream.cuda_stream), reps,
+                                      ct.byref(g))
+    if rc != 0:
+        raise NSRGSError(rc, "probe_read_stream")
+    return g.value
 
 
 def plan(n: int, d: int, world: int = 1, rank: int = 0) -> dict:
