@@ -264,6 +264,9 @@ FULL = {  # BASELINE.json configs[2], configs[3] in the launch configuration ben
 
 @pytest.mark.parametrize("cfg", ["mid", "c3", "c4", "c5"])
 def test_full_size_sampled_step(nsrgs, cfg):
+    """One step at the full BASELINE sizes on 64 sampled nodes, at the same 1e-6 bar as the small
+    shapes (measured on B200: 5.4e-8 mid, 1.1e-7 c3, 1.3e-7 c4, 1.5e-7 c5; per block <= 2.3e-7;
+    tools/fullsize_err.py)."""
     n, d, sigma, K = FULL[cfg]
     s = nsrgs.Solver(n, d)
     s.generate(0, sigma, want_Z=False)
@@ -272,11 +275,64 @@ def test_full_size_sampled_step(nsrgs, cfg):
     s.set_X(X)
     s.step(1.0 / n, K)
     Xg = s.get_X()
-    nodes = np.unique(np.r_[0, n - 1, np.random.default_rng(1).integers(0, n, 14)])
+    nodes = np.unique(np.r_[0, n - 1, np.random.default_rng(1).integers(0, n, 62)])
     R = inst.measurement_rows(0, Z, sigma, nodes)
     Xo = oracle_node_step(R, X.astype(np.float64), nodes, 1.0 / n, K)
-    assert rel_fro(Xg[nodes], Xo) <= 1e-5
+    assert rel_fro(Xg[nodes], Xo) <= 1e-6
+    assert max_block_err(Xg[nodes], Xo) <= 1e-6
     s.close()
+
+
+@pytest.mark.parametrize("cfg", ["c3", "c4", "c5"])
+def test_full_size_solution_is_oracle_fixed_point(nsrgs, cfg):
+    """The bench's whole step at full size (spectral init + T = 100 iterations, cooperative
+    launch): X^T is a fixed point of the oracle's Algorithm 2 map on 64 sampled nodes — one fp64
+    oracle step from X^T moves those blocks by no more than fp32 resolution (measured <= 1.6e-7,
+    per block <= 2.6e-7) — and each block is orthogonal."""
+    n, d, sigma, K = FULL[cfg]
+    s = nsrgs.Solver(n, d)
+    Z = s.generate(0, sigma).astype(np.float64)
+    s.init_spectral(0, 100, 1e-5)
+    s.run(100, 1.0 / n, K, trace=False)
+    XT = s.get_X().astype(np.float64)
+    s.close()
+    nodes = np.unique(np.r_[0, n - 1, np.random.default_rng(2).integers(0, n, 62)])
+    R = inst.measurement_rows(0, Z, sigma, nodes)
+    Xf = oracle_node_step(R, XT, nodes, 1.0 / n, K)
+    assert rel_fro(XT[nodes], Xf) <= 1e-6
+    assert max_block_err(XT[nodes], Xf) <= 1e-6
+    assert np.max(np.abs(np.einsum("nka,nkb->nab", XT, XT) - np.eye(d))) < 1e-5
+
+
+@pytest.mark.parametrize("n,d,sigma,K", [(6000, 5, 0.3 * np.sqrt(6000) / 5, 5), (3000, 10, 0.2 * np.sqrt(3000) / 10, 6)])
+def test_shared_x0_T100_matches_oracle(nsrgs, n, d, sigma, K):
+    """North-star bar at a benchmarked shape (c3 / c4 d and sigma scaling, N = 30000, A 3.6 GB
+    fp32): from the oracle's spectral X^0, T = 100 NS-RGS iterations on the GPU (the cooperative
+    multi-iteration launch with split panels and the dynamic unit queue, as bench.py runs them)
+    against the fp64 oracle with the whole A on the host: relative Frobenius difference <= 1e-4
+    after T (north star), every block within 1e-4, objective trace within 1e-6."""
+    s = nsrgs.Solver(n, d)
+    s.generate(0, sigma, want_Z=False)
+    st = s.stats()
+    assert st["cut_panels"] > 0 and st["panels"] > st["grid"]      # split panels + queue engaged
+    Z = inst.ground_truth(0, n, d)
+    A = inst.measurement_matrix(0, Z, sigma)
+    X0, _, _ = ons.spectral_init(A, d, "subspace", Y0=inst.initial_subspace(0, n, d), tol=1e-12)
+    X0 = X0.astype(np.float32)
+    s.set_X(X0)
+    tr = s.run(100, 1.0 / n, K, trace=True)
+    XT = s.get_X()
+    s.close()
+    Xo, Fo = X0.astype(np.float64), {}
+    for t in range(100):
+        if t % 10 == 0 or t == 99:
+            Fo[t] = ons.objective_expanded(A, Xo)
+        Xo, _, _ = ons.step(A, Xo, 1.0 / n, K)
+    print(f"T=100 n={n} d={d}: rel {rel_fro(XT, Xo):.3e} max-block {max_block_err(XT, Xo):.3e}")
+    assert rel_fro(XT, Xo) <= 1e-4
+    assert max_block_err(XT, Xo) <= 1e-4
+    for t, f in Fo.items():
+        assert abs(tr[t] - f) <= 1e-6 * abs(f), (t, tr[t], f)
 
 
 @pytest.mark.parametrize("cfg", ["c3", "c5"])
@@ -513,10 +569,10 @@ def test_symmetric_full_size_sampled_and_run(nsrgs, cfg):
     s.set_X(X)
     s.step(1.0 / n, K)
     Xg = s.get_X()
-    nodes = np.unique(np.r_[0, n - 1, np.random.default_rng(1).integers(0, n, 14)])
+    nodes = np.unique(np.r_[0, n - 1, np.random.default_rng(1).integers(0, n, 62)])
     R = inst.measurement_rows(0, Z, sigma, nodes)
     Xo = oracle_node_step(R, X.astype(np.float64), nodes, 1.0 / n, K)
-    assert rel_fro(Xg[nodes], Xo) <= 1e-5
+    assert rel_fro(Xg[nodes], Xo) <= 1e-6 and max_block_err(Xg[nodes], Xo) <= 1e-6
     s.init_spectral(0, 100, 1e-5)
     tr = s.run(30, 1.0 / n, K)
     assert np.all(np.diff(tr) <= 1e-6 * tr[0])
