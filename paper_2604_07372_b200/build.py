@@ -15,7 +15,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 OUT = os.path.join(PKG, "libnsrgs.so")
 BUILD = os.path.join(PKG, "_build")
-SOURCES = ["panel.cu", "sym.cu", "wide.cu", "bsr.cu", "polar.cu", "aux.cu", "objective64.cu", "probe.cu", "runtime.cu"]
+SOURCES = ["panel.cu", "sym.cu", "wide.cu", "wide_tc.cu", "bsr.cu", "polar.cu", "aux.cu", "objective64.cu", "probe.cu", "runtime.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "--expt-relaxed-constexpr",
          "-I" + os.path.join(ROOT, "include"), "-I" + CSRC]

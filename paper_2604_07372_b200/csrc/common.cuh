@@ -55,6 +55,10 @@ struct PanelParams {
   // at exit each CTA adds its count of (panel, warp) epilogues to every rank's arrival counter
   // for this rank (peer_cnt[g] + rank) after a system-scope release; the producer reads rank
   // g's slice of X^t only once xcnt[g] >= xtarget (its acquire).  Replaces the all-gather.
+  // ---- tcgen05 wide pass (wide_tc.cu): column tiles per accumulator drain; launch epoch of the
+  // per-CTA contribution flags (ucnt[cta] == epoch: the CTA's partial rows are in Bpart[cta])
+  int drain_tiles;
+  unsigned epoch;
   int p2p;
   unsigned xtarget;
   const unsigned *xcnt;

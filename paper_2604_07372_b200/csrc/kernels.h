@@ -24,6 +24,10 @@ cudaError_t launch_p2p_wait(const unsigned *xcnt, int world, unsigned target, in
 bool wide_supported(int d);
 cudaError_t wide_dispatch(int d, int mode, bool shape_only, PanelShape *shape, const CUtensorMap *tm,
                           const PanelParams *p, int grid, cudaStream_t s, bool mma);
+// wide_tc.cu: d > 10 on tcgen05 (3xTF32, TMEM accumulators, persistent stream-K grid).
+// slot_floats: floats of one CTA's partial-row slot (Bpart = grid slots, ucnt = grid flags).
+cudaError_t wide_tc_dispatch(int d, int mode, bool shape_only, PanelShape *shape, int *slot_floats,
+                             const CUtensorMap *tm, const PanelParams *p, int grid, cudaStream_t s);
 
 // sym.cu: symmetric half-storage pass (fp32, world == 1, d in [2, 6]).
 struct SymShape {

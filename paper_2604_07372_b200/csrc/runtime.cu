@@ -167,8 +167,11 @@ struct nsrgs_ctx {
   bool own_A = false, have_A = false;
   CUtensorMap tmA;
   CUtensorMap tmA_sym;   // symmetric pass: same A, its own panel height
-  bool wide_mma = false; // d > 10: 3xTF32 tensor-core pass (default; A tensor map with the 128-byte
-                         // swizzle); NSRGS_WIDE_MMA=0 selects the CUDA-core pass
+  int wide_mma = 0;      // d > 10 pass: 2 (default) 3xTF32 on tcgen05 (wide_tc.cu), 1 3xTF32 on mma.sync,
+                         // 0 CUDA cores (NSRGS_WIDE_MMA); 1 and 2 read A through the 128-byte TMA swizzle
+  int wide_drain = 1;    // tcgen05 pass: column tiles per accumulator drain (NSRGS_WIDE_DRAIN)
+  unsigned wide_epoch = 0;
+  int wide_slot = 0;     // floats per CTA partial-row slot (tcgen05 pass)
   double a_fro2 = 0.0;
   // iterate
   void *X[2] = {nullptr, nullptr};   // both inside xblock (one IPC-shareable allocation)
@@ -300,7 +303,7 @@ int sync_and_check(nsrgs_ctx *c, int *flags_out = nullptr) {
     CUDA_TRY(c, cudaMemsetAsync(c->err, 0, sizeof(int), c->stream));
     if (flags & kErrTimeout) {   // a timed-out launch may leave the dense kernel's counters dirty
       if (c->ctl) CUDA_TRY(c, cudaMemsetAsync(c->ctl, 0, sizeof(unsigned) * 4, c->stream));
-      if (c->ucnt) CUDA_TRY(c, cudaMemsetAsync(c->ucnt, 0, sizeof(unsigned) * (size_t)c->panels * c->shape.nw, c->stream));
+      if (c->ucnt && c->d <= kMaxNarrowD) CUDA_TRY(c, cudaMemsetAsync(c->ucnt, 0, sizeof(unsigned) * (size_t)c->panels * c->shape.nw, c->stream));
       if (c->acc) CUDA_TRY(c, cudaMemsetAsync(c->acc, 0, sizeof(unsigned long long) * 2 * (size_t)c->acc_cap * c->shape.npart, c->stream));
       CUDA_TRY(c, cudaStreamSynchronize(c->stream));
     }
@@ -479,7 +482,7 @@ int build_tmap(nsrgs_ctx *c, CUtensorMap *out = nullptr, int rows = 0) {
                            (cuuint64_t)(c->lda * c->esz)};
   cuuint32_t box[3] = {(cuuint32_t)col_tile(c->d), 1u, (cuuint32_t)rows};
   cuuint32_t estr[3] = {1u, 1u, 1u};
-  const bool swz = out == &c->tmA && c->wide_mma;   // the tensor-core wide pass reads swizzled tiles
+  const bool swz = out == &c->tmA && c->wide_mma != 0;   // the tensor-core wide pass reads swizzled tiles
   CUresult r = encode(out, c->dtype == NSRGS_F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64,
                       3, c->A, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                       swz ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -573,7 +576,13 @@ int launch_panel(nsrgs_ctx *c, int mode, const void *Xin, void *Xout, double *re
     CUDA_TRY(c, sym_dispatch(c->d, mode, false, nullptr, &c->tmA_sym, &sp, c->sym_grid, c->stream));
     c->kernel_launches++;
   } else if (c->d > kMaxNarrowD) {
-    CUDA_TRY(c, wide_dispatch(c->d, mode, false, nullptr, &c->tmA, &p, c->grid, c->stream, c->wide_mma));
+    if (c->wide_mma == 2) {
+      p.drain_tiles = c->wide_drain;
+      p.epoch = ++c->wide_epoch;
+      CUDA_TRY(c, wide_tc_dispatch(c->d, mode, false, nullptr, nullptr, &c->tmA, &p, c->grid, c->stream));
+    } else {
+      CUDA_TRY(c, wide_dispatch(c->d, mode, false, nullptr, &c->tmA, &p, c->grid, c->stream, c->wide_mma == 1));
+    }
   } else {
     CUDA_TRY(c, panel_dispatch(c->dtype, c->d, mode, false, nullptr, &c->tmA, &p, c->grid, c->stream));
   }
@@ -899,9 +908,13 @@ int nsrgs_create(const nsrgs_desc *desc, nsrgs_ctx **out) {
       const char *wm = std::getenv("NSRGS_WIDE_MMA");
       // 3xTF32 tensor-core pass by default (accumulator drained per tile: ≤ 3.1e-7 per step vs
       // 8.4e-7 on CUDA cores, 1.07-1.9x faster; profiles/r01c_wide_variants.txt); =0 CUDA cores
-      c->wide_mma = c->dtype == NSRGS_F32 && !(wm && wm[0] == '0');
+      c->wide_mma = (wm && wm[0] >= '0' && wm[0] <= '2') ? wm[0] - '0' : 2;
+      if (const char *wd = std::getenv("NSRGS_WIDE_DRAIN")) c->wide_drain = std::max(1, std::atoi(wd));
     }
-    wide_dispatch(c->d, 0, true, &c->shape, nullptr, nullptr, 0, nullptr, c->wide_mma);
+    if (c->wide_mma == 2)
+      wide_tc_dispatch(c->d, 0, true, &c->shape, &c->wide_slot, nullptr, nullptr, 0, nullptr);
+    else
+      wide_dispatch(c->d, 0, true, &c->shape, nullptr, nullptr, 0, nullptr, c->wide_mma == 1);
   } else {
     panel_dispatch(c->dtype, c->d, 0, true, &c->shape, nullptr, nullptr, 0, nullptr);
   }
@@ -912,6 +925,10 @@ int nsrgs_create(const nsrgs_desc *desc, nsrgs_ctx **out) {
   std::vector<int2> pinfo;
   if (c->d <= kMaxNarrowD) build_units(c, units, pinfo);
   c->grid = c->d > kMaxNarrowD ? c->panels : std::min(c->nunits, c->sm_count);
+  if (c->d > kMaxNarrowD && c->wide_mma == 2) {   // persistent stream-K grid: >= 8 column tiles per CTA
+    const int64_t U = (int64_t)c->panels * c->total_tiles;
+    c->grid = (int)std::max<int64_t>(1, std::min<int64_t>(c->sm_count, U / 8));
+  }
   {
     int l2 = 0;
     cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, c->device);
@@ -961,6 +978,9 @@ int nsrgs_create(const nsrgs_desc *desc, nsrgs_ctx **out) {
                  cudaMemcpyAsync(c->pinfo, pinfo.data(), sizeof(int2) * pinfo.size(), cudaMemcpyHostToDevice, c->stream) == cudaSuccess &&
                  cudaStreamSynchronize(c->stream) == cudaSuccess;
   }
+  if (ok && c->d > kMaxNarrowD && c->wide_mma == 2)
+    ok = alloc((void **)&c->ucnt, sizeof(unsigned) * (size_t)c->grid) &&
+         alloc(&c->Bpart, sizeof(float) * (size_t)c->grid * (size_t)c->wide_slot);
   if (!ok) return bail(NSRGS_ERR_OOM, "device allocation failed");
   if (c->d <= kMaxNarrowD && ensure_acc(c, 1)) return bail(NSRGS_ERR_OOM);
   if (ensure_res(c, 128) || ensure_small(c, kSmallOut + 256)) return bail(NSRGS_ERR_OOM);
@@ -1686,7 +1706,7 @@ int nsrgs_get_stats(nsrgs_ctx *c, nsrgs_stats_t *o) {
   o->bsr_nnzb = c->bsr ? c->bsr_nnzb : 0;
   o->bsr_slab = (c->bsr && c->bsr_lg2g >= 0) ? 1 : 0;
   o->bsr_g4 = (c->bsr && c->bsr_g4) ? 1 : 0;
-  o->wide_tc = (c->d > kMaxNarrowD && !c->bsr && c->wide_mma) ? 1 : 0;
+  o->wide_tc = (c->d > kMaxNarrowD && !c->bsr) ? c->wide_mma : 0;
   o->p2p = c->p2p ? 1 : 0;
   return NSRGS_OK;
 }

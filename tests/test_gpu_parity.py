@@ -646,7 +646,7 @@ def test_masked_end_to_end_and_symmetric(nsrgs):
 def test_wide_generator_step_gpm(nsrgs, n, d, sigma, K):
     s = nsrgs.Solver(n, d)
     Zg = s.generate(4, sigma)
-    assert s.stats()["wide_tc"] == 1                # the default wide pass is the tensor-core one
+    assert s.stats()["wide_tc"] == 2                # the default wide pass is the tcgen05 one
     Z = inst.ground_truth(4, n, d)
     assert np.max(np.abs(Zg.astype(np.float64) - Z)) <= 2e-7
     A = inst.measurement_matrix(4, Z, sigma)
@@ -679,20 +679,21 @@ def _table1_rows():
     return [tuple(float(t) for t in l.split()) for l in open(path) if l.strip() and not l.startswith("#")]
 
 
-@pytest.mark.parametrize("variant", ["0", "1"])
+@pytest.mark.parametrize("variant", ["0", "1", "2"])
 @pytest.mark.parametrize("n,d,sigma,K", [(60, 12, 0.5, 3), (50, 25, 0.1, 1), (23, 32, 0.2, 2), (700, 25, 0.3, 1),
                                          (333, 20, 0.4, 2), (257, 16, 0.2, 1), (1500, 12, 0.3, 1)])
 def test_wide_pass_variants(nsrgs, monkeypatch, variant, n, d, sigma, K):
-    """Both wide passes (d > 10) at the fp32 bar over several tiles and ragged tails:
-    NSRGS_WIDE_MMA=1 (default) the 3xTF32 tensor-core pass — A and X split into tf32 hi + lo,
-    A X ~ A_lo X_hi + A_hi X_lo + A_hi X_hi (the dropped A_lo X_lo is ~2^-22 relative), the MMA
-    accumulator drained into a CUDA-core fp32 sum every 32-column tile so the tensor core's
-    non-round-to-nearest accumulation never runs over a long chain (undrained, the step error
-    grew linearly with N: 3.1e-5 at n 700, d 25) — and =0 the CUDA-core pass."""
+    """All wide passes (d > 10) at the fp32 bar over several tiles, ragged tails and (variant 2)
+    panels split between CTAs.  NSRGS_WIDE_MMA=2 (default): 3xTF32 on tcgen05 — the raw fp32 tile is
+    the hi part (kind::tf32 truncates), lo = x - trunc(x), A X ~ A_lo X_hi + A X_hi + A X_lo (the
+    dropped A_lo X_lo is ~2^-22 relative), TMEM accumulators, the main one drained into a
+    CUDA-core fp32 sum every 32-column tile so the tensor core's non-round-to-nearest
+    accumulation never runs over a long chain (undrained, the step error grew linearly with N:
+    3.1e-5 at n 700, d 25); =1 the same on legacy mma.sync; =0 the CUDA-core pass."""
     monkeypatch.setenv("NSRGS_WIDE_MMA", variant)
     s = nsrgs.Solver(n, d)
     s.generate(4, sigma, want_Z=False)
-    assert s.stats()["wide_tc"] == (variant == "1")
+    assert s.stats()["wide_tc"] == int(variant)
     Z = inst.ground_truth(4, n, d)
     A = inst.measurement_matrix(4, Z, sigma)
     X = oracle_iterate_near(Z, 0.1, 2).astype(np.float32)

@@ -61,7 +61,7 @@ __global__ void __launch_bounds__(128, 1) umma_probe(const float *A, const float
     *reinterpret_cast<float *>(sXlt + sw128(n, k)) = tf32_lo(v);
   }
   if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)), "n"(32));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)), "n"(64));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 0) {
@@ -92,7 +92,42 @@ __global__ void __launch_bounds__(128, 1) umma_probe(const float *A, const float
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;");
   }
-  if (variant != 2 && tid == 0) {
+  if (variant == 6) {   // A_lo row `warp*32+lane` -> TMEM lanes, columns 32..63 (A operand from TMEM)
+    uint32_t w[32];
+    const int row = warp * 32 + lane;
+    for (int j = 0; j < 32; ++j) w[j] = __float_as_uint(tf32_lo(A[row * K + j]));
+    const uint32_t ta = tmem + ((uint32_t)(warp * 32) << 16) + 32u;
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+                 "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+                 "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};"
+                 ::"r"(ta), "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7]),
+                 "r"(w[8]), "r"(w[9]), "r"(w[10]), "r"(w[11]), "r"(w[12]), "r"(w[13]), "r"(w[14]), "r"(w[15]),
+                 "r"(w[16]), "r"(w[17]), "r"(w[18]), "r"(w[19]), "r"(w[20]), "r"(w[21]), "r"(w[22]), "r"(w[23]),
+                 "r"(w[24]), "r"(w[25]), "r"(w[26]), "r"(w[27]), "r"(w[28]), "r"(w[29]), "r"(w[30]), "r"(w[31]));
+    asm volatile("tcgen05.wait::st.sync.aligned;");
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    if (tid == 0) {
+      const uint32_t idk = idesc & ~(1u << 16);
+      for (int t = 0; t < 3; ++t)
+        for (int ks = 0; ks < K / 8; ++ks) {
+          const uint64_t da = sdesc(smem_u32(sA) + ks * 32, 16, 1024);
+          const uint64_t db = sdesc(smem_u32(t == 2 ? sXlt : sXt) + ks * 32, 16, 1024);
+          const uint32_t acc = (t | ks) ? 1u : 0u;
+          if (t == 1)
+            asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                         "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}"
+                         ::"r"(tmem), "r"(tmem + 32u + (uint32_t)ks * 8u), "l"(db), "r"(idk), "r"(acc));
+          else
+            asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                         "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}"
+                         ::"r"(tmem), "l"(da), "l"(db), "r"(idk), "r"(acc));
+        }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&bar)));
+    }
+  }
+  if (variant != 2 && variant != 6 && tid == 0) {
     const int nterms = (variant == 1 || variant == 5) ? 3 : 1;
     int first = variant == 3 ? 0 : 1;
     const bool kmajor_b = variant >= 4;
@@ -138,7 +173,7 @@ __global__ void __launch_bounds__(128, 1) umma_probe(const float *A, const float
   if (tid == 33) printf("  [dev] row 33 D[33][0..1] %g %g\n", __uint_as_float(v[0]), __uint_as_float(v[1]));
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(32));
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(64));
 }
 
 static float trunc_tf32(float v) { uint32_t u; memcpy(&u, &v, 4); u &= 0xFFFFE000u; memcpy(&v, &u, 4); return v; }
@@ -158,7 +193,7 @@ int main() {
     double ex0 = 0; for (int k = 0; k < K; ++k) ex0 += (double)A[k] * X[k * N];
     printf("host D[0][0] exact %g\n", ex0);
   }
-  for (int variant = 0; variant < 6; ++variant) {
+  for (int variant = 0; variant < 7; ++variant) {
     memset(D, 0, M * N * 4);
     umma_probe<<<1, 128>>>(A, X, D, variant);
     cudaError_t e = cudaDeviceSynchronize();
@@ -178,7 +213,7 @@ int main() {
         ref = fmax(ref, fabs(ex));
       }
     printf("variant %d (%s): max|D| %.3f  max err vs exact %.3e  vs trunc-tf32 %.3e  vs rne-tf32 %.3e\n", variant,
-           variant == 0 ? "raw operands" : variant == 1 ? "3xTF32 split" : variant == 2 ? "tmem roundtrip" : variant == 3 ? "preload 7, accumulate" : variant == 4 ? "K-major B" : "K-major B, 3xTF32", ref, e_exact, e_tr, e_rn);
+           variant == 0 ? "raw operands" : variant == 1 ? "3xTF32 split" : variant == 2 ? "tmem roundtrip" : variant == 3 ? "preload 7, accumulate" : variant == 4 ? "K-major B" : variant == 5 ? "K-major B, 3xTF32" : "3xTF32, A_lo operand in TMEM", ref, e_exact, e_tr, e_rn);
   }
   return 0;
 }

@@ -14,5 +14,5 @@ if len(sys.argv) > 1:
     print(f"variant={os.environ.get('NSRGS_WIDE_MMA', '0')} d={d} n={n} pass {ms*1e3:.1f} us  {4*N*N/ms/1e6:.0f} GB/s", flush=True)
     sys.exit(0)
 for n, d in [(500, 25), (2000, 25), (4000, 25), (7000, 25), (1000, 16), (8000, 16)]:
-    for v in ("0", "1"):
+    for v in ("1", "2"):
         subprocess.run([sys.executable, __file__, str(n), str(d)], env={**os.environ, "NSRGS_WIDE_MMA": v}, timeout=300)

@@ -19,5 +19,5 @@ if len(sys.argv) > 1:
     print(f"variant={os.environ.get('NSRGS_WIDE_MMA','0')} n={n} d={d} step rel {e:.2e} obj rel {abs(f-fo)/fo:.2e}", flush=True)
     sys.exit(0)
 for n, d in [(100, 25), (300, 25), (700, 25), (1500, 25), (700, 16), (1500, 12)]:
-    for v in ("0", "1"):
+    for v in ("1", "2"):
         subprocess.run([sys.executable, __file__, str(n), str(d)], env={**os.environ, "NSRGS_WIDE_MMA": v}, timeout=300)
