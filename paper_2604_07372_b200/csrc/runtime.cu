@@ -967,7 +967,7 @@ int nsrgs_create(const nsrgs_desc *desc, nsrgs_ctx **out) {
   }
   ok = ok && alloc(&c->stage, c->esz * (size_t)(c->n * c->d * c->d)) &&
             alloc((void **)&c->cta_part, sizeof(double) * (size_t)c->grid * 2 * c->shape.npart) &&
-            alloc((void **)&c->counters, sizeof(unsigned) * 4) &&
+            alloc((void **)&c->counters, sizeof(unsigned) * 64) &&
             alloc((void **)&c->err, sizeof(int)) && alloc((void **)&c->ns_region, sizeof(unsigned));
   if (ok && c->d <= kMaxNarrowD) {
     ok = alloc((void **)&c->units, sizeof(int4) * units.size()) && alloc((void **)&c->pinfo, sizeof(int2) * pinfo.size()) &&
@@ -979,8 +979,8 @@ int nsrgs_create(const nsrgs_desc *desc, nsrgs_ctx **out) {
                  cudaStreamSynchronize(c->stream) == cudaSuccess;
   }
   if (ok && c->d > kMaxNarrowD && c->wide_mma == 2)
-    ok = alloc((void **)&c->ucnt, sizeof(unsigned) * (size_t)c->grid) &&
-         alloc(&c->Bpart, sizeof(float) * (size_t)c->grid * (size_t)c->wide_slot);
+    ok = alloc((void **)&c->ucnt, sizeof(unsigned) * 2 * (size_t)c->grid) &&   // two partial segments per CTA
+         alloc(&c->Bpart, sizeof(float) * 2 * (size_t)c->grid * (size_t)c->wide_slot);
   if (!ok) return bail(NSRGS_ERR_OOM, "device allocation failed");
   if (c->d <= kMaxNarrowD && ensure_acc(c, 1)) return bail(NSRGS_ERR_OOM);
   if (ensure_res(c, 128) || ensure_small(c, kSmallOut + 256)) return bail(NSRGS_ERR_OOM);

@@ -11,25 +11,29 @@
 //   * draining: the tensor core's fp32 accumulation does not round to nearest, so one accumulator
 //     over all N columns drifts ∝ N.  The main accumulator (hi·hi + lo·hi) is double
 //     buffered in TMEM and after every `drain` column tiles it is read back (tcgen05.ld) and added
-//     into a CUDA-core fp32 sum (round to nearest) while the MMAs fill the other buffer.  The hi·lo
-//     term is 2^-11 smaller; it has its own TMEM accumulator, read once per segment.
+//     into a CUDA-core fp32 sum (round to nearest) while the MMAs fill the other buffer.
 //
 // CTA = 10 warps: 4 split warps, 4 drain/epilogue warps, 1 TMA producer, 1 MMA issuer.
 //   producer  A tile (ROWS x 32 fp32, 128-byte swizzle, 3-D tensor map) + the X slab (32 x d) per
-//             stage into an mbarrier ring;
-//   split     A_lo of the stage straight into TMEM (thread = row: 8 conflict-free LDS.128 through
-//             the swizzle, tcgen05.st) — A_lo never touches shared memory, the MMA takes it as
-//             its TMEM A operand — and the X slab transposed into K-major swizzled X^T_hi / X^T_lo
-//             tiles (the B operands);
-//   MMA       per stage and 128-row half: 4 K-steps x {A·X_hi, A_lo·X_hi -> main; A·X_lo -> hilo},
-//             tcgen05.commit releases the stage, the X^T buffer and (per drain period) the
-//             accumulator buffer;
+//             stage into an mbarrier ring (a pure landing buffer: free again once it is read);
+//   split     thread = row: 8 conflict-free LDS.128 through the swizzle, then the row goes into
+//             TMEM twice with tcgen05.st — raw (= A_hi, the tensor core truncates) and A_lo — as
+//             the MMAs' TMEM A operands (3 operand buffers); the X slab is transposed into K-major
+//             swizzled X^T_hi / X^T_lo smem tiles (the B operands).  No MMA reads A from shared
+//             memory: measured (tools/micro/umma_rate.cu) an M 128 x N 32 x K 8 kind::tf32 MMA
+//             takes 42 cycles with A in smem (the 4 KB A read is exposed) and 17 from TMEM;
+//   MMA       per operand buffer and 128-row half: 4 K-steps x {A_lo·X_hi, A·X_lo, A·X_hi} into the
+//             half's accumulator; tcgen05.commit releases the operand buffer and (per drain
+//             period) the accumulator buffer.  Issued under elect.sync so the UTCHMMAs are straight-line;
 //   drain     tcgen05.ld of the main buffer -> fp32 sums in registers (thread = panel row); at
-//             the end of a segment the node epilogue (epilogue.cuh), 4 nodes at a time.
+//             the end of a whole panel the node epilogue (epilogue.cuh), 4 nodes at a time.
 // Work: persistent grid; the (panel, column tile) space is cut into equal contiguous ranges
 // (stream-K).  A CTA's first segment may continue a panel (contribution: partial B rows to a
 // per-CTA slot + flag) and its last may start one (head: waits for the later CTAs' slots, which
-// they produced FIRST, adds them in CTA order — deterministic — and runs the epilogue).
+// they produced FIRST).  Both kinds of partial segment go to a per-CTA slot + flag; after its
+// range every CTA sharing a split panel takes every np-th node of it, sums that node's partial
+// rows over all sharers' slots in CTA order (deterministic) and runs its epilogue — so at small n
+// (Table 1: 50 panels for 148 SMs) the epilogues are spread over all CTAs.
 #include <cuda.h>
 
 #include "common.cuh"
@@ -48,7 +52,7 @@ struct TcCfgE {
   static constexpr int A_BYTES = ROWS * CW * 4;
   static constexpr int X_BYTES = CW * D * 4;
   static constexpr int STAGE_BYTES = (A_BYTES + X_BYTES + 1023) / 1024 * 1024;
-  static constexpr int NXB = 2;                        // X^T (hi, lo) buffers
+  static constexpr int NXB = 3;                        // operand buffers: X^T (hi, lo) in smem, A (hi, lo) in TMEM
   static constexpr int XT_BYTES = NP * 128;
   static constexpr int XBUF_BYTES = 2 * XT_BYTES;
   static constexpr int DD = D * D, E = DD, DDL = (DD + 31) / 32;
@@ -60,19 +64,20 @@ struct TcCfgE {
   static constexpr int FIXED = 1024 + NXB * XBUF_BYTES + SCR + RED + BARS;
   static constexpr int BUDGET = 227 * 1024;
   static constexpr int STAGES_RAW = (BUDGET - FIXED) / STAGE_BYTES;
-  static constexpr int STAGES_CAP = 10 / MH;           // TMEM: 32 A_lo columns per (stage, half)
-  static constexpr int STAGES = STAGES_RAW > STAGES_CAP ? STAGES_CAP : STAGES_RAW;
+  static constexpr int STAGES = STAGES_RAW > 6 ? 6 : STAGES_RAW;
   static constexpr int SMEM = FIXED + STAGES * STAGE_BYTES;
   static constexpr int THREADS = 320;
-  // TMEM columns (512 allocated): main[h][b] | hilo[h] | alo[stage][h]
-  static constexpr int TM_MAIN = 0, TM_HILO = 128, TM_ALO = 192;
-  static_assert(MH * 2 * NP <= 128 && MH * NP <= 64 && TM_ALO + STAGES * MH * 32 <= 512, "TMEM map");
+  // TMEM columns (512 allocated): accumulators acc[h][b] | A operand buffers [ob][h] = (A_hi 32 | A_lo 32)
+  static constexpr int TM_MAIN = 0, TM_A = 128;
+  static_assert(MH * 2 * NP <= 128 && TM_A + NXB * MH * 64 <= 512, "TMEM map");
   // the MMA and the split warps read rows up to MROWS - 1 of a stage (rows >= ROWS are padding
   // whose products land in accumulator rows nobody reads): stay inside the stage
   static_assert(MROWS * 128 <= STAGE_BYTES, "padding rows must stay inside the stage");
 };
 template <int D, int MH>
-struct TcCfg : TcCfgE<D, MH, (TcCfgE<D, MH, 4>::STAGES_RAW >= 4 ? 4 : 2)> {};
+struct TcCfg : TcCfgE<D, MH, (TcCfgE<D, MH, 4>::STAGES_RAW >= 4 ? 4 : 2)> {
+  static_assert(TcCfgE<D, MH, (TcCfgE<D, MH, 4>::STAGES_RAW >= 4 ? 4 : 2)>::STAGES >= 3, "ring");
+};
 
 // ---- tcgen05 helpers; descriptor encodings pinned by tools/micro/umma_tf32.cu -----------------
 // shared-memory matrix descriptor: K-major, 128-byte swizzle, 8-row groups 1024 B apart
@@ -137,6 +142,36 @@ __device__ __forceinline__ void tmem_ld(uint32_t taddr, uint32_t (&v)[NP]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+// one lane of a converged warp; ptxas then emits the uniform-datapath instructions issued under
+// this predicate (UTCHMMA, UTMALDG, UBLKCP, UTCBAR) straight-line — under a `lane == 0` test it
+// wraps each of them in an ELECT loop (measured: 50 instead of 17 cycles per N = 32 MMA)
+__device__ __forceinline__ bool elect_one() {
+  uint32_t e;
+  asm volatile("{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.u32 %0, 1, 0, P;\n\t}" : "=r"(e));
+  return e != 0;
+}
+// try_wait without the long suspend hint of common.cuh's mbar_wait: the handshakes of this
+// pipeline (split -> MMA -> drain) are latency-critical
+__device__ __forceinline__ void mbar_wait_spin(uint64_t *bar, uint32_t parity) {
+  const uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAITS_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAITS_%=;\n\t}" ::"r"(addr), "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait_t(uint64_t *bar, uint32_t parity, bool timed, long long &acc) {
+  if (timed) {
+    const long long t = clock64();
+    mbar_wait_spin(bar, parity);
+    acc += clock64() - t;
+  } else {
+    mbar_wait_spin(bar, parity);
+  }
+}
+constexpr int kTcGroup = 12;   // CTAs per first-level group of the final partial-sum reduction
+
 // the CTA's contiguous range of (panel, column tile) units, walked as segments of one panel
 struct TcRange {
   int64_t u, u1;
@@ -164,24 +199,25 @@ __global__ void __launch_bounds__(TcCfg<D, MH>::THREADS, 1)
   float *scr = reinterpret_cast<float *>(xbuf + C::NXB * C::XBUF_BYTES);
   double *red = reinterpret_cast<double *>(reinterpret_cast<uint8_t *>(scr) + C::SCR);
   uint64_t *full = reinterpret_cast<uint64_t *>(reinterpret_cast<uint8_t *>(red) + C::RED);
-  uint64_t *empty = full + 10, *split_full = empty + 10, *xfree = split_full + 10;
-  uint64_t *acc_full = xfree + 2, *acc_free = acc_full + 2, *seg_free = acc_free + 2;
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(seg_free + 1);
+  uint64_t *empty = full + 10, *split_full = empty + 10, *bfree = split_full + 4;
+  uint64_t *acc_full = bfree + 4, *acc_free = acc_full + 2;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(acc_free + 2);
   int *flag = reinterpret_cast<int *>(tmem_slot + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
-      mbar_init(&split_full[s], 4);
+      mbar_init(&empty[s], 4);
+    }
+    for (int b = 0; b < C::NXB; ++b) {
+      mbar_init(&split_full[b], 4);
+      mbar_init(&bfree[b], 1);
     }
     for (int b = 0; b < 2; ++b) {
-      mbar_init(&xfree[b], 1);
       mbar_init(&acc_full[b], 1);
       mbar_init(&acc_free[b], 4);
     }
-    mbar_init(seg_free, 4);
     fence_mbar_init();
   }
   // zero the ring, the X^T tiles (component rows >= d stay zero) and the partial sums once: the
@@ -203,21 +239,24 @@ __global__ void __launch_bounds__(TcCfg<D, MH>::THREADS, 1)
   const int64_t U = (int64_t)p.panels * TT;
   TcRange rng{tc_start(U, (int)blockIdx.x, G), tc_start(U, (int)blockIdx.x + 1, G), TT};
   const int DP = p.drain_tiles > 0 ? p.drain_tiles : 1;
+  const bool timed = p.ts != nullptr;   // debug: per-role wait / busy cycles into ts[cta][slot]
   int panel, t0, t1;
 
   if (warp == 8) {   // ----------------------------------------------------------- TMA producer
-    if (lane == 0) {
+    if (elect_one()) {
       prefetch_tmap(&tmA);
       const uint64_t pol_a = p.a_keep > 0.f ? policy_keep_fraction(p.a_keep) : policy_evict_first();
       const uint64_t pol_x = policy_evict_last();
       int stage = 0;
       uint32_t phase = 0;
+      long long tw = 0;
+      const long long tb = timed ? clock64() : 0;
       while (rng.next(panel, t0, t1)) {
         for (int t = t0; t < t1; ++t) {
           const int g0 = t / tpr;
           const int g = (g0 + p.rank) % p.world, jt = t - g0 * tpr;     // own rank slice first
           const int tt = g * tpr + jt;
-          mbar_wait(&empty[stage], phase ^ 1u);
+          mbar_wait_t(&empty[stage], phase ^ 1u, timed, tw);
           uint8_t *sb = smem + stage * C::STAGE_BYTES;
           mbar_arrive_expect_tx(&full[stage], C::A_BYTES + C::X_BYTES);
           tma_load_3d(sb, &tmA, &full[stage], jt * C::CW, g, panel * C::ROWS, pol_a);
@@ -225,51 +264,53 @@ __global__ void __launch_bounds__(TcCfg<D, MH>::THREADS, 1)
           if (++stage == C::STAGES) { stage = 0; phase ^= 1u; }
         }
       }
+      if (timed) {
+        p.ts[(size_t)blockIdx.x * kTsSlots + 0] = (unsigned long long)(clock64() - tb);
+        p.ts[(size_t)blockIdx.x * kTsSlots + 1] = (unsigned long long)tw;
+      }
     }
   } else if (warp == 9) {   // ---------------------------------------------------- MMA issuer
-    if (lane == 0) {
+    if (elect_one()) {
       constexpr uint32_t idesc = umma_idesc_tf32(NP);
-      int stage = 0;
-      uint32_t phase = 0;
-      unsigned i = 0, pc = 0, sc = 0;
+      unsigned i = 0, pc = 0;
+      long long tw_in = 0, tw_acc = 0;
+      const long long tb = timed ? clock64() : 0;
       while (rng.next(panel, t0, t1)) {
-        if (sc > 0) mbar_wait(seg_free, (sc - 1u) & 1u);   // hilo of the previous segment has been read
         int b = 0;
         for (int t = t0; t < t1; ++t, ++i) {
           const int j = t - t0;
           const bool pfirst = j % DP == 0;
-          mbar_wait(&full[stage], phase);
-          mbar_wait(&split_full[stage], phase);
+          const unsigned ob = i % C::NXB;
+          mbar_wait_t(&split_full[ob], (i / C::NXB) & 1u, timed, tw_in);
           if (pfirst) {
             b = (int)(pc & 1u);
-            mbar_wait(&acc_free[b], ((pc >> 1) & 1u) ^ 1u);
+            mbar_wait_t(&acc_free[b], ((pc >> 1) & 1u) ^ 1u, timed, tw_acc);
           }
           tc_fence_after();
-          const uint32_t sa = smem_u32(smem + stage * C::STAGE_BYTES);
-          const uint32_t xh = smem_u32(xbuf + (i % C::NXB) * C::XBUF_BYTES), xl = xh + C::XT_BYTES;
+          const uint32_t xh = smem_u32(xbuf + ob * C::XBUF_BYTES), xl = xh + C::XT_BYTES;
 #pragma unroll
           for (int h = 0; h < MH; ++h) {
             const uint32_t dmain = tmem + C::TM_MAIN + (uint32_t)(h * 2 + b) * NP;
-            const uint32_t dhilo = tmem + C::TM_HILO + (uint32_t)h * NP;
-            const uint32_t alo = tmem + C::TM_ALO + (uint32_t)(stage * MH + h) * 32u;
+            const uint32_t ahi = tmem + C::TM_A + (uint32_t)(ob * MH + h) * 64u, alo = ahi + 32u;
 #pragma unroll
-            for (int ks = 0; ks < C::CW / 8; ++ks) {
-              const uint64_t da = umma_sdesc(sa + h * 16384 + ks * 32);
+            for (int ks = 0; ks < C::CW / 8; ++ks) {   // all three A operands come from TMEM
               const uint64_t dxh = umma_sdesc(xh + ks * 32), dxl = umma_sdesc(xl + ks * 32);
               umma_ts(dmain, alo + ks * 8, dxh, idesc, !(pfirst && ks == 0));
-              umma_ss(dmain, da, dxh, idesc, 1u);
-              umma_ss(dhilo, da, dxl, idesc, !(j == 0 && ks == 0));
+              umma_ts(dmain, ahi + ks * 8, dxl, idesc, 1u);
+              umma_ts(dmain, ahi + ks * 8, dxh, idesc, 1u);
             }
           }
-          umma_commit(&empty[stage]);
-          umma_commit(&xfree[i % C::NXB]);
+          umma_commit(&bfree[ob]);
           if (j % DP == DP - 1 || t == t1 - 1) {
             umma_commit(&acc_full[b]);
             ++pc;
           }
-          if (++stage == C::STAGES) { stage = 0; phase ^= 1u; }
         }
-        ++sc;
+      }
+      if (timed) {
+        p.ts[(size_t)blockIdx.x * kTsSlots + 5] = (unsigned long long)tw_in;
+        p.ts[(size_t)blockIdx.x * kTsSlots + 6] = (unsigned long long)tw_acc;
+        p.ts[(size_t)blockIdx.x * kTsSlots + 7] = (unsigned long long)(clock64() - tb);
       }
     }
   } else if (warp < 4) {   // ------------------------------------------------------ split warps
@@ -277,29 +318,35 @@ __global__ void __launch_bounds__(TcCfg<D, MH>::THREADS, 1)
     int stage = 0;
     uint32_t phase = 0;
     unsigned i = 0;
+    long long tw_full = 0, tw_x = 0;
+    const long long tb = timed ? clock64() : 0;
     while (rng.next(panel, t0, t1)) {
       for (int t = t0; t < t1; ++t, ++i) {
-        mbar_wait(&full[stage], phase);
+        const unsigned xb = i % C::NXB;
+        mbar_wait_t(&full[stage], phase, timed, tw_full);
+        mbar_wait_t(&bfree[xb], ((i / C::NXB) & 1u) ^ 1u, timed, tw_x);   // MMAs of tile i - NXB are done
+        tc_fence_after();
         const uint8_t *sb = smem + stage * C::STAGE_BYTES;
-        // A_lo row by row into TMEM (thread = row; the swizzle makes the 8 LDS.128 conflict-free)
+        // A (raw = hi) and A_lo row by row into TMEM (thread = row; the swizzle makes the 8
+        // LDS.128 conflict-free): the MMA reads both as TMEM A operands, never from smem
 #pragma unroll
         for (int h = 0; h < MH; ++h) {
           const int row = h * 128 + r;
           const uint8_t *rb = sb + row * 128;
-          uint32_t w[32];
+          uint32_t wh[32], wl[32];
 #pragma unroll
           for (int jc = 0; jc < 8; ++jc) {
             const float4 v = *reinterpret_cast<const float4 *>(rb + ((jc ^ (row & 7)) << 4));
-            w[4 * jc + 0] = __float_as_uint(tf32_lo(v.x));
-            w[4 * jc + 1] = __float_as_uint(tf32_lo(v.y));
-            w[4 * jc + 2] = __float_as_uint(tf32_lo(v.z));
-            w[4 * jc + 3] = __float_as_uint(tf32_lo(v.w));
+            wh[4 * jc + 0] = __float_as_uint(v.x); wl[4 * jc + 0] = __float_as_uint(tf32_lo(v.x));
+            wh[4 * jc + 1] = __float_as_uint(v.y); wl[4 * jc + 1] = __float_as_uint(tf32_lo(v.y));
+            wh[4 * jc + 2] = __float_as_uint(v.z); wl[4 * jc + 2] = __float_as_uint(tf32_lo(v.z));
+            wh[4 * jc + 3] = __float_as_uint(v.w); wl[4 * jc + 3] = __float_as_uint(tf32_lo(v.w));
           }
-          tmem_st32(tmem + ((uint32_t)(warp * 32) << 16) + C::TM_ALO + (uint32_t)(stage * MH + h) * 32u, w);
+          const uint32_t ta = tmem + ((uint32_t)(warp * 32) << 16) + C::TM_A + (uint32_t)(xb * MH + h) * 64u;
+          tmem_st32(ta, wh);
+          tmem_st32(ta + 32u, wl);
         }
         // X slab (32 columns x d, row-major) -> K-major swizzled X^T (raw = hi) and X^T_lo
-        const unsigned xb = i % C::NXB;
-        mbar_wait(&xfree[xb], ((i / C::NXB) & 1u) ^ 1u);
         const float *Xs = reinterpret_cast<const float *>(sb + C::A_BYTES);
         uint8_t *XH = xbuf + xb * C::XBUF_BYTES, *XL = XH + C::XT_BYTES;
         if constexpr (D & 1) {   // lane = column k: stride-d reads are conflict-free for odd d
@@ -323,18 +370,58 @@ __global__ void __launch_bounds__(TcCfg<D, MH>::THREADS, 1)
         fence_proxy_async_smem();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&split_full[stage]);
+        if (lane == 0) {
+          mbar_arrive(&split_full[xb]);
+          mbar_arrive(&empty[stage]);   // the stage is only a TMA landing buffer: free once it is read
+        }
         if (++stage == C::STAGES) { stage = 0; phase ^= 1u; }
       }
+    }
+    if (timed && threadIdx.x == 0) {
+      p.ts[(size_t)blockIdx.x * kTsSlots + 2] = (unsigned long long)tw_full;
+      p.ts[(size_t)blockIdx.x * kTsSlots + 3] = (unsigned long long)tw_x;
+      p.ts[(size_t)blockIdx.x * kTsSlots + 4] = (unsigned long long)(clock64() - tb);
     }
   } else {   // ------------------------------------------------------ drain + epilogue warps 4..7
     const int wq = warp - 4, r = wq * 32 + lane, tid = threadIdx.x - 128;
     const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
     float *Bp = static_cast<float *>(p.Bpart);
     unsigned *flags = p.ucnt;
+    constexpr int SLOT = C::MROWS * NP;
     unsigned pc = 0;
     float ns_region = 0.f;
     int err = 0;
+    int nsplit = 0, sp_panel[2] = {0, 0}, segidx = 0;
+    long long t_wait = 0, t_epi = 0;
+    const long long t_begin = timed ? clock64() : 0;
+
+    // one epilogue round: warp wq runs node `node_q` of `panel` (B_i already in its sG), then the
+    // objective / Gram partials go into the CTA's sums one warp after the other (fixed order)
+    auto epilogue_round = [&](int pnl, int node_q) {
+      const bool active = wq < C::EW && node_q >= 0 && node_q < C::NPP;
+      double g1s[C::DDL], g2s[C::DDL], so = 0.0, xs = 0.0;
+      if (active) {
+        float *sX = scr + wq * 5 * C::E, *sG = sX + C::E, *sH = sG + C::E, *sS = sH + C::E, *sM = sS + C::E;
+        const int64_t node = (int64_t)pnl * C::NPP + node_q;
+        const int nvalid = node < p.n_local ? 1 : 0;
+        node_epilogue<float, D, 1, MODE>(p, Xg, p.Xout, lane, node, nvalid, sX, sG, sH, sS, sM, g1s, g2s, so, xs,
+                                         ns_region, err);
+        so = warp_sum(so);
+        xs = warp_sum(xs);
+      }
+      for (int w = 0; w < C::EW; ++w) {
+        if (w == wq && active) {
+#pragma unroll
+          for (int m = 0; m < C::DDL; ++m) {
+            const int e2 = lane + 32 * m;
+            if (e2 < C::DD) { red[e2] += g1s[m]; red[C::DD + e2] += g2s[m]; }
+          }
+          if (lane == 0) { red[2 * C::DD] += so; red[2 * C::DD + 1] += xs; }
+        }
+        named_bar_sync(2, 128);
+      }
+    };
+
     while (rng.next(panel, t0, t1)) {
       float tot[MH][NP];
 #pragma unroll
@@ -344,7 +431,7 @@ __global__ void __launch_bounds__(TcCfg<D, MH>::THREADS, 1)
       const int nper = (t1 - t0 + DP - 1) / DP;
       for (int per = 0; per < nper; ++per, ++pc) {
         const int b = (int)(pc & 1u);
-        mbar_wait(&acc_full[b], (pc >> 1) & 1u);
+        mbar_wait_t(&acc_full[b], (pc >> 1) & 1u, timed, t_wait);
         tc_fence_after();
 #pragma unroll
         for (int h = 0; h < MH; ++h) {
@@ -353,25 +440,30 @@ __global__ void __launch_bounds__(TcCfg<D, MH>::THREADS, 1)
 #pragma unroll
           for (int k = 0; k < NP; ++k) tot[h][k] += __uint_as_float(v[k]);
         }
-        if (per == nper - 1) {
-#pragma unroll
-          for (int h = 0; h < MH; ++h) {
-            uint32_t v[NP];
-            tmem_ld<NP>(tmem + lane_base + C::TM_HILO + (uint32_t)h * NP, v);
-#pragma unroll
-            for (int k = 0; k < NP; ++k) tot[h][k] += __uint_as_float(v[k]);
-          }
-        }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) {
-          mbar_arrive(&acc_free[b]);
-          if (per == nper - 1) mbar_arrive(seg_free);
-        }
+        if (lane == 0) mbar_arrive(&acc_free[b]);
       }
-      const bool head = t0 == 0, tail = t1 == TT;
-      if (!head) {   // contribution: partial rows -> this CTA's slot ([k][row]: coalesced), then the flag
-        float *bp = Bp + (size_t)blockIdx.x * (C::MROWS * NP);
+      const long long te0 = timed ? clock64() : 0;
+      if (t0 == 0 && t1 == TT) {   // whole panel: epilogue straight from the registers, EW nodes at a time
+        for (int q0 = 0; q0 < C::NPP; q0 += C::EW) {
+#pragma unroll
+          for (int h = 0; h < MH; ++h) {
+            const int row = h * 128 + r;
+            const int q = row / D, a = row - q * D;
+            if (row < C::ROWS && q >= q0 && q < q0 + C::EW) {
+              float *g = scr + (q - q0) * 5 * C::E + C::E + a * D;
+#pragma unroll
+              for (int k = 0; k < NP; ++k)
+                if (k < D) g[k] = tot[h][k];
+            }
+          }
+          named_bar_sync(2, 128);
+          epilogue_round(panel, q0 + wq);
+        }
+      } else {   // part of a split panel: partial rows -> slot ([k][row]: coalesced), flag; epilogue deferred
+        const int si = 2 * (int)blockIdx.x + (segidx == 0 ? 0 : 1);
+        float *bp = Bp + (size_t)si * SLOT;
 #pragma unroll
         for (int h = 0; h < MH; ++h)
 #pragma unroll
@@ -379,80 +471,95 @@ __global__ void __launch_bounds__(TcCfg<D, MH>::THREADS, 1)
         named_bar_sync(2, 128);
         if (tid == 0) {
           fence_acq_rel_gpu();
-          atomicExch(flags + blockIdx.x, p.epoch);
+          atomicExch(flags + si, p.epoch);
         }
-        continue;
+        sp_panel[nsplit++] = panel;
       }
-      if (!tail) {   // head of a split panel: add the later CTAs' partial rows in CTA order
-        const int64_t last = (int64_t)(panel + 1) * TT - 1;
-        for (int cc = (int)blockIdx.x + 1; cc < G && tc_start(U, cc, G) <= last; ++cc) {
-          while (ld_acquire_gpu(flags + cc) != p.epoch) __nanosleep(64);
-          const float *bp = Bp + (size_t)cc * (C::MROWS * NP);
-#pragma unroll
-          for (int h = 0; h < MH; ++h)
-#pragma unroll
-            for (int k = 0; k < NP; ++k) tot[h][k] += __ldcg(bp + k * C::MROWS + h * 128 + r);
-        }
+      if (timed) t_epi += clock64() - te0;
+      ++segidx;
+    }
+    const long long t_stream = timed ? clock64() : 0;
+    // split panels: the CTAs sharing a panel deal its nodes round-robin; each sums the partial rows
+    // of its nodes over all sharers' slots in CTA order (deterministic) and runs their epilogues
+    for (int sidx = 0; sidx < nsplit; ++sidx) {
+      const int pnl = sp_panel[sidx];
+      const int64_t ub = (int64_t)pnl * TT, ue = ub + TT - 1;
+      int cf = (int)blockIdx.x, cl = (int)blockIdx.x;
+      while (cf > 0 && tc_start(U, cf, G) > ub) --cf;
+      while (cl + 1 < G && tc_start(U, cl + 1, G) <= ue) ++cl;
+      const int np = cl - cf + 1, pi = (int)blockIdx.x - cf;
+      for (int cc = cf; cc <= cl; ++cc) {
+        const unsigned *f = flags + 2 * cc + (tc_start(U, cc, G) >= ub ? 0 : 1);
+        while (ld_acquire_gpu(f) != p.epoch) __nanosleep(40);
       }
-      // node epilogue, EW nodes at a time (warp wq takes node q0 + wq)
-      for (int q0 = 0; q0 < C::NPP; q0 += C::EW) {
-#pragma unroll
-        for (int h = 0; h < MH; ++h) {
-          const int row = h * 128 + r;
-          const int q = row / D, a = row - q * D;
-          if (row < C::ROWS && q >= q0 && q < q0 + C::EW) {
-            float *g = scr + (q - q0) * 5 * C::E + C::E + a * D;
-#pragma unroll
-            for (int k = 0; k < NP; ++k)
-              if (k < D) g[k] = tot[h][k];
+      for (int q0 = pi; q0 < C::NPP; q0 += np * C::EW) {
+        for (int idx = tid; idx < C::EW * C::DD; idx += 128) {
+          const int w = idx / C::DD, e = idx - w * C::DD;
+          const int k = e / D, a = e - k * D;
+          const int q = q0 + w * np;
+          if (q < C::NPP) {
+            float v = 0.f;
+            for (int cc = cf; cc <= cl; ++cc) {
+              const float *bp = Bp + (size_t)(2 * cc + (tc_start(U, cc, G) >= ub ? 0 : 1)) * SLOT;
+              v += __ldcg(bp + k * C::MROWS + q * D + a);
+            }
+            scr[w * 5 * C::E + C::E + a * D + k] = v;
           }
         }
         named_bar_sync(2, 128);
-        const bool active = wq < C::EW && q0 + wq < C::NPP;
-        double g1s[C::DDL], g2s[C::DDL], so = 0.0, xs = 0.0;
-        if (active) {
-          float *sX = scr + wq * 5 * C::E, *sG = sX + C::E, *sH = sG + C::E, *sS = sH + C::E, *sM = sS + C::E;
-          const int64_t node = (int64_t)panel * C::NPP + q0 + wq;
-          const int nvalid = node < p.n_local ? 1 : 0;
-          node_epilogue<float, D, 1, MODE>(p, Xg, p.Xout, lane, node, nvalid, sX, sG, sH, sS, sM, g1s, g2s, so, xs,
-                                           ns_region, err);
-          so = warp_sum(so);
-          xs = warp_sum(xs);
-        }
-        // objective / Gram partials into the CTA's sums, one warp after the other (fixed order)
-        for (int w = 0; w < C::EW; ++w) {
-          if (w == wq && active) {
-#pragma unroll
-            for (int m = 0; m < C::DDL; ++m) {
-              const int e2 = lane + 32 * m;
-              if (e2 < C::DD) { red[e2] += g1s[m]; red[C::DD + e2] += g2s[m]; }
-            }
-            if (lane == 0) { red[2 * C::DD] += so; red[2 * C::DD + 1] += xs; }
-          }
-          named_bar_sync(2, 128);
-        }
+        epilogue_round(pnl, q0 + wq * np);
       }
     }
+    const long long t_shared = timed ? clock64() : 0;
     if (err) atomicOr(p.err, err);
     if (lane == 0 && ns_region > 0.f) atomicMax(p.ns_region, __float_as_uint(ns_region));
-    // per-CTA partials -> slot; the last CTA reduces all slots in order
+    // per-CTA partials -> slot; two-level fixed-order reduction: the last CTA of each group of
+    // kTcGroup sums its group's slots, the last group to finish sums the group sums
+    double *grp = p.cta_part + (int64_t)G * C::NPART;
+    const int gi = (int)blockIdx.x / kTcGroup, ngrp = (G + kTcGroup - 1) / kTcGroup;
+    const int gfirst = gi * kTcGroup, gsize = min(kTcGroup, G - gfirst);
     for (int i = tid; i < C::NPART; i += 128) __stcg(p.cta_part + (int64_t)blockIdx.x * C::NPART + i, red[i]);
     named_bar_sync(2, 128);
     if (tid == 0) {
       fence_acq_rel_gpu();
-      const int is_last = (atomicAdd(p.done_cnt, 1u) == gridDim.x - 1);
+      const int is_last = (atomicAdd(p.done_cnt + 1 + gi, 1u) == (unsigned)gsize - 1u);
       if (is_last) fence_acq_rel_gpu();
       *flag = is_last;
     }
     named_bar_sync(2, 128);
     if (*flag) {
-      for (int i = wq; i < C::NPART; i += 4) {
+      for (int i = tid; i < C::NPART; i += 128) {
         double v = 0.0;
-        for (int b = lane; b < (int)gridDim.x; b += 32) v += __ldcg(p.cta_part + (int64_t)b * C::NPART + i);
-        v = warp_sum(v);
-        if (lane == 0) p.result[i] = v;
+#pragma unroll
+        for (int b = 0; b < kTcGroup; ++b)
+          if (b < gsize) v += __ldcg(p.cta_part + (int64_t)(gfirst + b) * C::NPART + i);
+        __stcg(grp + (int64_t)gi * C::NPART + i, v);
       }
-      if (tid == 0) *p.done_cnt = 0u;
+      named_bar_sync(2, 128);
+      if (tid == 0) {
+        p.done_cnt[1 + gi] = 0u;
+        fence_acq_rel_gpu();
+        const int is_last = (atomicAdd(p.done_cnt, 1u) == (unsigned)ngrp - 1u);
+        if (is_last) fence_acq_rel_gpu();
+        *flag = is_last;
+      }
+      named_bar_sync(2, 128);
+      if (*flag) {
+        for (int i = tid; i < C::NPART; i += 128) {
+          double v = 0.0;
+          for (int g = 0; g < ngrp; ++g) v += __ldcg(grp + (int64_t)g * C::NPART + i);
+          p.result[i] = v;
+        }
+        if (tid == 0) *p.done_cnt = 0u;
+      }
+    }
+    if (timed && tid == 0) {
+      unsigned long long *ts = p.ts + (size_t)blockIdx.x * kTsSlots;
+      ts[8] = (unsigned long long)t_wait;
+      ts[9] = (unsigned long long)(t_stream - t_begin);
+      ts[10] = (unsigned long long)t_epi;
+      ts[11] = (unsigned long long)(t_shared - t_stream);
+      ts[12] = (unsigned long long)(clock64() - t_shared);
     }
   }
   tc_fence_before();

@@ -9,7 +9,7 @@ from paper_2604_07372_b200 import nsrgs
 cfg = sys.argv[1] if len(sys.argv) > 1 else "c3"
 sym = "sym" in sys.argv[2:]   # symmetric half-storage pass (sym_block_kernel + sym_final_kernel)
 n, d, c, K = {"c2": (2000, 3, None, 5), "c3": (20000, 5, 0.3, 5), "c4": (12000, 10, 0.2, 6),
-              "w25": (4000, 25, 0.2, 1)}[cfg]   # w25: wide pass (-k regex:wide_kernel)
+              "w25": (4000, 25, 0.2, 1), "w500": (500, 25, 0.2, 1), "w16": (8000, 16, 0.2, 1)}[cfg]   # w25: wide pass (-k regex:wide_kernel)
 s = nsrgs.Solver(n, d)
 s.generate(0, 0.5 if c is None else c * np.sqrt(n) / d, want_Z=False)
 rng = np.random.default_rng(0)
