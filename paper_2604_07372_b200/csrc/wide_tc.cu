@@ -13,7 +13,9 @@
 //     buffered in TMEM and after every `drain` column tiles it is read back (tcgen05.ld) and added
 //     into a CUDA-core fp32 sum (round to nearest) while the MMAs fill the other buffer.
 //
-// CTA = 10 warps: 4 split warps, 4 drain/epilogue warps, 1 TMA producer, 1 MMA issuer.
+// CTA = 16 warps in 4 warpgroups, registers re-dealt with setmaxnreg (104 / 104 / 232 / 72): two
+// split warpgroups (alternate tiles), one drain/epilogue warpgroup, and a control group (TMA
+// producer warp, MMA issuer warp, 2 idle warps).
 //   producer  A tile (ROWS x 32 fp32, 128-byte swizzle, 3-D tensor map) + the X slab (32 x d) per
 //             stage into an mbarrier ring (a pure landing buffer: free again once it is read);
 //   split     thread = row: 8 conflict-free LDS.128 through the swizzle, then the row goes into
@@ -66,7 +68,11 @@ struct TcCfgE {
   static constexpr int STAGES_RAW = (BUDGET - FIXED) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_RAW > 6 ? 6 : STAGES_RAW;
   static constexpr int SMEM = FIXED + STAGES * STAGE_BYTES;
-  static constexpr int THREADS = 320;
+  // 16 warps: split WG 0 (warps 0-3), split WG 1 (4-7), drain/epilogue WG (8-11), producer (12),
+  // MMA issuer (13), 2 idle; launched at 128 registers, re-dealt with setmaxnreg
+  static constexpr int THREADS = 512;
+  static constexpr int REG_SPLIT = 104, REG_DRAIN = 232, REG_CTRL = 72;
+  static_assert(2 * REG_SPLIT + REG_DRAIN + REG_CTRL <= 512, "register file: 4 warpgroups x 128 threads");
   // TMEM columns (512 allocated): accumulators acc[h][b] | A operand buffers [ob][h] = (A_hi 32 | A_lo 32)
   static constexpr int TM_MAIN = 0, TM_A = 128;
   static_assert(MH * 2 * NP <= 128 && TM_A + NXB * MH * 64 <= 512, "TMEM map");
@@ -108,6 +114,15 @@ __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::
 __device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ float tf32_lo(float x) {   // x - trunc_tf32(x): exact
   return x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+}
+template <int R> __device__ __forceinline__ void reg_dec() { asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(R)); }
+template <int R> __device__ __forceinline__ void reg_inc() { asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(R)); }
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&w)[16]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+               "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"
+               ::"r"(taddr), "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7]),
+               "r"(w[8]), "r"(w[9]), "r"(w[10]), "r"(w[11]), "r"(w[12]), "r"(w[13]), "r"(w[14]), "r"(w[15])
+               : "memory");
 }
 __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&w)[32]) {
   asm volatile("tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
@@ -226,7 +241,7 @@ __global__ void __launch_bounds__(TcCfg<D, MH>::THREADS, 1)
     reinterpret_cast<float4 *>(smem)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
   for (int i = threadIdx.x; i < C::NPART; i += C::THREADS) red[i] = 0.0;
   fence_proxy_async_smem();
-  if (warp == 9) {
+  if (warp == 13) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)) : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
@@ -242,7 +257,9 @@ __global__ void __launch_bounds__(TcCfg<D, MH>::THREADS, 1)
   const bool timed = p.ts != nullptr;   // debug: per-role wait / busy cycles into ts[cta][slot]
   int panel, t0, t1;
 
-  if (warp == 8) {   // ----------------------------------------------------------- TMA producer
+  if (warp >= 12) {   // ---------------------------------- control warpgroup: producer, MMA issuer, 2 idle
+    reg_dec<C::REG_CTRL>();
+  if (warp == 12) {   // ---------------------------------------------------------- TMA producer
     if (elect_one()) {
       prefetch_tmap(&tmA);
       const uint64_t pol_a = p.a_keep > 0.f ? policy_keep_fraction(p.a_keep) : policy_evict_first();
@@ -269,7 +286,7 @@ __global__ void __launch_bounds__(TcCfg<D, MH>::THREADS, 1)
         p.ts[(size_t)blockIdx.x * kTsSlots + 1] = (unsigned long long)tw;
       }
     }
-  } else if (warp == 9) {   // ---------------------------------------------------- MMA issuer
+  } else if (warp == 13) {   // --------------------------------------------------- MMA issuer
     if (elect_one()) {
       constexpr uint32_t idesc = umma_idesc_tf32(NP);
       unsigned i = 0, pc = 0;
@@ -313,16 +330,19 @@ __global__ void __launch_bounds__(TcCfg<D, MH>::THREADS, 1)
         p.ts[(size_t)blockIdx.x * kTsSlots + 7] = (unsigned long long)(clock64() - tb);
       }
     }
-  } else if (warp < 4) {   // ------------------------------------------------------ split warps
-    const int r = warp * 32 + lane;
-    int stage = 0;
-    uint32_t phase = 0;
+  }
+  } else if (warp < 8) {   // ------------------- split warps: warpgroup g takes the tiles i = g (mod 2)
+    reg_dec<C::REG_SPLIT>();
+    const int wg = warp >> 2, wq = warp & 3, r = wq * 32 + lane;
     unsigned i = 0;
     long long tw_full = 0, tw_x = 0;
     const long long tb = timed ? clock64() : 0;
     while (rng.next(panel, t0, t1)) {
       for (int t = t0; t < t1; ++t, ++i) {
+        if ((int)(i & 1u) != wg) continue;
         const unsigned xb = i % C::NXB;
+        const int stage = (int)(i % C::STAGES);
+        const uint32_t phase = (i / C::STAGES) & 1u;
         mbar_wait_t(&full[stage], phase, timed, tw_full);
         mbar_wait_t(&bfree[xb], ((i / C::NXB) & 1u) ^ 1u, timed, tw_x);   // MMAs of tile i - NXB are done
         tc_fence_after();
@@ -333,31 +353,35 @@ __global__ void __launch_bounds__(TcCfg<D, MH>::THREADS, 1)
         for (int h = 0; h < MH; ++h) {
           const int row = h * 128 + r;
           const uint8_t *rb = sb + row * 128;
-          uint32_t wh[32], wl[32];
+          const uint32_t ta = tmem + ((uint32_t)(wq * 32) << 16) + C::TM_A + (uint32_t)(xb * MH + h) * 64u;
 #pragma unroll
-          for (int jc = 0; jc < 8; ++jc) {
-            const float4 v = *reinterpret_cast<const float4 *>(rb + ((jc ^ (row & 7)) << 4));
-            wh[4 * jc + 0] = __float_as_uint(v.x); wl[4 * jc + 0] = __float_as_uint(tf32_lo(v.x));
-            wh[4 * jc + 1] = __float_as_uint(v.y); wl[4 * jc + 1] = __float_as_uint(tf32_lo(v.y));
-            wh[4 * jc + 2] = __float_as_uint(v.z); wl[4 * jc + 2] = __float_as_uint(tf32_lo(v.z));
-            wh[4 * jc + 3] = __float_as_uint(v.w); wl[4 * jc + 3] = __float_as_uint(tf32_lo(v.w));
+          for (int c16 = 0; c16 < 2; ++c16) {   // 16 columns at a time: 32 live data registers
+            uint32_t wh[16], wl[16];
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj) {
+              const int jc = c16 * 4 + jj;
+              const float4 v = *reinterpret_cast<const float4 *>(rb + ((jc ^ (row & 7)) << 4));
+              wh[4 * jj + 0] = __float_as_uint(v.x); wl[4 * jj + 0] = __float_as_uint(tf32_lo(v.x));
+              wh[4 * jj + 1] = __float_as_uint(v.y); wl[4 * jj + 1] = __float_as_uint(tf32_lo(v.y));
+              wh[4 * jj + 2] = __float_as_uint(v.z); wl[4 * jj + 2] = __float_as_uint(tf32_lo(v.z));
+              wh[4 * jj + 3] = __float_as_uint(v.w); wl[4 * jj + 3] = __float_as_uint(tf32_lo(v.w));
+            }
+            tmem_st16(ta + 16u * c16, wh);
+            tmem_st16(ta + 32u + 16u * c16, wl);
           }
-          const uint32_t ta = tmem + ((uint32_t)(warp * 32) << 16) + C::TM_A + (uint32_t)(xb * MH + h) * 64u;
-          tmem_st32(ta, wh);
-          tmem_st32(ta + 32u, wl);
         }
         // X slab (32 columns x d, row-major) -> K-major swizzled X^T (raw = hi) and X^T_lo
         const float *Xs = reinterpret_cast<const float *>(sb + C::A_BYTES);
         uint8_t *XH = xbuf + xb * C::XBUF_BYTES, *XL = XH + C::XT_BYTES;
         if constexpr (D & 1) {   // lane = column k: stride-d reads are conflict-free for odd d
-          for (int n = warp; n < D; n += 4) {
+          for (int n = wq; n < D; n += 4) {
             const float x = Xs[lane * D + n];
             const uint32_t off = (uint32_t)n * 128u + ((uint32_t)((lane >> 2) ^ (n & 7)) << 4) + (uint32_t)(lane & 3) * 4u;
             *reinterpret_cast<float *>(XH + off) = x;
             *reinterpret_cast<float *>(XL + off) = tf32_lo(x);
           }
         } else {                 // lane = component n: contiguous reads, 4-way conflicting stores
-          for (int k = warp; k < C::CW; k += 4) {
+          for (int k = wq; k < C::CW; k += 4) {
             if (lane < D) {
               const float x = Xs[k * D + lane];
               const uint32_t off = (uint32_t)lane * 128u + ((uint32_t)((k >> 2) ^ (lane & 7)) << 4) + (uint32_t)(k & 3) * 4u;
@@ -374,7 +398,6 @@ __global__ void __launch_bounds__(TcCfg<D, MH>::THREADS, 1)
           mbar_arrive(&split_full[xb]);
           mbar_arrive(&empty[stage]);   // the stage is only a TMA landing buffer: free once it is read
         }
-        if (++stage == C::STAGES) { stage = 0; phase ^= 1u; }
       }
     }
     if (timed && threadIdx.x == 0) {
@@ -382,8 +405,9 @@ __global__ void __launch_bounds__(TcCfg<D, MH>::THREADS, 1)
       p.ts[(size_t)blockIdx.x * kTsSlots + 3] = (unsigned long long)tw_x;
       p.ts[(size_t)blockIdx.x * kTsSlots + 4] = (unsigned long long)(clock64() - tb);
     }
-  } else {   // ------------------------------------------------------ drain + epilogue warps 4..7
-    const int wq = warp - 4, r = wq * 32 + lane, tid = threadIdx.x - 128;
+  } else {   // ----------------------------------------------------- drain + epilogue warps 8..11
+    reg_inc<C::REG_DRAIN>();
+    const int wq = warp - 8, r = wq * 32 + lane, tid = threadIdx.x - 256;
     const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
     float *Bp = static_cast<float *>(p.Bpart);
     unsigned *flags = p.ucnt;
@@ -565,7 +589,7 @@ __global__ void __launch_bounds__(TcCfg<D, MH>::THREADS, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == 9) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+  if (warp == 13) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
 }
 
 template <int D, int MODE, int MH>
