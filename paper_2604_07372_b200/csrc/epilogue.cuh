@@ -138,7 +138,12 @@ __device__ __forceinline__ void node_epilogue(const PanelParams &p, const T *Xg,
       // GPM (comparison method): X_i <- sgn(B_i), B_i = sum_{j!=i} A_ij X_j, by
       // Newton-Schulz from S_0 = B_i / ||B_i||_F (singular values in (0, 1]) to convergence.
       T *inv = sM + E - NPW;   // scratch: per-node scale (sM is rewritten below)
-      if (lane < NPW) {
+      if constexpr (NPW == 1) {   // one node per warp (wide blocks): the d^2 sum over the lanes
+        T f2 = T(0);
+        for (int e2 = lane; e2 < DD; e2 += 32) f2 += sG[e2] * sG[e2];
+        f2 = warp_sum(f2);
+        if (lane == 0) inv[0] = f2 > T(0) ? T(1) / sqrt(f2) : T(0);
+      } else if (lane < NPW) {
         T f2 = T(0);
         for (int e2 = 0; e2 < DD; ++e2) f2 += sG[lane * DD + e2] * sG[lane * DD + e2];
         inv[lane] = f2 > T(0) ? T(1) / sqrt(f2) : T(0);
@@ -168,7 +173,15 @@ __device__ __forceinline__ void node_epilogue(const PanelParams &p, const T *Xg,
         }
         __syncwarp();
         bool ok = true;
-        if (lane < nvalid) {
+        if constexpr (NPW == 1) {
+          T dev = T(0);
+          for (int e2 = lane; e2 < DD; e2 += 32) {
+            const T dv = (e2 / D == e2 % D ? T(1) : T(0)) - sM[e2];
+            dev += dv * dv;
+          }
+          dev = warp_sum(dev);
+          ok = nvalid == 0 || sqrt(dev) <= tol;
+        } else if (lane < nvalid) {
           T dev = T(0);
           for (int e2 = 0; e2 < DD; ++e2) {
             const T dv = (e2 / D == e2 % D ? T(1) : T(0)) - sM[lane * DD + e2];
@@ -255,7 +268,17 @@ __device__ __forceinline__ void node_epilogue(const PanelParams &p, const T *Xg,
         }
       }
       __syncwarp();
-      if (it == 0 && lane < nvalid) {   // ||I - F^T F||_F of node `lane` (PAPER.md:465 eq:conclusion:sigma)
+      if constexpr (NPW == 1) {   // ||I - F^T F||_F of the warp's node (PAPER.md:465 eq:conclusion:sigma)
+        if (it == 0) {
+          float acc2 = 0.f;
+          for (int e2 = lane; e2 < DD; e2 += 32) {
+            const float dv = (float)((e2 / D == e2 % D ? T(1) : T(0)) - sM[e2]);
+            acc2 += dv * dv;
+          }
+          acc2 = warp_sum(acc2);
+          if (lane < nvalid) ns_region = fmaxf(ns_region, sqrtf(acc2));
+        }
+      } else if (it == 0 && lane < nvalid) {   // ... of node `lane`
         const T *Mq = sM + lane * DD;
         float acc2 = 0.f;
         for (int e2 = 0; e2 < DD; ++e2) {
@@ -288,7 +311,12 @@ __device__ __forceinline__ void node_epilogue(const PanelParams &p, const T *Xg,
     }
     }  // MODE == kModeRgs
     // divergence guard: non-finite or ||S||_F > 10 sqrt(d)
-    if (lane < nvalid) {
+    if constexpr (NPW == 1) {
+      float f2 = 0.f;   // a threshold test at ||S||_F^2 = 100 d: fp32 lane sums suffice (NaN / Inf propagate)
+      for (int e2 = lane; e2 < DD; e2 += 32) f2 += (float)sS[e2] * (float)sS[e2];
+      f2 = warp_sum(f2);
+      if (nvalid > 0 && !(f2 <= 100.f * D)) err |= kErrDivergence;
+    } else if (lane < nvalid) {
       const T *Sq = sS + lane * DD;
       double f2 = 0.0;
       for (int e2 = 0; e2 < DD; ++e2) f2 += (double)Sq[e2] * (double)Sq[e2];

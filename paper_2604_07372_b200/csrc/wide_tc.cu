@@ -517,18 +517,30 @@ __global__ void __launch_bounds__(TcCfg<D, MH>::THREADS, 1)
         while (ld_acquire_gpu(f) != p.epoch) __nanosleep(40);
       }
       for (int q0 = pi; q0 < C::NPP; q0 += np * C::EW) {
-        for (int idx = tid; idx < C::EW * C::DD; idx += 128) {
+        constexpr int GPT = (C::EW * C::DD + 127) / 128;   // gathered entries per thread
+        float v[GPT];
+        int off[GPT];
+#pragma unroll
+        for (int u = 0; u < GPT; ++u) {
+          const int idx = tid + 128 * u;
           const int w = idx / C::DD, e = idx - w * C::DD;
           const int k = e / D, a = e - k * D;
           const int q = q0 + w * np;
-          if (q < C::NPP) {
-            float v = 0.f;
-            for (int cc = cf; cc <= cl; ++cc) {
-              const float *bp = Bp + (size_t)(2 * cc + (tc_start(U, cc, G) >= ub ? 0 : 1)) * SLOT;
-              v += __ldcg(bp + k * C::MROWS + q * D + a);
-            }
-            scr[w * 5 * C::E + C::E + a * D + k] = v;
-          }
+          v[u] = 0.f;
+          off[u] = (idx < C::EW * C::DD && q < C::NPP) ? k * C::MROWS + q * D + a : -1;
+        }
+        for (int cc = cf; cc <= cl; ++cc) {   // sharers in CTA order: the fixed summation order
+          const float *bp = Bp + (size_t)(2 * cc + (tc_start(U, cc, G) >= ub ? 0 : 1)) * SLOT;
+#pragma unroll
+          for (int u = 0; u < GPT; ++u)
+            if (off[u] >= 0) v[u] += __ldcg(bp + off[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < GPT; ++u) {
+          const int idx = tid + 128 * u;
+          const int w = idx / C::DD, e = idx - w * C::DD;
+          const int k = e / D, a = e - k * D;
+          if (off[u] >= 0) scr[w * 5 * C::E + C::E + a * D + k] = v[u];
         }
         named_bar_sync(2, 128);
         epilogue_round(pnl, q0 + wq * np);
