@@ -34,6 +34,9 @@ CONFIGS = {  # BASELINE.json "configs" (seed 0 everywhere, eta = 1/n)
     "c4": dict(n=12000, d=10, sigma=0.2 * np.sqrt(12000) / 10, T=100, K=6),
     "c5": dict(n=40000, d=5, sigma=0.3 * np.sqrt(40000) / 5, T=100, K=5),
 }
+# Not a BASELINE config: the paper's block size d = 25 (Table 1 :336-363) at a size that
+# streams 40 GB, with the paper's protocol T_s = 1 (K = 1) — the tcgen05 wide pass
+SIDE_CONFIGS = {"w25": dict(n=4000, d=25, sigma=0.2, T=50, K=1)}
 METRIC = "NS-RGS iterations/sec and effective HBM GB/s (% of roofline) at 1/2/4/8 B200"
 INIT_TOL, INIT_MAX_SWEEPS = 1e-5, 100
 
@@ -272,7 +275,10 @@ def _side_config(nsrgs, torch, make_solver, name, cfg, steps, warmup, barrier, s
             "avg_pass_ms": avg, "bytes_per_launch": bytes_launch, "achieved_gbs": bytes_launch / (avg / 1e3) / 1e9,
             "frac_of_peak": bytes_launch / (avg / 1e3) / 1e9 / peak,
             "aggregate_gbs": world * bytes_launch / (avg / 1e3) / 1e9, "rel_err": met[0],
-            "rel_err_first_order": cfg["sigma"] * np.sqrt((d - 1) / n), "x_exchange": (
+            "rel_err_first_order": cfg["sigma"] * np.sqrt((d - 1) / n),
+            "kernel": ("wide_tc_kernel (tcgen05 kind::tf32 3xTF32, TMEM operands + accumulators)" if st.get("wide_tc") == 2
+                       else "wide_kernel" if d > 10 else "panel_kernel (fused A.X + epilogue)"),
+            "x_exchange": (
                 ("fused P2P NVLink stores from the epilogue" if st.get("p2p") else "NCCL all-gather")
                 if world > 1 else "none (1 GPU)")}
 
@@ -454,8 +460,8 @@ def run_gpu(args, cfg):
     for name in args.side_configs.split(",") if args.side_configs else []:
         if name == args.config:
             continue
-        c = CONFIGS[name]
-        if 4 * (c["n"] * c["d"]) ** 2 / world > 170e9:     # shard must fit one B200's 180 GB
+        c = CONFIGS.get(name) or SIDE_CONFIGS[name]
+        if c["n"] % world or 4 * (c["n"] * c["d"]) ** 2 / world > 170e9:     # shard must fit one B200's 180 GB
             continue
         side[name] = _side_config(nsrgs, torch, make_solver, name, c, max(1, args.side_steps), 1, barrier,
                                   stream, world, local)
@@ -549,7 +555,7 @@ def main():
     ap.add_argument("--sigma", type=float, default=None, help="noise level override (c2 lists 0.5, 2 and 8)")
     ap.add_argument("--bsr-p", type=float, default=0.5, help="observation probability of the block-sparse variant")
     ap.add_argument("--no-bsr-variant", action="store_true", help="skip the block-sparse (p < 1) variant")
-    ap.add_argument("--side-configs", default="c4,c5",
+    ap.add_argument("--side-configs", default="c4,c5,w25",
                     help="other dense configs measured on the same GPUs after the headline ('' = none)")
     ap.add_argument("--side-steps", type=int, default=2)
     args = ap.parse_args()

@@ -613,8 +613,12 @@ static cudaError_t tc_launch(const CUtensorMap *tm, const PanelParams &p, int gr
     const cudaError_t e = set_smem_attr_once(reinterpret_cast<const void *>(kern), C::SMEM, attr);
     if (e != cudaSuccess) return e;
   }
-  kern<<<grid, C::THREADS, C::SMEM, s>>>(*tm, p);
-  return cudaGetLastError();
+  // CTAs sharing a split panel wait for each other's partial rows, so the whole grid (<= one CTA
+  // per SM) must be co-resident: a cooperative launch guarantees it (or waits / fails, never hangs)
+  CUtensorMap tmv = *tm;
+  PanelParams pv = p;
+  void *args[] = {&tmv, &pv};
+  return cudaLaunchCooperativeKernel(reinterpret_cast<const void *>(kern), dim3(grid), dim3(C::THREADS), args, C::SMEM, s);
 }
 
 template <int D, int MH>

@@ -33,6 +33,12 @@ def summary(path):
             elif u in SCALE:
                 v *= SCALE[u]
             out[name] = v
+    for i, k in enumerate(hdr):   # tensor-pipe and TMEM counters, whatever this ncu names them
+        if ("tensor" in k or "tmem" in k) and "pct" in k:
+            try:
+                out[k] = float(vals[i].replace(",", ""))
+            except ValueError:
+                pass
     if "dram_bytes_read" in out and "duration_ms" in out:
         out["dram_tbs"] = (out["dram_bytes_read"] + out.get("dram_bytes_write", 0.0)) / (out["duration_ms"] * 1e-3) / 1e12
     return out

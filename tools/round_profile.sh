@@ -17,12 +17,15 @@ cap() {   # cap <tag> <kernel regex> <skip> <command...>
   ncu -i $O/prof_${R}_$tag.ncu-rep --page raw --csv > $O/${R}_${tag}_full_raw.csv 2>/dev/null
   ncu -i $O/prof_${R}_$tag.ncu-rep --page details --csv > $O/${R}_${tag}_details.csv 2>/dev/null
   ncu -i $O/prof_${R}_$tag.ncu-rep --page source --csv --print-source sass > $O/${R}_${tag}_source.csv 2>/dev/null
+  gzip -f $O/${R}_${tag}_source.csv
   python tools/ncu_summary.py $tag=$O/prof_${R}_$tag.ncu-rep > $O/${R}_${tag}_summary.json 2>&1
   rm -f $O/prof_${R}_$tag.ncu-rep
 }
 cap c3 panel_kernel 3 python tools/prof_target.py c3
 cap c4 panel_kernel 3 python tools/prof_target.py c4
 cap c3sym sym_block 3 python tools/prof_target.py c3 sym
+cap w25 wide_tc_kernel 3 python tools/prof_target.py w25
+cap w16 wide_tc_kernel 3 python tools/prof_target.py w16
 cap c3bsr bsr_kernel 5 python tools/bsr_bench.py 20000 5 0.5 4
 cap c3bsrslab bsr_slab 5 python tools/bsr_bench.py 20000 5 0.9 4
 python bench.py > $O/bench_$R.log 2>&1
