@@ -1,15 +1,18 @@
-// wide.cu — the A.X pass + fused epilogue for wide blocks, d in {11, ..., 16, 20, 24, 25, 32}
+// wide.cu — the two fallback A.X passes for wide blocks, d in {11, ..., 16, 20, 24, 25, 32}
 // (the paper's experiments use d = 25; §8(b) asks for d <= 16).
+// The DEFAULT wide pass is wide_tc.cu (tcgen05, NSRGS_WIDE_MMA=2 / unset); the passes here are
+// selected with NSRGS_WIDE_MMA=1 / 0 and kept as independent implementations for the variant
+// parity tests (tests/test_gpu_parity.py::test_wide_pass_variants) and as A/B baselines.
 //
 // With d > 10 the narrow kernel's register tile (RT rows x d accumulators per lane) no longer
 // fits, so a consumer warp owns ONE node (d rows of A).  4 consumer warps + 1 TMA producer warp
 // per CTA, one CTA per row panel (4 nodes), the same mbarrier ring, tensor map and per-node
 // epilogue (epilogue.cuh) as the narrow kernel.  Two inner products:
 //
-//  * MMA = true (DEFAULT, the runtime's `wide_mma`): 3xTF32 on the tensor cores with legacy
-//    mma.sync m16n8k8 — A fragments read from the stage through the 128-byte TMA swizzle (so the
-//    runtime's tensor map MUST be encoded with CU_TENSOR_MAP_SWIZZLE_128B whenever this variant
-//    runs: build_tmap couples the two through ctx->wide_mma), X fragments from the row-major
+//  * MMA = true (NSRGS_WIDE_MMA=1): 3xTF32 on the tensor cores with legacy mma.sync m16n8k8 — A
+//    fragments read from the stage through the 128-byte TMA swizzle (so the runtime's tensor map
+//    MUST be encoded with CU_TENSOR_MAP_SWIZZLE_128B whenever a tensor-core variant runs:
+//    build_tmap couples the two through ctx->wide_mma != 0), X fragments from the row-major
 //    32 x d slab, hi/lo splits on the fly, and the MMA accumulator drained into a CUDA-core fp32
 //    sum after every 32-column tile (the tensor core's fp32 accumulation does not round to
 //    nearest; bounding each chain to one tile keeps the step error at <= 3.1e-7, below the
@@ -18,8 +21,9 @@
 //    acc[r] += A[r][c] X[c][k] with A row pieces as 128-bit smem broadcasts and FFMA2 on column
 //    pairs (even / odd partial sums).
 //
-// Measured (same box, mean pass): the MMA variant is 1.07-1.21x faster at d = 25
-// and 1.46-1.76x at d = 16; both are latency / issue bound (2.1-3.5 TB/s), not HBM-bound.
+// Measured on B200 (same box, mean pass of a 20-iteration run, profiles/r02_wide_ab.log): d = 25,
+// n = 4000: 19.1 ms (mma.sync) vs 7.6 ms (tcgen05); d = 16, n = 8000: 19.2 vs 10.5 ms; the
+// CUDA-core pass is another 1.07-1.9x slower than mma.sync (profiles/r01c_wide_variants.txt).
 #include <cuda.h>
 
 #include "common.cuh"

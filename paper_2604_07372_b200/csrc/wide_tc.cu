@@ -309,13 +309,17 @@ __global__ void __launch_bounds__(TcCfg<D, MH>::THREADS, 1)
           for (int h = 0; h < MH; ++h) {
             const uint32_t dmain = tmem + C::TM_MAIN + (uint32_t)(h * 2 + b) * NP;
             const uint32_t ahi = tmem + C::TM_A + (uint32_t)(ob * MH + h) * 64u, alo = ahi + 32u;
+            // all three A operands come from TMEM.  Order: the two small terms (2^-11 of the
+            // product) first, A.X_hi last — every accumulation truncates toward zero at the
+            // accumulator's magnitude, so only the last 4 of the 12 MMAs of a tile lose an ulp of
+            // the full partial sum (measured bias of <X, A X>, n 1100, d 16: 5.1e-7 interleaved)
 #pragma unroll
-            for (int ks = 0; ks < C::CW / 8; ++ks) {   // all three A operands come from TMEM
-              const uint64_t dxh = umma_sdesc(xh + ks * 32), dxl = umma_sdesc(xl + ks * 32);
-              umma_ts(dmain, alo + ks * 8, dxh, idesc, !(pfirst && ks == 0));
-              umma_ts(dmain, ahi + ks * 8, dxl, idesc, 1u);
-              umma_ts(dmain, ahi + ks * 8, dxh, idesc, 1u);
-            }
+            for (int ks = 0; ks < C::CW / 8; ++ks)
+              umma_ts(dmain, alo + ks * 8, umma_sdesc(xh + ks * 32), idesc, !(pfirst && ks == 0));
+#pragma unroll
+            for (int ks = 0; ks < C::CW / 8; ++ks) umma_ts(dmain, ahi + ks * 8, umma_sdesc(xl + ks * 32), idesc, 1u);
+#pragma unroll
+            for (int ks = 0; ks < C::CW / 8; ++ks) umma_ts(dmain, ahi + ks * 8, umma_sdesc(xh + ks * 32), idesc, 1u);
           }
           umma_commit(&bfree[ob]);
           if (j % DP == DP - 1 || t == t1 - 1) {
