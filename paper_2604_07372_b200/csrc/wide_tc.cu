@@ -176,14 +176,12 @@ __device__ __forceinline__ void mbar_wait_spin(uint64_t *bar, uint32_t parity) {
       "@!P1 bra WAITS_%=;\n\t}" ::"r"(addr), "r"(parity)
       : "memory");
 }
+template <bool SPIN = true>
 __device__ __forceinline__ void mbar_wait_t(uint64_t *bar, uint32_t parity, bool timed, long long &acc) {
-  if (timed) {
-    const long long t = clock64();
-    mbar_wait_spin(bar, parity);
-    acc += clock64() - t;
-  } else {
-    mbar_wait_spin(bar, parity);
-  }
+  const long long t = timed ? clock64() : 0;
+  if constexpr (SPIN) mbar_wait_spin(bar, parity);
+  else mbar_wait(bar, parity);   // suspended wait (common.cuh)
+  if (timed) acc += clock64() - t;
 }
 constexpr int kTcGroup = 12;   // CTAs per first-level group of the final partial-sum reduction
 
@@ -273,7 +271,7 @@ __global__ void __launch_bounds__(TcCfg<D, MH>::THREADS, 1)
           const int g0 = t / tpr;
           const int g = (g0 + p.rank) % p.world, jt = t - g0 * tpr;     // own rank slice first
           const int tt = g * tpr + jt;
-          mbar_wait_t(&empty[stage], phase ^ 1u, timed, tw);
+          mbar_wait_t<false>(&empty[stage], phase ^ 1u, timed, tw);
           uint8_t *sb = smem + stage * C::STAGE_BYTES;
           mbar_arrive_expect_tx(&full[stage], C::A_BYTES + C::X_BYTES);
           tma_load_3d(sb, &tmA, &full[stage], jt * C::CW, g, panel * C::ROWS, pol_a);
@@ -289,42 +287,46 @@ __global__ void __launch_bounds__(TcCfg<D, MH>::THREADS, 1)
   } else if (warp == 13) {   // --------------------------------------------------- MMA issuer
     if (elect_one()) {
       constexpr uint32_t idesc = umma_idesc_tf32(NP);
-      unsigned i = 0, pc = 0;
+      // descriptor of X^T buffer 0, K-step 0; every other one is this + a constant: the start
+      // address field counts 16-byte units and cannot carry out of its 14 bits (smem < 256 KB),
+      // so the per-tile uniform-datapath work is a handful of adds, not 16 descriptor builds
+      const uint64_t dx0 = umma_sdesc(smem_u32(xbuf));
+      unsigned pc = 0, ob = 0, ophase = 0;
       long long tw_in = 0, tw_acc = 0;
       const long long tb = timed ? clock64() : 0;
       while (rng.next(panel, t0, t1)) {
-        int b = 0;
-        for (int t = t0; t < t1; ++t, ++i) {
-          const int j = t - t0;
-          const bool pfirst = j % DP == 0;
-          const unsigned ob = i % C::NXB;
-          mbar_wait_t(&split_full[ob], (i / C::NXB) & 1u, timed, tw_in);
+        int b = 0, jp = 0;   // jp: tile index within the drain period
+        for (int t = t0; t < t1; ++t) {
+          const bool pfirst = jp == 0;
+          mbar_wait_t(&split_full[ob], ophase, timed, tw_in);
           if (pfirst) {
             b = (int)(pc & 1u);
             mbar_wait_t(&acc_free[b], ((pc >> 1) & 1u) ^ 1u, timed, tw_acc);
           }
           tc_fence_after();
-          const uint32_t xh = smem_u32(xbuf + ob * C::XBUF_BYTES), xl = xh + C::XT_BYTES;
+          const uint64_t dxh = dx0 + (uint64_t)(ob * (C::XBUF_BYTES >> 4)), dxl = dxh + (C::XT_BYTES >> 4);
+          const uint32_t abase = tmem + C::TM_A + ob * (MH * 64u);
 #pragma unroll
           for (int h = 0; h < MH; ++h) {
             const uint32_t dmain = tmem + C::TM_MAIN + (uint32_t)(h * 2 + b) * NP;
-            const uint32_t ahi = tmem + C::TM_A + (uint32_t)(ob * MH + h) * 64u, alo = ahi + 32u;
+            const uint32_t ahi = abase + (uint32_t)h * 64u, alo = ahi + 32u;
             // all three A operands come from TMEM.  Order: the two small terms (2^-11 of the
             // product) first, A.X_hi last — every accumulation truncates toward zero at the
             // accumulator's magnitude, so only the last 4 of the 12 MMAs of a tile lose an ulp of
             // the full partial sum (measured bias of <X, A X>, n 1100, d 16: 5.1e-7 interleaved)
 #pragma unroll
-            for (int ks = 0; ks < C::CW / 8; ++ks)
-              umma_ts(dmain, alo + ks * 8, umma_sdesc(xh + ks * 32), idesc, !(pfirst && ks == 0));
+            for (int ks = 0; ks < C::CW / 8; ++ks) umma_ts(dmain, alo + ks * 8, dxh + 2 * ks, idesc, !(pfirst && ks == 0));
 #pragma unroll
-            for (int ks = 0; ks < C::CW / 8; ++ks) umma_ts(dmain, ahi + ks * 8, umma_sdesc(xl + ks * 32), idesc, 1u);
+            for (int ks = 0; ks < C::CW / 8; ++ks) umma_ts(dmain, ahi + ks * 8, dxl + 2 * ks, idesc, 1u);
 #pragma unroll
-            for (int ks = 0; ks < C::CW / 8; ++ks) umma_ts(dmain, ahi + ks * 8, umma_sdesc(xh + ks * 32), idesc, 1u);
+            for (int ks = 0; ks < C::CW / 8; ++ks) umma_ts(dmain, ahi + ks * 8, dxh + 2 * ks, idesc, 1u);
           }
           umma_commit(&bfree[ob]);
-          if (j % DP == DP - 1 || t == t1 - 1) {
+          if (++ob == C::NXB) { ob = 0; ophase ^= 1u; }
+          if (++jp == DP || t == t1 - 1) {
             umma_commit(&acc_full[b]);
             ++pc;
+            jp = 0;
           }
         }
       }
@@ -348,9 +350,22 @@ __global__ void __launch_bounds__(TcCfg<D, MH>::THREADS, 1)
         const int stage = (int)(i % C::STAGES);
         const uint32_t phase = (i / C::STAGES) & 1u;
         mbar_wait_t(&full[stage], phase, timed, tw_full);
+        const uint8_t *sb = smem + stage * C::STAGE_BYTES;
+        // the X slab (32 columns x d, row-major) of the stage into registers first
+        const float *Xs = reinterpret_cast<const float *>(sb + C::A_BYTES);
+        constexpr int NI = (D & 1) ? (D + 3) / 4 : C::CW / 4;
+        float xv[NI];
+#pragma unroll
+        for (int it = 0; it < NI; ++it) {
+          if constexpr (D & 1) {   // lane = column k: stride-d reads are conflict-free for odd d
+            const int n = wq + 4 * it;
+            xv[it] = n < D ? Xs[lane * D + n] : 0.f;
+          } else {                 // lane = component n: contiguous reads
+            xv[it] = lane < D ? Xs[(wq + 4 * it) * D + lane] : 0.f;
+          }
+        }
         mbar_wait_t(&bfree[xb], ((i / C::NXB) & 1u) ^ 1u, timed, tw_x);   // MMAs of tile i - NXB are done
         tc_fence_after();
-        const uint8_t *sb = smem + stage * C::STAGE_BYTES;
         // A (raw = hi) and A_lo row by row into TMEM (thread = row; the swizzle makes the 8
         // LDS.128 conflict-free): the MMA reads both as TMEM A operands, never from smem
 #pragma unroll
@@ -374,23 +389,27 @@ __global__ void __launch_bounds__(TcCfg<D, MH>::THREADS, 1)
             tmem_st16(ta + 32u + 16u * c16, wl);
           }
         }
-        // X slab (32 columns x d, row-major) -> K-major swizzled X^T (raw = hi) and X^T_lo
-        const float *Xs = reinterpret_cast<const float *>(sb + C::A_BYTES);
+        // every read of the stage has completed (its values fed the stores above): the stage is only
+        // a TMA landing buffer, so it goes back to the producer now, not after the fences below
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[stage]);
+        // X^T (raw = hi) and X^T_lo as K-major swizzled tiles (4-way conflicting stores for even d)
         uint8_t *XH = xbuf + xb * C::XBUF_BYTES, *XL = XH + C::XT_BYTES;
-        if constexpr (D & 1) {   // lane = column k: stride-d reads are conflict-free for odd d
-          for (int n = wq; n < D; n += 4) {
-            const float x = Xs[lane * D + n];
-            const uint32_t off = (uint32_t)n * 128u + ((uint32_t)((lane >> 2) ^ (n & 7)) << 4) + (uint32_t)(lane & 3) * 4u;
-            *reinterpret_cast<float *>(XH + off) = x;
-            *reinterpret_cast<float *>(XL + off) = tf32_lo(x);
-          }
-        } else {                 // lane = component n: contiguous reads, 4-way conflicting stores
-          for (int k = wq; k < C::CW; k += 4) {
+#pragma unroll
+        for (int it = 0; it < NI; ++it) {
+          if constexpr (D & 1) {
+            const int n = wq + 4 * it;
+            if (n < D) {
+              const uint32_t off = (uint32_t)n * 128u + ((uint32_t)((lane >> 2) ^ (n & 7)) << 4) + (uint32_t)(lane & 3) * 4u;
+              *reinterpret_cast<float *>(XH + off) = xv[it];
+              *reinterpret_cast<float *>(XL + off) = tf32_lo(xv[it]);
+            }
+          } else {
+            const int k = wq + 4 * it;
             if (lane < D) {
-              const float x = Xs[k * D + lane];
               const uint32_t off = (uint32_t)lane * 128u + ((uint32_t)((k >> 2) ^ (lane & 7)) << 4) + (uint32_t)(k & 3) * 4u;
-              *reinterpret_cast<float *>(XH + off) = x;
-              *reinterpret_cast<float *>(XL + off) = tf32_lo(x);
+              *reinterpret_cast<float *>(XH + off) = xv[it];
+              *reinterpret_cast<float *>(XL + off) = tf32_lo(xv[it]);
             }
           }
         }
@@ -398,10 +417,7 @@ __global__ void __launch_bounds__(TcCfg<D, MH>::THREADS, 1)
         fence_proxy_async_smem();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) {
-          mbar_arrive(&split_full[xb]);
-          mbar_arrive(&empty[stage]);   // the stage is only a TMA landing buffer: free once it is read
-        }
+        if (lane == 0) mbar_arrive(&split_full[xb]);
       }
     }
     if (timed && threadIdx.x == 0) {
@@ -459,7 +475,7 @@ __global__ void __launch_bounds__(TcCfg<D, MH>::THREADS, 1)
       const int nper = (t1 - t0 + DP - 1) / DP;
       for (int per = 0; per < nper; ++per, ++pc) {
         const int b = (int)(pc & 1u);
-        mbar_wait_t(&acc_full[b], (pc >> 1) & 1u, timed, t_wait);
+        mbar_wait_t<false>(&acc_full[b], (pc >> 1) & 1u, timed, t_wait);
         tc_fence_after();
 #pragma unroll
         for (int h = 0; h < MH; ++h) {

@@ -42,6 +42,34 @@ __global__ void __launch_bounds__(128, 1) rate(int pattern, int reps, long long 
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tm = tmem_base;
+  // patterns >= 13: pattern - 13 issued by warp 0 while warps 1..3 keep TMEM busy with the split /
+  // drain traffic of wide_tc.cu (per rep and warp: 4 x STTM.x16 + 1 x LDTM.x32 + waits)
+  const int traffic = pattern >= 13;
+  if (traffic) pattern -= 2;   // 13 -> 11 (all-TS sequence), 14 -> 12 (all-TS stacked)
+  if (traffic && warp > 0) {
+    uint32_t w[16], v[32];
+    for (int j = 0; j < 16; ++j) w[j] = tid * 16 + j;
+    const uint32_t la = tm + ((uint32_t)(warp * 32) << 16);
+    for (int r = 0; r < reps; ++r) {
+      for (int q = 0; q < 4; ++q)
+        asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"
+                     ::"r"(la + 384u + 16u * q), "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]),
+                       "r"(w[7]), "r"(w[8]), "r"(w[9]), "r"(w[10]), "r"(w[11]), "r"(w[12]), "r"(w[13]), "r"(w[14]), "r"(w[15]) : "memory");
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+                   "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                   "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                   : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                     "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+                     "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
+                     "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
+                     "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+                   : "r"(la + 448u) : "memory");
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      w[r & 15] += v[r & 31];
+    }
+    if (w[3] == 0x12345678u) out[8] = w[5];
+  }
   uint32_t elected = 0;
   if (warp == 0)
     asm volatile("{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.u32 %0, 1, 0, P;\n\t}" : "=r"(elected));
@@ -122,9 +150,10 @@ int main() {
   const char *names[] = {"SS N=32 one accumulator", "SS N=32 four accumulators", "TS N=32 one accumulator",
                          "TS N=32 four accumulators", "SS N=64 one accumulator", "SS N=64 two accumulators",
                          "SS N=128", "SS N=256", "wide_tc stage sequence (24 MMAs)", "stacked stage sequence (16 MMAs)",
-                         "K-outer interleaved sequence (24)", "all-TS sequence (24)", "all-TS stacked sequence (16)"};
+                         "K-outer interleaved sequence (24)", "all-TS sequence (24)", "all-TS stacked sequence (16)",
+                         "all-TS (24) + STTM/LDTM traffic x3 warps", "all-TS stacked (16) + traffic"};
   for (int grid : {1, 148})
-    for (int pat = 0; pat < 13; ++pat) {
+    for (int pat = 0; pat < 15; ++pat) {
       const int reps = 256;
       rate<<<grid, 128, 68 * 1024>>>(pat, reps, out);
       cudaError_t e = cudaDeviceSynchronize();

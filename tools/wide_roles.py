@@ -1,5 +1,5 @@
 """Per-role wait / busy cycles of the tcgen05 wide pass (wide_tc.cu debug counters, one launch).
-Usage: python tools/wide_roles.py n d [K]"""
+Usage: python tools/wide_roles.py n d [K [warm-up iterations]]"""
 import sys
 sys.path.insert(0, '.')
 import numpy as np
@@ -13,6 +13,8 @@ s.reset_stats(True)
 for _ in range(5):
     s.set_X(X); s.step(1.0 / n, K)
 st = s.stats(); us = st['panel_ms_total'] / st['panel_launches'] * 1e3
+if len(sys.argv) > 4:   # sustained: the counters of a launch at power-capped clocks
+    s.run(int(sys.argv[4]), 1.0 / n, K)
 s.set_X(X); s.debug_timestamps(1); s.step(1.0 / n, K); ts = s.debug_timestamps(0)[0].astype(np.float64)
 names = ["producer total", "producer wait empty", "split wait full", "split wait xfree", "split total",
          "mma wait full+split", "mma wait acc/seg free", "mma total", "drain wait acc_full", "drain stream total",
