@@ -486,7 +486,9 @@ def run_gpu(args, cfg):
                    "x_exchange": ("fused P2P NVLink stores from the epilogue" if st.get("p2p") else "NCCL all-gather")
                    if world > 1 else "none (1 GPU)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "peak_kind": peak_kind, "kernel": "panel_kernel (fused A.X + epilogue)",
+                     "traffic": traffic, "peak_kind": peak_kind,
+                     "kernel": ("wide_tc_kernel (tcgen05 kind::tf32 3xTF32, TMEM operands + accumulators, fused epilogue)"
+                                if st.get("wide_tc") == 2 else "panel_kernel (fused A.X + epilogue)"),
                      "bytes_per_launch": bytes_launch, "avg_launch_ms": avg_ms,
                      "frac_of_nominal_8TBs": achieved / 8000.0,
                      "read_stream_gbs_in_run": read_peak,

@@ -172,6 +172,15 @@ struct nsrgs_ctx {
   int wide_drain = 1;    // tcgen05 pass: column tiles per accumulator drain (NSRGS_WIDE_DRAIN)
   unsigned wide_epoch = 0;
   int wide_slot = 0;     // floats per CTA partial-row slot (tcgen05 pass)
+  // d = 10 on the tcgen05 pass (X stays in the narrow tile layout; wide_tc.cu NL): its own launch
+  // shape, tensor map (32-column box, 128-byte swizzle) and partial buffers next to the narrow ones
+  bool narrow_tc = false;
+  PanelShape tc_shape{};
+  int tc_grid = 0, tc_panels = 0;
+  CUtensorMap tmA_tc;
+  unsigned *tc_flags = nullptr, *tc_cnt = nullptr;
+  void *tc_bpart = nullptr;
+  double *tc_part = nullptr;
   double a_fro2 = 0.0;
   // iterate
   void *X[2] = {nullptr, nullptr};   // both inside xblock (one IPC-shareable allocation)
@@ -480,9 +489,10 @@ int build_tmap(nsrgs_ctx *c, CUtensorMap *out = nullptr, int rows = 0) {
   cuuint64_t dims[3] = {c->world == 1 ? (cuuint64_t)c->N : Nr, (cuuint64_t)c->world, (cuuint64_t)c->plan.rows_local};
   cuuint64_t strides[2] = {c->world == 1 ? (cuuint64_t)(c->lda * c->esz) : (cuuint64_t)(Nr * c->esz),
                            (cuuint64_t)(c->lda * c->esz)};
-  cuuint32_t box[3] = {(cuuint32_t)col_tile(c->d), 1u, (cuuint32_t)rows};
+  const bool tcmap = out == &c->tmA_tc;   // d = 10 on the tcgen05 pass: 32-column swizzled boxes
+  cuuint32_t box[3] = {(cuuint32_t)(tcmap ? kWideColTile : col_tile(c->d)), 1u, (cuuint32_t)rows};
   cuuint32_t estr[3] = {1u, 1u, 1u};
-  const bool swz = out == &c->tmA && c->wide_mma != 0;   // the tensor-core wide pass reads swizzled tiles
+  const bool swz = tcmap || (out == &c->tmA && c->wide_mma != 0);   // the tensor-core passes read swizzled tiles
   CUresult r = encode(out, c->dtype == NSRGS_F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64,
                       3, c->A, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                       swz ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -575,6 +585,15 @@ int launch_panel(nsrgs_ctx *c, int mode, const void *Xin, void *Xout, double *re
     sp.N = c->N;
     CUDA_TRY(c, sym_dispatch(c->d, mode, false, nullptr, &c->tmA_sym, &sp, c->sym_grid, c->stream));
     c->kernel_launches++;
+  } else if (c->narrow_tc && iters == 1 && !p2p) {
+    p.drain_tiles = c->wide_drain;
+    p.epoch = ++c->wide_epoch;
+    p.panels = c->tc_panels;
+    p.ucnt = c->tc_flags;
+    p.Bpart = c->tc_bpart;
+    p.cta_part = c->tc_part;
+    p.done_cnt = c->tc_cnt;
+    CUDA_TRY(c, wide_tc_dispatch(c->d, mode, false, nullptr, nullptr, &c->tmA_tc, &p, c->tc_grid, c->stream));
   } else if (c->d > kMaxNarrowD) {
     if (c->wide_mma == 2) {
       p.drain_tiles = c->wide_drain;
@@ -844,7 +863,7 @@ int nsrgs_destroy(nsrgs_ctx *c) {
     c->group = nullptr;
   }
   if (c->group_tmp) cudaFree(c->group_tmp);
-  void *bufs[] = {c->units, c->pinfo, c->ucnt, c->ctl, c->acc, c->ts, c->xblock, c->stage, c->cta_part, c->counters, c->Bpart, c->res, c->red_part, c->small,
+  void *bufs[] = {c->tc_flags, c->tc_cnt, c->tc_bpart, c->tc_part, c->units, c->pinfo, c->ucnt, c->ctl, c->acc, c->ts, c->xblock, c->stage, c->cta_part, c->counters, c->Bpart, c->res, c->red_part, c->small,
                   c->err, c->ns_region, c->rowpart, c->colpart, c->blocks, c->sym_cnt, c->sym_part,
                   c->bsr_xs, c->bsr_part, c->bsr_cnt, c->yprev};
   for (void *b : bufs)
@@ -981,6 +1000,26 @@ int nsrgs_create(const nsrgs_desc *desc, nsrgs_ctx **out) {
   if (ok && c->d > kMaxNarrowD && c->wide_mma == 2)
     ok = alloc((void **)&c->ucnt, sizeof(unsigned) * 2 * (size_t)c->grid) &&   // two partial segments per CTA
          alloc(&c->Bpart, sizeof(float) * 2 * (size_t)c->grid * (size_t)c->wide_slot);
+  {
+    // d = 10 (c4): the CUDA-core pass is FMA co-limited under the power cap; the
+    // tcgen05 pass streams it at the rate of d = 16.  World 1, fp32, dense storage; small
+    // instances keep the cooperative multi-iteration CUDA-core launch (latency-bound there).
+    const char *nt = std::getenv("NSRGS_NARROW_TC");
+    const double a_bytes = (double)c->esz * (double)c->plan.rows_local * (double)c->N;
+    const bool want = nt ? nt[0] == '1' : a_bytes >= 4e9;
+    if (ok && want && c->d == 10 && c->dtype == NSRGS_F32 && c->world == 1 && !c->emulated) {
+      int slot = 0;
+      wide_tc_dispatch(c->d, 0, true, &c->tc_shape, &slot, nullptr, nullptr, 0, nullptr);
+      c->tc_panels = (int)ceil_div(c->plan.rows_local, c->tc_shape.rows);
+      const int64_t U = (int64_t)c->tc_panels * 4 * c->total_tiles;
+      c->tc_grid = (int)std::max<int64_t>(1, std::min<int64_t>(c->sm_count, U / 8));
+      ok = alloc((void **)&c->tc_flags, sizeof(unsigned) * 2 * (size_t)c->tc_grid) &&
+           alloc(&c->tc_bpart, sizeof(float) * 2 * (size_t)c->tc_grid * (size_t)slot) &&
+           alloc((void **)&c->tc_part, sizeof(double) * 2 * (size_t)c->tc_grid * c->tc_shape.npart) &&
+           alloc((void **)&c->tc_cnt, sizeof(unsigned) * 64);
+      c->narrow_tc = ok;
+    }
+  }
   if (!ok) return bail(NSRGS_ERR_OOM, "device allocation failed");
   if (c->d <= kMaxNarrowD && ensure_acc(c, 1)) return bail(NSRGS_ERR_OOM);
   if (ensure_res(c, 128) || ensure_small(c, kSmallOut + 256)) return bail(NSRGS_ERR_OOM);
@@ -1006,7 +1045,7 @@ int nsrgs_create(const nsrgs_desc *desc, nsrgs_ctx **out) {
     int coop = 0;
     cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, c->device);
     const char *env = getenv("NSRGS_NO_COOP");
-    c->coop = coop && c->world == 1 && !c->forced_nccl && c->d <= kMaxNarrowD && !(env && env[0] == '1');
+    c->coop = coop && c->world == 1 && !c->forced_nccl && c->d <= kMaxNarrowD && !c->narrow_tc && !(env && env[0] == '1');
   }
   if (cudaStreamSynchronize(c->stream) != cudaSuccess) return bail(NSRGS_ERR_CUDA);
   *out = c;
@@ -1024,6 +1063,7 @@ int nsrgs_attach_A(nsrgs_ctx *c, const void *A_shard_dev, int64_t lda) {
   c->own_A = false;
   NSRGS_TRY(build_tmap(c));
   if (c->sym) NSRGS_TRY(build_tmap(c, &c->tmA_sym, c->symshape.rows));
+  if (c->narrow_tc) NSRGS_TRY(build_tmap(c, &c->tmA_tc, c->tc_shape.rows));
   int nb = 0;
   NSRGS_TRY(ensure_red(c, 8 * 4096));
   CUDA_TRY(c, launch_sumsq(c->dtype, c->A, c->plan.rows_local, c->N, c->lda, c->red_part, &nb, c->stream));
@@ -1069,6 +1109,7 @@ int nsrgs_generate_observed(nsrgs_ctx *c, uint64_t seed, double sigma, double p_
                                 c->stream));
   NSRGS_TRY(build_tmap(c));
   if (c->sym) NSRGS_TRY(build_tmap(c, &c->tmA_sym, c->symshape.rows));
+  if (c->narrow_tc) NSRGS_TRY(build_tmap(c, &c->tmA_tc, c->tc_shape.rows));
   int s = fro2_finish(c, nb);
   cudaFree(Z64);
   if (s) return s;
@@ -1706,7 +1747,7 @@ int nsrgs_get_stats(nsrgs_ctx *c, nsrgs_stats_t *o) {
   o->bsr_nnzb = c->bsr ? c->bsr_nnzb : 0;
   o->bsr_slab = (c->bsr && c->bsr_lg2g >= 0) ? 1 : 0;
   o->bsr_g4 = (c->bsr && c->bsr_g4) ? 1 : 0;
-  o->wide_tc = (c->d > kMaxNarrowD && !c->bsr) ? c->wide_mma : 0;
+  o->wide_tc = (c->d > kMaxNarrowD && !c->bsr) ? c->wide_mma : (c->narrow_tc && !c->bsr && !c->sym) ? 2 : 0;
   o->p2p = c->p2p ? 1 : 0;
   return NSRGS_OK;
 }

@@ -201,10 +201,13 @@ struct TcRange {
 };
 __device__ __forceinline__ int64_t tc_start(int64_t U, int c, int G) { return U * c / G; }
 
-template <int D, int MODE, int MH>
+// NL: X in the narrow tile layout of d <= 10 (common.cuh tile_index: 128-column tiles of component
+// pair blocks) — the same kernel then serves d = 10 (c4), whose CUDA-core pass is FMA co-limited
+template <int D, int MODE, int MH, bool NL>
 __global__ void __launch_bounds__(TcCfg<D, MH>::THREADS, 1)
     wide_tc_kernel(const __grid_constant__ CUtensorMap tmA, const PanelParams p) {
   using C = TcCfg<D, MH>;
+  static_assert(!NL || (D % 2 == 0 && D <= kMaxNarrowD), "narrow layout: even d <= 10 (pair blocks only)");
   constexpr int NP = C::NP;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = smem_raw + (((smem_u32(smem_raw) + 1023u) & ~1023u) - smem_u32(smem_raw));
@@ -248,7 +251,9 @@ __global__ void __launch_bounds__(TcCfg<D, MH>::THREADS, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const float *Xg = static_cast<const float *>(p.X);
-  const int TT = p.total_tiles, tpr = (int)p.tiles_per_rank, G = (int)gridDim.x;
+  // 32-column tiles: the narrow layout's plan counts 128-column tiles
+  const int TT = NL ? 4 * p.total_tiles : p.total_tiles, tpr = NL ? 4 * (int)p.tiles_per_rank : (int)p.tiles_per_rank;
+  const int G = (int)gridDim.x;
   const int64_t U = (int64_t)p.panels * TT;
   TcRange rng{tc_start(U, (int)blockIdx.x, G), tc_start(U, (int)blockIdx.x + 1, G), TT};
   const int DP = p.drain_tiles > 0 ? p.drain_tiles : 1;
@@ -275,7 +280,14 @@ __global__ void __launch_bounds__(TcCfg<D, MH>::THREADS, 1)
           uint8_t *sb = smem + stage * C::STAGE_BYTES;
           mbar_arrive_expect_tx(&full[stage], C::A_BYTES + C::X_BYTES);
           tma_load_3d(sb, &tmA, &full[stage], jt * C::CW, g, panel * C::ROWS, pol_a);
-          bulk_load(sb + C::A_BYTES, Xg + (int64_t)tt * C::CW * D, C::X_BYTES, &full[stage], pol_x);
+          if constexpr (NL) {   // 32 columns of every component pair block: d/2 runs of 64 floats
+            const float *xt = Xg + (int64_t)(tt >> 2) * (D * kColTile) + (tt & 3) * 64;
+#pragma unroll
+            for (int kp = 0; kp < D / 2; ++kp)
+              bulk_load(sb + C::A_BYTES + kp * 256, xt + kp * 2 * kColTile, 256, &full[stage], pol_x);
+          } else {
+            bulk_load(sb + C::A_BYTES, Xg + (int64_t)tt * C::CW * D, C::X_BYTES, &full[stage], pol_x);
+          }
           if (++stage == C::STAGES) { stage = 0; phase ^= 1u; }
         }
       }
@@ -360,6 +372,8 @@ __global__ void __launch_bounds__(TcCfg<D, MH>::THREADS, 1)
           if constexpr (D & 1) {   // lane = column k: stride-d reads are conflict-free for odd d
             const int n = wq + 4 * it;
             xv[it] = n < D ? Xs[lane * D + n] : 0.f;
+          } else if constexpr (NL) {   // lane = component n of pair block n / 2: (column, pair) interleaved
+            xv[it] = lane < D ? Xs[(lane >> 1) * 64 + 2 * (wq + 4 * it) + (lane & 1)] : 0.f;
           } else {                 // lane = component n: contiguous reads
             xv[it] = lane < D ? Xs[(wq + 4 * it) * D + lane] : 0.f;
           }
@@ -624,10 +638,10 @@ __global__ void __launch_bounds__(TcCfg<D, MH>::THREADS, 1)
   if (warp == 13) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
 }
 
-template <int D, int MODE, int MH>
+template <int D, int MODE, int MH, bool NL = false>
 static cudaError_t tc_launch(const CUtensorMap *tm, const PanelParams &p, int grid, cudaStream_t s) {
   using C = TcCfg<D, MH>;
-  auto kern = wide_tc_kernel<D, MODE, MH>;
+  auto kern = wide_tc_kernel<D, MODE, MH, NL>;
   static bool attr[64] = {};
   {
     const cudaError_t e = set_smem_attr_once(reinterpret_cast<const void *>(kern), C::SMEM, attr);
@@ -641,12 +655,12 @@ static cudaError_t tc_launch(const CUtensorMap *tm, const PanelParams &p, int gr
   return cudaLaunchCooperativeKernel(reinterpret_cast<const void *>(kern), dim3(grid), dim3(C::THREADS), args, C::SMEM, s);
 }
 
-template <int D, int MH>
+template <int D, int MH, bool NL = false>
 static cudaError_t tc_mode(int mode, const CUtensorMap *tm, const PanelParams &p, int grid, cudaStream_t s) {
-  if (mode == kModeRgs) return tc_launch<D, kModeRgs, MH>(tm, p, grid, s);
-  if (mode == kModeObjective) return tc_launch<D, kModeObjective, MH>(tm, p, grid, s);
-  if (mode == kModeGpm) return tc_launch<D, kModeGpm, MH>(tm, p, grid, s);
-  return tc_launch<D, kModeProduct, MH>(tm, p, grid, s);
+  if (mode == kModeRgs) return tc_launch<D, kModeRgs, MH, NL>(tm, p, grid, s);
+  if (mode == kModeObjective) return tc_launch<D, kModeObjective, MH, NL>(tm, p, grid, s);
+  if (mode == kModeGpm) return tc_launch<D, kModeGpm, MH, NL>(tm, p, grid, s);
+  return tc_launch<D, kModeProduct, MH, NL>(tm, p, grid, s);
 }
 
 // shape->nw reports MROWS * NP floats / 1024 (the per-CTA partial slot, for the runtime's allocation)
@@ -663,6 +677,15 @@ cudaError_t wide_tc_dispatch(int d, int mode, bool shape_only, PanelShape *shape
     return tc_mode<DV, 2>(mode, tm, *p, grid, s);                                                  \
   }
   switch (d) {
+    case 10: {   // d = 10 in the narrow X layout (runtime: ctx->narrow_tc)
+      using C = TcCfg<10, 2>;
+      if (shape_only) {
+        *shape = PanelShape{C::ROWS, C::NPP, C::STAGES, C::SMEM, C::NPART, C::THREADS, 4};
+        if (slot_floats) *slot_floats = C::MROWS * C::NP;
+        return cudaSuccess;
+      }
+      return tc_mode<10, 2, true>(mode, tm, *p, grid, s);
+    }
     NSRGS_TC_CASE(11)
     NSRGS_TC_CASE(12)
     NSRGS_TC_CASE(13)

@@ -746,6 +746,45 @@ def test_wide_tc_deterministic_and_drain_periods(nsrgs, monkeypatch, n, d, sigma
         s.close()
 
 
+@pytest.mark.parametrize("n,sigma,K", [(60, 0.8, 6), (333, 0.5, 3), (1500, 0.2 * np.sqrt(1500) / 10, 6)])
+def test_d10_on_tcgen05(nsrgs, monkeypatch, n, sigma, K):
+    """d = 10 (c4's block size) routed through the tcgen05 pass with X in the narrow tile layout
+    (the default for dense fp32 shards >= 4 GB on one GPU; NSRGS_NARROW_TC=1 forces it at any
+    size): step, fused objective, GPM, spectral init and T = 30 iterations against the fp64
+    oracle at the same bars as the CUDA-core pass, and against the CUDA-core pass itself."""
+    d = 10
+    Z = inst.ground_truth(3, n, d)
+    A = inst.measurement_matrix(3, Z, sigma)
+    X = oracle_iterate_near(Z, 0.1, 2).astype(np.float32)
+    Xo, _, _ = ons.step(A, X.astype(np.float64), 1.0 / n, K)
+    fo = ons.objective(A, X.astype(np.float64))
+    out = {}
+    for flag in ("0", "1"):
+        monkeypatch.setenv("NSRGS_NARROW_TC", flag)
+        s = nsrgs.Solver(n, d)
+        s.generate(3, sigma, want_Z=False)
+        assert s.stats()["wide_tc"] == (2 if flag == "1" else 0)
+        s.set_X(X)
+        f = s.step(1.0 / n, K)
+        X1 = s.get_X()
+        assert rel_fro(X1, Xo) <= 1e-6 and max_block_err(X1, Xo) <= 2e-6
+        assert abs(f - fo) <= 2e-6 * fo
+        s.set_X(X)
+        s.gpm_run(1)
+        assert rel_fro(s.get_X(), ons.gpm_step(A, X.astype(np.float64))) <= 1e-6
+        s.init_spectral(3, 200, 1e-6)
+        X0 = s.get_X().astype(np.float64)
+        tr = s.run(30, 1.0 / n, K, trace=True)
+        XT = s.get_X()
+        XTo = ons.run(A, X0, 30, 1.0 / n, K)
+        assert rel_fro(XT, XTo) <= 1e-4 and max_block_err(XT, XTo) <= 1e-4
+        assert abs(tr[0] - ons.objective(A, X0)) <= 2e-6 * tr[0]
+        out[flag] = (X1, XT)
+        s.close()
+    assert rel_fro(out["1"][0], out["0"][0]) <= 1e-6
+    assert rel_mod_rotation(out["1"][1], out["0"][1]) <= 1e-4
+
+
 def test_table1_on_b200(nsrgs):
     """PAPER.md Table 1 (all nine cells, :345-359) with the paper's protocol on the GPU:
     spectral init, T_s = 1, mu = 1/(np), stop at R^t < 1e-8 / MaxIter 100, NS-RGS and GPM."""
