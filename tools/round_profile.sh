@@ -22,14 +22,16 @@ cap() {   # cap <tag> <kernel regex> <skip> <command...>
   rm -f $O/prof_${R}_$tag.ncu-rep
 }
 cap c3 panel_kernel 3 python tools/prof_target.py c3
-cap c4 panel_kernel 3 python tools/prof_target.py c4
+cap c4 wide_tc_kernel 3 python tools/prof_target.py c4
+NSRGS_NARROW_TC=0 cap c4cc panel_kernel 3 python tools/prof_target.py c4
 cap c3sym sym_block 3 python tools/prof_target.py c3 sym
 cap w25 wide_tc_kernel 3 python tools/prof_target.py w25
 cap w16 wide_tc_kernel 3 python tools/prof_target.py w16
 cap c3bsr bsr_kernel 5 python tools/bsr_bench.py 20000 5 0.5 4
 cap c3bsrslab bsr_slab 5 python tools/bsr_bench.py 20000 5 0.9 4
 python bench.py > $O/bench_$R.log 2>&1
-python bench.py --config c4 --no-sym-variant > $O/bench_${R}_c4.log 2>&1
+python bench.py --config c4 --no-sym-variant --side-configs "" > $O/bench_${R}_c4.log 2>&1
+NSRGS_NARROW_TC=0 python bench.py --config c4 --no-sym-variant --no-bsr-variant --no-cpu-baseline --side-configs "" > $O/bench_${R}_c4_cudacore.log 2>&1
 python bench.py --config c2 --no-bsr-variant > $O/bench_${R}_c2.log 2>&1
 python bench.py --impl reference --steps 2 --warmup 1 > $O/bench_${R}_reference.log 2>&1
 L="--steps 1 --warmup 3 --no-sym-variant --no-bsr-variant --no-cpu-baseline --no-read-probe"
