@@ -1,3 +1,5 @@
+"""Bias of the fused fp32 objective (one-sided error of <X, A X>) of the wide-pass variants and
+tcgen05 drain periods vs the fp64 oracle (test infrastructure: imports oracle/).  n 1100, d 16."""
 import os, sys
 sys.path.insert(0, '.')
 import numpy as np
