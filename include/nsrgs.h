@@ -251,7 +251,9 @@ typedef struct {
   int32_t bsr_slab;             /* 1 if the block-sparse pass runs the column-group slab variant  */
   int32_t bsr_g4;               /* 1 if it gathers X records with TMA tile::gather4              */
   int32_t wide_tc;              /* d > 10: 2 if the A.X pass runs 3xTF32 on tcgen05 (default), 1 on
-                                   mma.sync (NSRGS_WIDE_MMA=1), 0 on CUDA cores (=0) or d <= 10  */
+                                   mma.sync (NSRGS_WIDE_MMA=1), 0 on CUDA cores (=0); d = 10: 2 if
+                                   it runs on the tcgen05 pass (dense fp32 shard >= 4 GB at world 1,
+                                   NSRGS_NARROW_TC), else 0; 0 for d < 10                          */
 } nsrgs_stats_t;
 int nsrgs_get_stats(nsrgs_ctx *ctx, nsrgs_stats_t *out);
 int nsrgs_reset_stats(nsrgs_ctx *ctx, int enable_panel_timing);

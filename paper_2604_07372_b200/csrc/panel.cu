@@ -181,7 +181,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   // ------------------------------------------------------------------ producer warp
   if (warp == kWarps) {
-    if (lane == 0) {
+    if (elect_one()) {   // one lane; the TMA instructions issue straight-line (no per-instruction ELECT loop)
       prefetch_tmap(&tmA);
       const uint64_t pol_frac = p.a_keep > 0.f ? policy_keep_fraction(p.a_keep) : policy_evict_first();
       const uint64_t pol_keep = policy_evict_last(), pol_stream = policy_evict_first();

@@ -593,6 +593,7 @@ int launch_panel(nsrgs_ctx *c, int mode, const void *Xin, void *Xout, double *re
     p.Bpart = c->tc_bpart;
     p.cta_part = c->tc_part;
     p.done_cnt = c->tc_cnt;
+    if (c->tc_grid > c->grid) p.ts = nullptr;   // the timestamp buffer is sized for the CUDA-core grid
     CUDA_TRY(c, wide_tc_dispatch(c->d, mode, false, nullptr, nullptr, &c->tmA_tc, &p, c->tc_grid, c->stream));
   } else if (c->d > kMaxNarrowD) {
     if (c->wide_mma == 2) {

@@ -157,14 +157,6 @@ __device__ __forceinline__ void tmem_ld(uint32_t taddr, uint32_t (&v)[NP]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-// one lane of a converged warp; ptxas then emits the uniform-datapath instructions issued under
-// this predicate (UTCHMMA, UTMALDG, UBLKCP, UTCBAR) straight-line — under a `lane == 0` test it
-// wraps each of them in an ELECT loop (measured: 50 instead of 17 cycles per N = 32 MMA)
-__device__ __forceinline__ bool elect_one() {
-  uint32_t e;
-  asm volatile("{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.u32 %0, 1, 0, P;\n\t}" : "=r"(e));
-  return e != 0;
-}
 // try_wait without the long suspend hint of common.cuh's mbar_wait: the handshakes of this
 // pipeline (split -> MMA -> drain) are latency-critical
 __device__ __forceinline__ void mbar_wait_spin(uint64_t *bar, uint32_t parity) {
