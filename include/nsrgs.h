@@ -178,7 +178,11 @@ int nsrgs_init_spectral(nsrgs_ctx *ctx, uint64_t seed, int max_sweeps, double to
  *   G_i = sum_{j!=i}(X_i - A_ij X_j),  F_i = X_i - eta P_{T_{X_i}}(G_i),  X_i <- S(F_i),
  * P_T(G) = (G - X G^T X)/2, S = K steps of Algorithm 1.
  * eta > 0 (paper: mu = 1/n); K >= 0.  objective_before: host, nullable —
- * receives F(X^t) computed from fp64 partials fused into the same A pass. */
+ * receives F(X^t) computed from fp64 partials fused into the same A pass.
+ * Arithmetic of B = A X: fp32 (F32) / fp64 (F64) FMAs on the CUDA cores for d <= 10; for d > 10
+ * (and d = 10 on dense fp32 shards >= 4 GB at world 1) 3xTF32 on the tensor cores with exact
+ * hi/lo splits and the accumulator drained into fp32 sums every column tile: per-step error
+ * vs fp64 <= 3e-7 (same 1e-6 bar as the CUDA-core pass; stats.wide_tc tells which pass ran). */
 int nsrgs_step(nsrgs_ctx *ctx, double eta, int K, double *objective_before);
 
 /* T iterations of nsrgs_step.  objective_trace: host, nullable, length T, receives
