@@ -400,7 +400,7 @@ def run_gpu(args, cfg):
     eff_gbs = passes * a_bytes * args.steps / (ms / 1e3) / 1e9 * world
     # in-run ceiling right after the headline's measurements (same instance resident, same clocks /
     # power state), before the variants and side configs
-    read_peak = _read_stream_gbs(torch, f"cuda:{local}", stream) if not args.no_read_probe else None
+    read_peak = _read_stream_gbs(torch, f"cuda:{local}", stream, reps=10) if not args.no_read_probe else None
     # §8(f) row 1 alongside the headline: the symmetric half-storage pass on the same instance
     sym_variant = None
     if world == 1 and d <= 6 and not args.symmetric and not args.no_sym_variant:
@@ -468,6 +468,8 @@ def run_gpu(args, cfg):
             continue
         side[name] = _side_config(nsrgs, torch, make_solver, name, c, max(1, args.side_steps), 1, barrier,
                                   stream, world, local)
+    if read_peak is not None:   # the ceiling is the best the probe reaches in this run: once more at the end
+        read_peak = max(read_peak, _read_stream_gbs(torch, f"cuda:{local}", stream, reps=10))
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
