@@ -1,15 +1,17 @@
-// wide_tc.cu — the A.X pass + fused epilogue for wide blocks (d in [11, 32], SURVEY §8(f) row 4:
-// the paper's experiments use d = 25) on the 5th-generation tensor cores:
-// tcgen05.mma kind::tf32, 3xTF32, accumulators in TMEM.  Default for d > 10 (NSRGS_WIDE_MMA=2).
+// wide_tc.cu — the A.X pass + fused epilogue on the 5th-generation tensor cores (tcgen05.mma
+// kind::tf32, 3xTF32, operands and accumulators in TMEM) for wide blocks, d in [11, 32] (SURVEY
+// §8(f) row 4: the paper's experiments use d = 25; default, NSRGS_WIDE_MMA=2), and
+// for d = 10 with X in the narrow tile layout (template flag NL: config c4 on large shards).
 //
-// Why tensor cores here and not for d <= 10: at d = 25 the contraction needs 12.5 flop per byte of
+// Why tensor cores here and not for small d: at d = 25 the contraction needs 12.5 flop per byte of
 // A, i.e. 87 TFLOP/s of fp32 at the HBM rate — more than the CUDA cores deliver — so the pass is
-// only HBM-bound on the tensor cores.  fp32 parity (1e-6 per step) is kept by
+// only HBM-bound on the tensor cores (d = 10 is FMA co-limited under the power cap).  fp32 parity
+// (1e-6 per step) is kept by
 //   * 3xTF32: kind::tf32 reads the top 19 bits of an fp32 operand (truncation, pinned by
-//     tools/micro/umma_tf32.cu), so the raw fp32 tile IS the hi part; lo = x - trunc(x) is exact.
-//     A X = A_hi X_hi + A_lo X_hi + A_hi X_lo (+ A_lo X_lo ~ 2^-22, dropped);
+//     tools/micro/umma_tf32.cu), so the raw fp32 value IS the hi part; lo = x - trunc(x) is exact.
+//     A X = A_lo X_hi + A X_lo + A X_hi (+ A_lo X_lo ~ 2^-20, dropped);
 //   * draining: the tensor core's fp32 accumulation does not round to nearest, so one accumulator
-//     over all N columns drifts ∝ N.  The main accumulator (hi·hi + lo·hi) is double
+//     over all N columns drifts ∝ N.  The accumulator of each 128-row half is double
 //     buffered in TMEM and after every `drain` column tiles it is read back (tcgen05.ld) and added
 //     into a CUDA-core fp32 sum (round to nearest) while the MMAs fill the other buffer.
 //
@@ -24,18 +26,19 @@
 //             swizzled X^T_hi / X^T_lo smem tiles (the B operands).  No MMA reads A from shared
 //             memory: measured (tools/micro/umma_rate.cu) an M 128 x N 32 x K 8 kind::tf32 MMA
 //             takes 42 cycles with A in smem (the 4 KB A read is exposed) and 17 from TMEM;
-//   MMA       per operand buffer and 128-row half: 4 K-steps x {A_lo·X_hi, A·X_lo, A·X_hi} into the
-//             half's accumulator; tcgen05.commit releases the operand buffer and (per drain
-//             period) the accumulator buffer.  Issued under elect.sync so the UTCHMMAs are straight-line;
-//   drain     tcgen05.ld of the main buffer -> fp32 sums in registers (thread = panel row); at
+//   MMA       per operand buffer and 128-row half: {A_lo·X_hi, A·X_lo, A·X_hi} x 4 K-steps into the
+//             half's accumulator (small terms first); tcgen05.commit releases the operand buffer
+//             and (per drain period) the accumulator buffer.  Issued under elect.sync so the
+//             UTCHMMAs are straight-line; per-tile descriptors are one base descriptor + constants;
+//   drain     tcgen05.ld of the accumulator -> fp32 sums in registers (thread = panel row); at
 //             the end of a whole panel the node epilogue (epilogue.cuh), 4 nodes at a time.
-// Work: persistent grid; the (panel, column tile) space is cut into equal contiguous ranges
-// (stream-K).  A CTA's first segment may continue a panel (contribution: partial B rows to a
-// per-CTA slot + flag) and its last may start one (head: waits for the later CTAs' slots, which
-// they produced FIRST).  Both kinds of partial segment go to a per-CTA slot + flag; after its
+// Work: persistent grid (one CTA per SM, cooperative launch); the (panel, column tile) space is cut
+// into equal contiguous ranges (stream-K).  A partial segment of a panel — a CTA's first segment
+// may continue a panel, its last may start one — goes to a per-CTA slot + epoch flag; after its
 // range every CTA sharing a split panel takes every np-th node of it, sums that node's partial
 // rows over all sharers' slots in CTA order (deterministic) and runs its epilogue — so at small n
-// (Table 1: 50 panels for 148 SMs) the epilogues are spread over all CTAs.
+// (Table 1: 50 panels for 148 SMs) the epilogues are spread over all CTAs.  Objective / Gram
+// partials: per-CTA slots, reduced in two fixed-order levels by the last CTA of each group.
 #include <cuda.h>
 
 #include "common.cuh"
