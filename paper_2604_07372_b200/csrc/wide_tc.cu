@@ -356,7 +356,7 @@ __global__ void __launch_bounds__(TcCfg<D, MH>::THREADS, 1)
         const unsigned xb = i % C::NXB;
         const int stage = (int)(i % C::STAGES);
         const uint32_t phase = (i / C::STAGES) & 1u;
-        mbar_wait_t(&full[stage], phase, timed, tw_full);
+        mbar_wait_t<false>(&full[stage], phase, timed, tw_full);   // TMA arrival: suspended wait (A/B neutral vs spinning)
         const uint8_t *sb = smem + stage * C::STAGE_BYTES;
         // the X slab (32 columns x d, row-major) of the stage into registers first
         const float *Xs = reinterpret_cast<const float *>(sb + C::A_BYTES);
