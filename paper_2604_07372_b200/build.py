@@ -15,7 +15,10 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 OUT = os.path.join(PKG, "libnsrgs.so")
 BUILD = os.path.join(PKG, "_build")
-SOURCES = ["panel.cu", "sym.cu", "wide.cu", "wide_tc.cu", "bsr.cu", "polar.cu", "aux.cu", "objective64.cu", "probe.cu", "runtime.cu"]
+# "file@MACRO=v": the same source compiled once per value (wide_tc.cu: its block sizes are split over
+# four objects, a single nvcc run over all of them takes > 8 minutes)
+SOURCES = ["panel.cu", "sym.cu", "wide.cu", "wide_tc.cu@NSRGS_TC_PART=0", "wide_tc.cu@NSRGS_TC_PART=1",
+           "wide_tc.cu@NSRGS_TC_PART=2", "wide_tc.cu@NSRGS_TC_PART=3", "bsr.cu", "polar.cu", "aux.cu", "objective64.cu", "probe.cu", "runtime.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "--expt-relaxed-constexpr",
          "-I" + os.path.join(ROOT, "include"), "-I" + CSRC]
@@ -53,11 +56,12 @@ def build(verbose: bool = False, force: bool = False, ptxas_v: bool = False) -> 
     nvcc = _nvcc()
     os.makedirs(BUILD, exist_ok=True)
     jobs = []
-    for src in SOURCES:
+    for item in SOURCES:
+        src, _, macro = item.partition("@")
         s = os.path.join(CSRC, src)
-        o = os.path.join(BUILD, src + ".o")
+        o = os.path.join(BUILD, item.replace("@", ".").replace("=", "_") + ".o")
         if force or _stale(o, [s] + sorted(_includes(s))):
-            cmd = [nvcc, *ARCH, *FLAGS, "-c", s, "-o", o]
+            cmd = [nvcc, *ARCH, *FLAGS, *(["-D" + macro] if macro else []), "-c", s, "-o", o]
             if ptxas_v:
                 cmd += ["-Xptxas", "-v"]
             jobs.append(cmd)
@@ -72,7 +76,7 @@ def build(verbose: bool = False, force: bool = False, ptxas_v: bool = False) -> 
                 sys.stderr.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)
             if r.returncode != 0:
                 raise RuntimeError(f"nvcc failed for {cmd[-3]}")
-    objs = [os.path.join(BUILD, s + ".o") for s in SOURCES]
+    objs = [os.path.join(BUILD, s.replace("@", ".").replace("=", "_") + ".o") for s in SOURCES]
     if force or jobs or _stale(OUT, objs):
         cmd = [nvcc, *ARCH, "-shared", "-o", OUT, *objs, "-ldl"]
         r = subprocess.run(cmd, capture_output=True, text=True)

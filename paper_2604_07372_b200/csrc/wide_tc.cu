@@ -658,42 +658,78 @@ static cudaError_t tc_mode(int mode, const CUtensorMap *tm, const PanelParams &p
   return tc_launch<D, kModeProduct, MH, NL>(tm, p, grid, s);
 }
 
-// shape->nw reports MROWS * NP floats / 1024 (the per-CTA partial slot, for the runtime's allocation)
-cudaError_t wide_tc_dispatch(int d, int mode, bool shape_only, PanelShape *shape, int *slot_floats,
-                             const CUtensorMap *tm, const PanelParams *p, int grid, cudaStream_t s) {
+// The block sizes are instantiated in four translation units (NSRGS_TC_PART = 0..3, balanced by
+// compile time: one nvcc run over all of them takes > 8 minutes); part 0 also holds the dispatcher.
+#ifndef NSRGS_TC_PART
+#define NSRGS_TC_PART 0
+#endif
 #define NSRGS_TC_CASE(DV)                                                                          \
   case DV: {                                                                                       \
     using C = TcCfg<DV, 2>;                                                                        \
     if (shape_only) {                                                                              \
       *shape = PanelShape{C::ROWS, C::NPP, C::STAGES, C::SMEM, C::NPART, C::THREADS, 4};          \
       if (slot_floats) *slot_floats = C::MROWS * C::NP;                                            \
-      return cudaSuccess;                                                                          \
+      *err = cudaSuccess;                                                                          \
+      return true;                                                                                 \
     }                                                                                              \
-    return tc_mode<DV, 2>(mode, tm, *p, grid, s);                                                  \
+    *err = tc_mode<DV, 2>(mode, tm, *p, grid, s);                                                  \
+    return true;                                                                                   \
   }
+#define NSRGS_TC_PART_FN(K) wide_tc_part##K
+#define NSRGS_TC_PART_NAME(K) NSRGS_TC_PART_FN(K)
+
+// true if this part instantiates block size d (then *err is the shape query's / launch's status)
+bool NSRGS_TC_PART_NAME(NSRGS_TC_PART)(int d, int mode, bool shape_only, PanelShape *shape, int *slot_floats,
+                                       const CUtensorMap *tm, const PanelParams *p, int grid, cudaStream_t s,
+                                       cudaError_t *err) {
   switch (d) {
+#if NSRGS_TC_PART == 0
     case 10: {   // d = 10 in the narrow X layout (runtime: ctx->narrow_tc)
       using C = TcCfg<10, 2>;
       if (shape_only) {
         *shape = PanelShape{C::ROWS, C::NPP, C::STAGES, C::SMEM, C::NPART, C::THREADS, 4};
         if (slot_floats) *slot_floats = C::MROWS * C::NP;
-        return cudaSuccess;
+        *err = cudaSuccess;
+        return true;
       }
-      return tc_mode<10, 2, true>(mode, tm, *p, grid, s);
+      *err = tc_mode<10, 2, true>(mode, tm, *p, grid, s);
+      return true;
     }
     NSRGS_TC_CASE(11)
     NSRGS_TC_CASE(12)
     NSRGS_TC_CASE(13)
     NSRGS_TC_CASE(14)
     NSRGS_TC_CASE(15)
+#elif NSRGS_TC_PART == 1
     NSRGS_TC_CASE(16)
+    NSRGS_TC_CASE(25)
+#elif NSRGS_TC_PART == 2
     NSRGS_TC_CASE(20)
     NSRGS_TC_CASE(24)
-    NSRGS_TC_CASE(25)
+#else
     NSRGS_TC_CASE(32)
-    default: return cudaErrorInvalidValue;
+#endif
+    default: return false;
   }
-#undef NSRGS_TC_CASE
 }
+#undef NSRGS_TC_CASE
+
+#if NSRGS_TC_PART == 0
+bool wide_tc_part1(int, int, bool, PanelShape *, int *, const CUtensorMap *, const PanelParams *, int, cudaStream_t, cudaError_t *);
+bool wide_tc_part2(int, int, bool, PanelShape *, int *, const CUtensorMap *, const PanelParams *, int, cudaStream_t, cudaError_t *);
+bool wide_tc_part3(int, int, bool, PanelShape *, int *, const CUtensorMap *, const PanelParams *, int, cudaStream_t, cudaError_t *);
+
+// slot_floats: floats of one CTA's partial-row slot (the runtime allocates 2 slots + 2 flags per CTA)
+cudaError_t wide_tc_dispatch(int d, int mode, bool shape_only, PanelShape *shape, int *slot_floats,
+                             const CUtensorMap *tm, const PanelParams *p, int grid, cudaStream_t s) {
+  cudaError_t err = cudaErrorInvalidValue;
+  if (wide_tc_part0(d, mode, shape_only, shape, slot_floats, tm, p, grid, s, &err) ||
+      wide_tc_part1(d, mode, shape_only, shape, slot_floats, tm, p, grid, s, &err) ||
+      wide_tc_part2(d, mode, shape_only, shape, slot_floats, tm, p, grid, s, &err) ||
+      wide_tc_part3(d, mode, shape_only, shape, slot_floats, tm, p, grid, s, &err))
+    return err;
+  return cudaErrorInvalidValue;
+}
+#endif
 
 }  // namespace nsrgs
